@@ -1,0 +1,388 @@
+/*
+ * oracle.c -- plain, slow, obviously-correct CPU oracle for the permanent.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference leg may load or call this
+ * library.  It shares no code, header, table or constant with the CUDA path
+ * under paper_1904_06229_b200/ and neither side includes the other.
+ *
+ * Arithmetic: __float128 (IEEE binary128) for complex matrices, unsigned
+ * __int128 (arithmetic mod 2^128) for 0-1 matrices.  Inputs are the same
+ * bytes the GPU reads: row-major n x n, entry (i,j) = A[2*(i*n+j)] + i*A[2*(i*n+j)+1].
+ * Results are returned as (hi, lo) double pairs so that the ~113-bit quad
+ * value survives the trip back to Python: value = hi + lo.
+ *
+ * Citations: "P:<line>" is a line of the paper text (PAPER.md, arXiv
+ * 1904.06229, Lundow & Markstrom) together with the equation/algorithm it is in.
+ *
+ * Functions and what pins them:
+ *   oracle_naive_c128     Eq. (1), P:56-59            brute force; pinned by hand values,
+ *                                                       per(J_n)=n!, D_n, diag, P7/P8 identities
+ *   oracle_ryser_c128     Eq. (3), P:121-130          pinned against naive (n<=9) and closed forms
+ *   oracle_subpermanent   App. A subpermanent, P:1131-1151 (steps 2-15 for a given (r, l))
+ *   oracle_permanent_hr   App. A permanent, P:1153-1163 (distribute + subpermanent + combine)
+ *   oracle_range_c128     App. A terms recomputed from steps 5-8 per rank (no walk)
+ *   oracle_seed_c128      App. A steps 2,5-8: w(r)
+ *   oracle_naive_i01 / oracle_ryser_i01   Eq. (1) / Eq. (3) in exact integers
+ *   oracle_distribute, oracle_gray        App. A distribute P:1077-1095, Gray unrank P:1097-1106
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#include <omp.h>
+
+typedef __float128 quad;
+typedef struct { quad re, im; } qc;            /* complex binary128 */
+typedef unsigned __int128 u128;
+
+static inline qc qc_add(qc a, qc b) { qc r = { a.re + b.re, a.im + b.im }; return r; }
+static inline qc qc_sub(qc a, qc b) { qc r = { a.re - b.re, a.im - b.im }; return r; }
+static inline qc qc_mul(qc a, qc b) {
+    qc r = { a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re };
+    return r;
+}
+static inline qc qc_scale(qc a, quad s) { qc r = { a.re * s, a.im * s }; return r; }
+static inline qc entry(const double* A, int n, int i, int j) {
+    qc r = { (quad)A[2 * ((size_t)i * n + j)], (quad)A[2 * ((size_t)i * n + j) + 1] };
+    return r;
+}
+static void put_q(double* out, quad q) {           /* (hi, lo) with hi + lo == q to ~106 bits */
+    double hi = (double)q;
+    out[0] = hi;
+    out[1] = (double)(q - (quad)hi);
+}
+static void put_qc(double* out, qc v) { put_q(out, v.re); put_q(out + 2, v.im); }
+
+/* ---------------- App. A integer helpers ---------------- */
+
+/* distribute(n, m, i, k, l): q = floor(n/m), r = n mod m,
+ * k = i*q + min(i, r), l = q + I(i < r). */
+void oracle_distribute(uint64_t n, uint64_t m, uint64_t i, uint64_t* k, uint64_t* l) {
+    uint64_t q = n / m, r = n % m;
+    *k = i * q + (i < r ? i : r);
+    *l = q + (i < r ? 1 : 0);
+}
+
+/* x := xor(k, rshift(k)) */
+uint64_t oracle_gray(uint64_t k) { return k ^ (k >> 1); }
+
+/* ---------------- Eq. (1): the definition ---------------- */
+
+/* Sum over all n! permutations (Heap's algorithm enumerates them), each term the
+ * plain product prod_i a_{i,pi(i)}.  n <= 10. */
+int oracle_naive_c128(const double* A, int n, double* out4) {
+    if (n < 1 || n > 10) return 1;
+    int perm[10], c[10];
+    for (int i = 0; i < n; i++) { perm[i] = i; c[i] = 0; }
+    qc total = { 0, 0 };
+    for (;;) {
+        qc p = { 1, 0 };
+        for (int i = 0; i < n; i++) p = qc_mul(p, entry(A, n, i, perm[i]));
+        total = qc_add(total, p);
+        /* Heap's algorithm, iterative form: next permutation */
+        int i = 1;
+        while (i < n && c[i] >= i) { c[i] = 0; i++; }
+        if (i >= n) break;
+        int s = (i % 2 == 0) ? 0 : c[i];
+        int tmp = perm[s]; perm[s] = perm[i]; perm[i] = tmp;
+        c[i]++;
+    }
+    put_qc(out4, total);
+    return 0;
+}
+
+/* Eq. (1) for a 0-1 (uint8) matrix in exact integers. */
+int oracle_naive_i01(const uint8_t* A, int n, uint64_t* out2) {
+    if (n < 1 || n > 12) return 1;
+    int perm[12], c[12];
+    for (int i = 0; i < n; i++) { perm[i] = i; c[i] = 0; }
+    u128 total = 0;
+    for (;;) {
+        u128 p = 1;
+        for (int i = 0; i < n; i++) p *= (u128)A[(size_t)i * n + perm[i]];
+        total += p;
+        int i = 1;
+        while (i < n && c[i] >= i) { c[i] = 0; i++; }
+        if (i >= n) break;
+        int s = (i % 2 == 0) ? 0 : c[i];
+        int tmp = perm[s]; perm[s] = perm[i]; perm[i] = tmp;
+        c[i]++;
+    }
+    out2[0] = (uint64_t)total;
+    out2[1] = (uint64_t)(total >> 64);
+    return 0;
+}
+
+/* ---------------- Eq. (3): Ryser, full range ----------------
+ * per(A) = (-1)^n sum_{J subset N} (-1)^{|J|} prod_i sum_{j in J} a_ij.
+ * The subsets J are visited in Gray-code order: J(r) = gray(r),
+ * r = 0 .. 2^n - 1, and the row sums are updated by the one column whose
+ * membership changed.  The 2^n ranks are split into m contiguous parts with
+ * distribute; each part seeds its row sums from the definition
+ * sum_{j in J} a_ij and the m partial sums are added in index order. */
+static qc ryser_part(const double* A, int n, uint64_t k0, uint64_t len) {
+    qc rs[64];
+    qc S = { 0, 0 };
+    uint64_t x = oracle_gray(k0);
+    for (int i = 0; i < n; i++) {
+        rs[i].re = 0; rs[i].im = 0;
+        for (int j = 0; j < n; j++)
+            if ((x >> j) & 1) rs[i] = qc_add(rs[i], entry(A, n, i, j));
+    }
+    for (uint64_t r = k0; r < k0 + len; r++) {
+        if (r != k0) {
+            uint64_t xn = oracle_gray(r);
+            int j = __builtin_ctzll(xn ^ x);
+            for (int i = 0; i < n; i++)
+                rs[i] = ((xn >> j) & 1) ? qc_add(rs[i], entry(A, n, i, j))
+                                        : qc_sub(rs[i], entry(A, n, i, j));
+            x = xn;
+        }
+        qc p = { 1, 0 };
+        for (int i = 0; i < n; i++) p = qc_mul(p, rs[i]);
+        if (__builtin_popcountll(x) & 1) S = qc_sub(S, p); else S = qc_add(S, p);
+    }
+    return S;
+}
+
+int oracle_ryser_c128(const double* A, int n, int m, double* out4) {
+    if (n < 1 || n > 40) return 1;
+    if (m < 1) m = 1;
+    uint64_t total = (uint64_t)1 << n;
+    if ((uint64_t)m > total) m = (int)total;
+    qc* part = (qc*)calloc((size_t)m, sizeof(qc));
+    #pragma omp parallel for schedule(dynamic, 1)
+    for (int k = 0; k < m; k++) {
+        uint64_t k0, len;
+        oracle_distribute(total, (uint64_t)m, (uint64_t)k, &k0, &len);
+        part[k] = ryser_part(A, n, k0, len);
+    }
+    qc S = { 0, 0 };
+    for (int k = 0; k < m; k++) S = qc_add(S, part[k]);
+    free(part);
+    if (n & 1) S = qc_scale(S, -1);
+    put_qc(out4, S);
+    return 0;
+}
+
+/* Eq. (3) in exact integer arithmetic for 0-1 matrices.  Row sums are
+ * non-negative integers; products and the signed sum are taken mod 2^128
+ * (unsigned __int128, two's complement), which is exact as long as
+ * |per| < 2^127, i.e. n <= 33 since per <= n!. */
+static u128 ryser_i01_part(const uint8_t* A, int n, uint64_t k0, uint64_t len) {
+    int64_t rs[64];
+    u128 S = 0;
+    uint64_t x = oracle_gray(k0);
+    for (int i = 0; i < n; i++) {
+        rs[i] = 0;
+        for (int j = 0; j < n; j++)
+            if ((x >> j) & 1) rs[i] += A[(size_t)i * n + j];
+    }
+    for (uint64_t r = k0; r < k0 + len; r++) {
+        if (r != k0) {
+            uint64_t xn = oracle_gray(r);
+            int j = __builtin_ctzll(xn ^ x);
+            for (int i = 0; i < n; i++)
+                rs[i] += ((xn >> j) & 1) ? A[(size_t)i * n + j] : -(int64_t)A[(size_t)i * n + j];
+            x = xn;
+        }
+        u128 p = 1;
+        for (int i = 0; i < n; i++) p *= (u128)(uint64_t)rs[i];
+        if (__builtin_popcountll(x) & 1) S -= p; else S += p;
+    }
+    return S;
+}
+
+int oracle_ryser_i01(const uint8_t* A, int n, int m, uint64_t* out2) {
+    if (n < 1 || n > 33) return 1;
+    if (m < 1) m = 1;
+    uint64_t total = (uint64_t)1 << n;
+    if ((uint64_t)m > total) m = (int)total;
+    u128* part = (u128*)calloc((size_t)m, sizeof(u128));
+    #pragma omp parallel for schedule(dynamic, 1)
+    for (int k = 0; k < m; k++) {
+        uint64_t k0, len;
+        oracle_distribute(total, (uint64_t)m, (uint64_t)k, &k0, &len);
+        part[k] = ryser_i01_part(A, n, k0, len);
+    }
+    u128 S = 0;
+    for (int k = 0; k < m; k++) S += part[k];
+    free(part);
+    if (n & 1) S = (u128)0 - S;
+    out2[0] = (uint64_t)S;
+    out2[1] = (uint64_t)(S >> 64);
+    return 0;
+}
+
+/* Batch of B independent 0-1 matrices, one Eq. (3) evaluation each. */
+int oracle_ryser_i01_batch(const uint8_t* A, int n, int64_t B, uint64_t* out2) {
+    if (n < 1 || n > 33) return 1;
+    int bad = 0;
+    #pragma omp parallel for schedule(dynamic, 1) reduction(|:bad)
+    for (int64_t b = 0; b < B; b++) {
+        u128 S = ryser_i01_part(A + (size_t)b * n * n, n, 0, (uint64_t)1 << n);
+        if (n & 1) S = (u128)0 - S;
+        out2[2 * b] = (uint64_t)S;
+        out2[2 * b + 1] = (uint64_t)(S >> 64);
+    }
+    return bad;
+}
+
+/* Batch of B independent complex matrices, one Eq. (3) evaluation each. */
+int oracle_ryser_c128_batch(const double* A, int n, int64_t B, double* out4) {
+    if (n < 1 || n > 40) return 1;
+    #pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t b = 0; b < B; b++) {
+        qc S = ryser_part(A + (size_t)b * 2 * n * n, n, 0, (uint64_t)1 << n);
+        if (n & 1) S = qc_scale(S, -1);
+        put_qc(out4 + 4 * b, S);
+    }
+    return 0;
+}
+
+/* ---------------- App. A, literally ---------------- */
+
+/* nextset(t, j, x).  x[1..n] (1-indexed as in the paper). */
+static void nextset(int* t, int* j, unsigned char* x) {
+    *j = 1;                                     /* [1] j := 1 */
+    *t = -*t;                                   /* [2] t := -t */
+    if (*t == 1) {                              /* [2] if t = 1 then */
+        while (x[*j] == 0) *j = *j + 1;         /* [3-5] while x_j = 0 do j := j+1 */
+        *j = *j + 1;                            /* [6] j := j+1 */
+    }
+    x[*j] = 1 - x[*j];                          /* [7] x_j := 1 - x_j */
+}
+
+/* subpermanent steps 2-15 for a given start rank r and length l
+ * (step 1, distribute, is done by the caller).  Returns S (no 2(-1)^n factor). */
+static qc subpermanent_rl(const double* A, int n, uint64_t r, uint64_t l) {
+    unsigned char x[66];
+    qc w[64];
+    uint64_t g = oracle_gray(r);                                /* [2] */
+    memset(x, 0, sizeof(x));
+    for (int j = 1; j <= n; j++) x[j] = (unsigned char)((g >> (j - 1)) & 1);
+    int t = (r & 1) ? -1 : 1;                                   /* [3] t := (-1)^r */
+    qc S = { 0, 0 };                                            /* [4] */
+    for (int i = 1; i <= n; i++) {                              /* [5] */
+        qc rowsum = { 0, 0 };
+        for (int j = 1; j <= n; j++) rowsum = qc_add(rowsum, entry(A, n, i - 1, j - 1));
+        w[i - 1] = qc_sub(entry(A, n, i - 1, n - 1), qc_scale(rowsum, (quad)0.5));
+    }
+    for (int j = 1; j <= n - 1; j++)                            /* [6] */
+        if (x[j] == 1)
+            for (int i = 1; i <= n; i++) w[i - 1] = qc_add(w[i - 1], entry(A, n, i - 1, j - 1)); /* [7] */
+    for (uint64_t it = 0; it < l; it++) {                       /* [9] do l times */
+        qc p = { 1, 0 };
+        for (int i = 0; i < n; i++) p = qc_mul(p, w[i]);        /* [10] */
+        int j;
+        nextset(&t, &j, x);                                     /* [11] */
+        S = (t == 1) ? qc_add(S, p) : qc_sub(S, p);             /* [12] S := S + t*p */
+        if (it + 1 == l) break;  /* the trailing update may address column n (C4); it is never used */
+        quad z = (quad)(2 * x[j] - 1);                          /* [13] */
+        for (int i = 0; i < n; i++)                             /* [14] */
+            w[i] = qc_add(w[i], qc_scale(entry(A, n, i, j - 1), z));
+    }
+    return S;
+}
+
+int oracle_subpermanent(const double* A, int n, uint64_t r, uint64_t l, double* out4) {
+    if (n < 1 || n > 64) return 1;
+    put_qc(out4, subpermanent_rl(A, n, r, l));
+    return 0;
+}
+
+/* Same, but the rank range [r, r+l) is cut into `parts` contiguous pieces with
+ * distribute and the pieces run on host threads; partials added in order.
+ * (This is App. A's permanent() loop restricted to a sub-range.) */
+int oracle_subpermanent_par(const double* A, int n, uint64_t r, uint64_t l, int parts, double* out4) {
+    if (n < 1 || n > 64 || parts < 1) return 1;
+    qc* part = (qc*)calloc((size_t)parts, sizeof(qc));
+    #pragma omp parallel for schedule(dynamic, 1)
+    for (int k = 0; k < parts; k++) {
+        uint64_t k0, len;
+        oracle_distribute(l, (uint64_t)parts, (uint64_t)k, &k0, &len);
+        if (len) part[k] = subpermanent_rl(A, n, r + k0, len);
+    }
+    qc S = { 0, 0 };
+    for (int k = 0; k < parts; k++) S = qc_add(S, part[k]);
+    free(part);
+    put_qc(out4, S);
+    return 0;
+}
+
+/* permanent(A, n, m, S): S = 2 (-1)^n sum_k S_k, with S_k from
+ * subpermanent(A, n, m, k) and distribute(2^{n-1}, m, k). */
+int oracle_permanent_hr(const double* A, int n, int m, double* out4) {
+    if (n < 1 || n > 64 || m < 1) return 1;
+    uint64_t total = (uint64_t)1 << (n - 1);
+    qc* part = (qc*)calloc((size_t)m, sizeof(qc));
+    #pragma omp parallel for schedule(dynamic, 1)
+    for (int k = 0; k < m; k++) {
+        uint64_t r, l;
+        oracle_distribute(total, (uint64_t)m, (uint64_t)k, &r, &l);   /* [1] */
+        if (l) part[k] = subpermanent_rl(A, n, r, l);
+    }
+    qc S = { 0, 0 };
+    for (int k = 0; k < m; k++) S = qc_add(S, part[k]);
+    free(part);
+    S = qc_scale(S, (n & 1) ? (quad)-2 : (quad)2);                      /* [4] */
+    put_qc(out4, S);
+    return 0;
+}
+
+/* w(r): App. A steps 2, 5-8 evaluated at rank r.  out: n x (re_hi, re_lo, im_hi, im_lo). */
+int oracle_seed_c128(const double* A, int n, uint64_t r, double* out) {
+    if (n < 1 || n > 64) return 1;
+    uint64_t x = oracle_gray(r);
+    for (int i = 0; i < n; i++) {
+        qc rowsum = { 0, 0 };
+        for (int j = 0; j < n; j++) rowsum = qc_add(rowsum, entry(A, n, i, j));
+        qc w = qc_sub(entry(A, n, i, n - 1), qc_scale(rowsum, (quad)0.5));
+        for (int j = 0; j < n - 1; j++)
+            if ((x >> j) & 1) w = qc_add(w, entry(A, n, i, j));
+        put_qc(out + 4 * i, w);
+    }
+    return 0;
+}
+
+/* P(k0, k1) = sum_{r=k0}^{k1-1} (-1)^{r+1} prod_i w_i(gray(r)): every term is
+ * re-derived from steps 2, 3, 5-8 and 10 of subpermanent (no incremental walk),
+ * so it checks the GPU's seeding, stepping and term signs independently. */
+int oracle_range_c128(const double* A, int n, uint64_t k0, uint64_t k1, double* out4) {
+    if (n < 1 || n > 64 || k1 < k0) return 1;
+    qc base[64];
+    for (int i = 0; i < n; i++) {
+        qc rowsum = { 0, 0 };
+        for (int j = 0; j < n; j++) rowsum = qc_add(rowsum, entry(A, n, i, j));
+        base[i] = qc_sub(entry(A, n, i, n - 1), qc_scale(rowsum, (quad)0.5));
+    }
+    int nt = omp_get_max_threads();
+    qc* part = (qc*)calloc((size_t)nt, sizeof(qc));
+    uint64_t len = k1 - k0;
+    #pragma omp parallel num_threads(nt)
+    {
+        int k = omp_get_thread_num();
+        uint64_t a, l;
+        oracle_distribute(len, (uint64_t)nt, (uint64_t)k, &a, &l);
+        qc S = { 0, 0 };
+        for (uint64_t r = k0 + a; r < k0 + a + l; r++) {
+            uint64_t x = oracle_gray(r);
+            qc p = { 1, 0 };
+            for (int i = 0; i < n; i++) {
+                qc w = base[i];
+                for (int j = 0; j < n - 1; j++)
+                    if ((x >> j) & 1) w = qc_add(w, entry(A, n, i, j));
+                p = qc_mul(p, w);
+            }
+            S = (r & 1) ? qc_add(S, p) : qc_sub(S, p);     /* (-1)^{r+1} */
+        }
+        part[k] = S;
+    }
+    qc S = { 0, 0 };
+    for (int k = 0; k < nt; k++) S = qc_add(S, part[k]);
+    free(part);
+    put_qc(out4, S);
+    return 0;
+}
+
+int oracle_num_threads(void) { return omp_get_max_threads(); }

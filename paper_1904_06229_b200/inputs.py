@@ -1,0 +1,108 @@
+"""Seeded synthetic inputs shaped like the paper's workloads.
+
+This module holds NO permanent arithmetic.  It is the one module that both the
+CUDA path's callers (bench.py, tests) and the oracle's callers draw inputs from,
+so that both sides read identical bytes.  Recipe:
+
+* complex Gaussian entries (g1 + i g2)/sqrt(2), g ~ N(0,1): re, im ~ N(0, 1/2)
+  (Ginibre ensemble);
+* Haar unitary U(m): QR of a complex Gaussian matrix, then U = Q * diag(r_ii/|r_ii|)
+  (P:944-952);
+* Boson-sampling submatrices: distinct rows and distinct columns drawn uniformly,
+  sorted (P:954-958 with m = n^2, i.e. a = 2 of Sec. VI);
+* Bernoulli(1/2) 0-1 matrices.
+
+numpy's PCG64 (default_rng) with the seeds of SURVEY.md 8(d).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+SEEDS = {"cfg1": 16, "cfg2_u": 2000, "cfg2_idx": 3000, "cfg3": 24, "cfg4": 1024, "cfg5": 44}
+
+
+def complex_gaussian(shape, seed: int | np.random.Generator) -> np.ndarray:
+    """(g1 + i g2)/sqrt(2): real block drawn first, then imaginary block."""
+    rng = np.random.default_rng(seed) if not isinstance(seed, np.random.Generator) else seed
+    re = rng.standard_normal(shape)
+    im = rng.standard_normal(shape)
+    return np.ascontiguousarray((re + 1j * im) / np.sqrt(2.0))
+
+
+def haar_unitary(m: int, seed: int | np.random.Generator) -> np.ndarray:
+    """Haar-random m x m unitary: Q R = Z, U = Q diag(r_ii / |r_ii|)."""
+    Z = complex_gaussian((m, m), seed)
+    Q, R = np.linalg.qr(Z)
+    d = np.diag(R)
+    return np.ascontiguousarray(Q * (d / np.abs(d))[None, :])
+
+
+def submatrix_indices(m: int, n: int, count: int, seed: int) -> tuple[np.ndarray, np.ndarray]:
+    """count pairs (rows, cols) of n distinct sorted indices in [0, m), in sample order."""
+    rng = np.random.default_rng(seed)
+    rows = np.empty((count, n), dtype=np.int64)
+    cols = np.empty((count, n), dtype=np.int64)
+    for s in range(count):
+        rows[s] = np.sort(rng.choice(m, n, replace=False))
+        cols[s] = np.sort(rng.choice(m, n, replace=False))
+    return rows, cols
+
+
+def gather_submatrices(U: np.ndarray, rows: np.ndarray, cols: np.ndarray) -> np.ndarray:
+    """(count, n, n) complex128 with out[s] = U[rows[s]][:, cols[s]]."""
+    return np.ascontiguousarray(U[rows[:, :, None], cols[:, None, :]])
+
+
+def bernoulli01(shape, seed: int) -> np.ndarray:
+    rng = np.random.default_rng(seed)
+    return np.ascontiguousarray(rng.integers(0, 2, size=shape, dtype=np.uint8))
+
+
+# ---------------------------------------------------------------- the 5 configs
+
+def cfg1() -> np.ndarray:
+    """Single 16x16 complex Gaussian (BASELINE.json configs[0])."""
+    return complex_gaussian((16, 16), SEEDS["cfg1"])
+
+
+def cfg2(n: int, count: int = 100_000) -> np.ndarray:
+    """(count, n, n) submatrices of an n^2 x n^2 Haar unitary (configs[1])."""
+    m = n * n
+    U = haar_unitary(m, SEEDS["cfg2_u"] + n)
+    rows, cols = submatrix_indices(m, n, count, SEEDS["cfg2_idx"] + n)
+    return gather_submatrices(U, rows, cols)
+
+
+def cfg3(batch: int = 64, n: int = 24) -> np.ndarray:
+    """(64, 24, 24) Bernoulli(1/2) 0-1 matrices (configs[2])."""
+    return bernoulli01((batch, n, n), SEEDS["cfg3"])
+
+
+def cfg4() -> np.ndarray:
+    """Leading 32x32 block of a 1024x1024 Haar unitary (configs[3])."""
+    U = haar_unitary(1024, SEEDS["cfg4"])
+    return np.ascontiguousarray(U[:32, :32])
+
+
+def cfg5() -> np.ndarray:
+    """Single 44x44 complex Gaussian (configs[4])."""
+    return complex_gaussian((44, 44), SEEDS["cfg5"])
+
+
+# ---------------------------------------------------------------- structured inputs
+
+def block_diag_scrambled(B1: np.ndarray, B2: np.ndarray, seed: int) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
+    """P (B1 (+) B2) Q with random permutations P, Q.  Returns (M, row_perm, col_perm)."""
+    n1, n2 = B1.shape[0], B2.shape[0]
+    n = n1 + n2
+    M = np.zeros((n, n), dtype=np.complex128)
+    M[:n1, :n1] = B1
+    M[n1:, n1:] = B2
+    rng = np.random.default_rng(seed)
+    rp = rng.permutation(n)
+    cp = rng.permutation(n)
+    return np.ascontiguousarray(M[rp][:, cp]), rp, cp
+
+
+def ones(n: int) -> np.ndarray:
+    return np.ones((n, n), dtype=np.complex128)
