@@ -1,0 +1,158 @@
+/*
+ * perm.h -- C ABI of the B200 (sm_100a) Gray-code Ryser/Glynn permanent library (libperm.so).
+ *
+ * The operation is the permanent of an n x n matrix,
+ *     per(A) = sum_{pi in S_n} prod_i a_{i,pi(i)}               (Eq. (1)),
+ * evaluated by Ryser's inclusion-exclusion formula (Eq. (3)) in its half-range
+ * (Nijenhuis-Wilf / Glynn) form walked in Gray-code order, exactly as the
+ * paper's App. A subpermanent/permanent:
+ *
+ *     w_i(r) = a_{i,n} - 1/2 sum_j a_{i,j} + sum_{j<n, x_j = 1} a_{i,j},   x = gray(r) = r ^ (r >> 1)
+ *     P(k0, k1) = sum_{r = k0}^{k1 - 1} (-1)^{r+1} prod_{i=1}^{n} w_i(r)         ("raw partial")
+ *     per(A) = 2 (-1)^n P(0, 2^{n-1})
+ *
+ * Conventions (all calls):
+ *   - Complex matrices are row-major n x n arrays of perm_c128_t = {re, im} (binary64), i.e. the
+ *     memory layout of a contiguous numpy / torch complex128 array.  Entry (i, j) is A[i*n + j].
+ *     Column index j is 0-based; the pinned column of App. A ("a_{i,n}") is column n-1, and Gray
+ *     bit j (bit 0 = least significant) selects column j.
+ *   - Every call returns a perm_status_t; PERM_OK == 0.  On PERM_E_CUDA the CUDA error text of
+ *     the failing call is available from perm_last_error() (thread-local).
+ *   - Work is enqueued on `stream` (a cudaStream_t; NULL = legacy default stream).  A call whose
+ *     output is HOST memory synchronizes that stream before returning; a call whose outputs are all
+ *     DEVICE memory returns after enqueueing (stream-ordered, no host sync).
+ *   - Pointers documented "host or device" are classified with cudaPointerGetAttributes.
+ *   - The caller owns every buffer.  The library keeps no mutable global state, so concurrent calls
+ *     on distinct buffers (and streams) are safe.  When `workspace` is NULL the library allocates
+ *     the scratch it needs stream-ordered (cudaMallocAsync / cudaFreeAsync) on `stream`.
+ *   - Results are deterministic: bit-identical for the same inputs, n, range and device.
+ *   - Floating point: IEEE-754 binary64, round-to-nearest, no fast-math; products in binary64
+ *     (FMA-contracted), sums accumulated in double-double (hi + lo) per component, i.e. the
+ *     paper's "double product, extended sum" mode.
+ */
+#ifndef PERM_H_
+#define PERM_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct { double re, im; } perm_c128_t;                      /* == complex128 */
+typedef struct { double hi_re, lo_re, hi_im, lo_im; } perm_dd_c128_t; /* value = (hi_re+lo_re) + i(hi_im+lo_im) */
+typedef struct { uint64_t lo; int64_t hi; } perm_i128_t;             /* two's-complement int128 = hi*2^64 + lo */
+
+typedef struct {
+    uint64_t terms;        /* Gray-code terms evaluated (2^{n-1} for a whole permanent, C20)      */
+    uint32_t chunk_log2;   /* b: the walk's aligned chunk length is 2^b                           */
+    uint32_t threads;      /* walker threads launched                                             */
+    uint32_t blocks;       /* walker blocks launched                                              */
+    uint32_t launches;     /* kernels launched by this call                                        */
+} perm_stats_t;
+
+typedef enum {
+    PERM_OK = 0,
+    PERM_E_ARG = 1,        /* null required pointer, negative count, k_begin > k_end, bad workspace size */
+    PERM_E_ORDER = 2,      /* n < 1, n > 64 (complex), n > 28 (int01), k_end > 2^{n-1}                  */
+    PERM_E_NONFINITE = 3,  /* a NaN/Inf matrix entry (perm_c128 / perm_c128_range)                       */
+    PERM_E_NOT01 = 4,      /* a byte other than 0 or 1 (perm_int01)                                      */
+    PERM_E_CUDA = 5,       /* a CUDA runtime call failed; see perm_last_error()                         */
+    PERM_E_WORKSPACE = 6,  /* workspace smaller than perm_workspace_bytes()                             */
+    PERM_E_CHECK = 7       /* int01 self-check failed: raw Glynn sum not divisible by 2^{n-1}           */
+} perm_status_t;
+
+/* ------------------------------------------------------------------------------------------
+ * Single matrix (BASELINE configs 1, 4, 5).
+ * ------------------------------------------------------------------------------------------ */
+
+/* Scratch bytes needed by perm_c128 / perm_c128_range for order n and rank range [k_begin, k_end). */
+perm_status_t perm_workspace_bytes(int n, uint64_t k_begin, uint64_t k_end, size_t* bytes);
+
+/* per(A) of one n x n complex matrix, 1 <= n <= 64 (ranks are 64-bit words).
+ *   A          host or device, n*n perm_c128_t, row-major, read only, all entries finite.
+ *   out        host or device, one perm_c128_t: per(A) = 2(-1)^n P(0, 2^{n-1}) rounded from dd.
+ *   out_dd     optional (may be NULL), host or device: the dd value of per(A) before rounding.
+ *   workspace  device scratch of >= perm_workspace_bytes(n, 0, 2^{n-1}) bytes, or NULL.
+ *   stats      optional host struct (may be NULL).
+ * Errors: PERM_E_ARG (A or out NULL), PERM_E_ORDER, PERM_E_NONFINITE, PERM_E_WORKSPACE, PERM_E_CUDA.
+ * Cite: problem P:56-59; method App. A P:1126-1163 (subpermanent + permanent). */
+perm_status_t perm_c128(const perm_c128_t* A, int n, perm_c128_t* out, perm_dd_c128_t* out_dd,
+                        void* workspace, size_t workspace_bytes, void* stream, perm_stats_t* stats);
+
+/* Raw partial P(k_begin, k_end) over the Gray ranks [k_begin, k_end) subset of [0, 2^{n-1}),
+ * WITHOUT the 2(-1)^n factor: App. A subpermanent for the rank span that
+ * distribute hands one worker.  Used to shard one permanent over GPUs/processes;
+ * any split of [0, 2^{n-1}) into spans combined by perm_c128_finalize gives per(A).
+ *   partial    host or device, one perm_dd_c128_t.  k_begin == k_end gives 0.
+ * Errors: as perm_c128, plus PERM_E_ORDER if k_end > 2^{n-1}, PERM_E_ARG if k_begin > k_end. */
+perm_status_t perm_c128_range(const perm_c128_t* A, int n, uint64_t k_begin, uint64_t k_end,
+                              perm_dd_c128_t* partial, void* workspace, size_t workspace_bytes,
+                              void* stream, perm_stats_t* stats);
+
+/* Host-only: out = 2(-1)^n * sum_{k=0}^{count-1} partials[k], summed in index order in double-double
+ * (App. A permanent step 4; "stored in an array before the final ... summation").
+ *   partials   host, count perm_dd_c128_t.   out   host.   out_dd optional host.
+ * Errors: PERM_E_ARG (NULL, count < 0), PERM_E_ORDER (n outside 1..64). */
+perm_status_t perm_c128_finalize(const perm_dd_c128_t* partials, int count, int n, perm_c128_t* out,
+                                 perm_dd_c128_t* out_dd);
+
+/* ------------------------------------------------------------------------------------------
+ * Batch of small complex matrices (BASELINE config 2: Boson-sampling probabilities).
+ * ------------------------------------------------------------------------------------------ */
+
+/* per and |per|^2 of B independent n x n complex matrices, 1 <= n <= 32.
+ *   A_dev      device, B*n*n perm_c128_t, matrix b at A_dev + b*n*n (row-major).
+ *   per_dev    device, B perm_c128_t, or NULL.       abs2_dev   device, B doubles |per|^2, or NULL.
+ * Stream-ordered: returns after enqueueing.  B == 0 is a no-op.  Non-finite entries are not
+ * checked; they propagate to NaN/Inf in that matrix's outputs only.
+ * Errors: PERM_E_ARG (A_dev NULL, B < 0, both outputs NULL), PERM_E_ORDER, PERM_E_CUDA.
+ * Cite: P:954-958 (submatrices of a Haar unitary), P:1126-1163 (method per matrix). */
+perm_status_t perm_c128_batched(const perm_c128_t* A_dev, int n, int64_t B, perm_c128_t* per_dev,
+                                double* abs2_dev, void* stream);
+
+/* ------------------------------------------------------------------------------------------
+ * Exact permanents of 0-1 matrices (BASELINE config 3; #P-hard even for 0-1).
+ * ------------------------------------------------------------------------------------------ */
+
+/* Scratch bytes needed by perm_int01 for B matrices of order n. */
+perm_status_t perm_int01_workspace_bytes(int n, int64_t B, size_t* bytes);
+
+/* Exact per(A) of B 0-1 matrices, 1 <= n <= 28, as int128.  Integer Glynn sums g_i = 2 w_i are walked
+ * in Gray order; products and the signed sum are exact mod 2^128, per = (-1)^n Sum / 2^{n-1} is exact
+ * for n <= 28 (n! 2^{n-1} < 2^127), and the low n-1 bits of Sum are checked to be zero.
+ *   A_dev     device, B*n*n bytes, each 0 or 1, row-major.
+ *   out_dev   device, B perm_i128_t.
+ * Synchronizes `stream` (to report PERM_E_NOT01 / PERM_E_CHECK).
+ * Errors: PERM_E_ARG, PERM_E_ORDER, PERM_E_NOT01 (outputs unspecified), PERM_E_CHECK, PERM_E_WORKSPACE,
+ *         PERM_E_CUDA. */
+perm_status_t perm_int01(const uint8_t* A_dev, int n, int64_t B, perm_i128_t* out_dev,
+                         void* workspace, size_t workspace_bytes, void* stream);
+
+/* ------------------------------------------------------------------------------------------
+ * Diagnostics.
+ * ------------------------------------------------------------------------------------------ */
+
+/* w(r) of App. A steps 2, 5-8 for ranks r_k = chunk-aligned starts, computed by the
+ * device seeding code: w_out (host or device) receives count*n perm_c128_t, w(ranks[k]) at
+ * w_out + k*n.  ranks: host array of count uint64 ranks < 2^{n-1}.  Synchronizes if w_out is host. */
+perm_status_t perm_c128_seed(const perm_c128_t* A, int n, const uint64_t* ranks, int count,
+                             perm_c128_t* w_out, void* stream);
+
+/* FP64 peak probe: each of blocks x threads threads runs `iters` iterations of 32 DFMA
+ * (8 independent dependent chains), i.e. 64 * iters flops per thread.  Writes a checksum to sink_dev
+ * (device, blocks*threads doubles).  Stream-ordered. */
+perm_status_t perm_fp64_probe(int blocks, int threads, int iters, double* sink_dev, void* stream);
+
+/* Number of kernels enqueued by this thread's last successful call (for launch accounting). */
+uint32_t perm_last_launches(void);
+
+const char* perm_status_string(perm_status_t status);
+const char* perm_last_error(void);
+int perm_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PERM_H_ */

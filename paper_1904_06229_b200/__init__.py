@@ -1,1 +1,329 @@
-"""B200-native Gray-code Ryser/Glynn permanent (placeholder, binding added with the C-ABI)."""
+"""B200-native Gray-code Ryser/Glynn permanent (arXiv 1904.06229, Lundow & Markstrom).
+
+Thin Python binding over the C ABI of ``libperm.so`` (``include/perm.h``): argument marshalling
+only.  Every step of the method runs in the library's sm_100a kernels; there is no CPU fallback --
+if ``libperm.so`` is missing or cannot reach a GPU, calls raise.  PyTorch is used only for device
+memory (workspace / outputs) and streams.
+
+Names follow the C ABI:
+
+* :func:`perm_c128`          -- per(A) of one complex matrix (App. A permanent)
+* :func:`perm_c128_range`    -- raw partial over a Gray-rank span (App. A subpermanent)
+* :func:`perm_c128_finalize` -- 2(-1)^n * ordered dd sum of partials
+* :func:`perm_c128_batched`  -- per and |per|^2 of a batch of small matrices
+* :func:`perm_int01`         -- exact int128 permanents of 0-1 matrices
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+from dataclasses import dataclass
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_PKG, "libperm.so")
+_HEADER = os.path.join(os.path.dirname(_PKG), "include", "perm.h")
+
+STATUS = {0: "PERM_OK", 1: "PERM_E_ARG", 2: "PERM_E_ORDER", 3: "PERM_E_NONFINITE", 4: "PERM_E_NOT01",
+          5: "PERM_E_CUDA", 6: "PERM_E_WORKSPACE", 7: "PERM_E_CHECK"}
+
+
+class PermError(RuntimeError):
+    def __init__(self, status: int, detail: str = ""):
+        self.status = status
+        self.name = STATUS.get(status, str(status))
+        super().__init__(f"{self.name}: {detail}" if detail else self.name)
+
+
+class c128(ctypes.Structure):
+    _fields_ = [("re", ctypes.c_double), ("im", ctypes.c_double)]
+
+
+class dd_c128(ctypes.Structure):
+    _fields_ = [("hi_re", ctypes.c_double), ("lo_re", ctypes.c_double),
+                ("hi_im", ctypes.c_double), ("lo_im", ctypes.c_double)]
+
+
+class i128(ctypes.Structure):
+    _fields_ = [("lo", ctypes.c_uint64), ("hi", ctypes.c_int64)]
+
+
+class stats_t(ctypes.Structure):
+    _fields_ = [("terms", ctypes.c_uint64), ("chunk_log2", ctypes.c_uint32), ("threads", ctypes.c_uint32),
+                ("blocks", ctypes.c_uint32), ("launches", ctypes.c_uint32)]
+
+
+@dataclass
+class DD:
+    """A complex double-double value (hi + lo per component)."""
+    hi_re: float
+    lo_re: float
+    hi_im: float
+    lo_im: float
+
+    @property
+    def value(self) -> complex:
+        return complex(self.hi_re + self.lo_re, self.hi_im + self.lo_im)
+
+    def astuple(self):
+        return (self.hi_re, self.lo_re, self.hi_im, self.lo_im)
+
+
+_lib = None
+
+
+def header_functions() -> list[str]:
+    """Names of the functions declared in include/perm.h."""
+    txt = open(_HEADER).read()
+    return sorted(set(re.findall(r"^\s*(?:perm_status_t|const char\*|uint32_t|int)\s+(perm_\w+)\s*\(", txt, re.M)))
+
+
+def lib() -> ctypes.CDLL:
+    """Load libperm.so (raises if it has not been built -- there is no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_LIB_PATH):
+        raise ImportError(f"{_LIB_PATH} not built: run `python -m paper_1904_06229_b200.build` "
+                          "(or __graft_entry__.build()); there is no CPU fallback")
+    L = ctypes.CDLL(_LIB_PATH)
+    P, i32, i64, u64, sz = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_uint64, ctypes.c_size_t
+    sig = {
+        "perm_workspace_bytes": [i32, u64, u64, ctypes.POINTER(sz)],
+        "perm_c128": [P, i32, P, P, P, sz, P, P],
+        "perm_c128_range": [P, i32, u64, u64, P, P, sz, P, P],
+        "perm_c128_finalize": [P, i32, i32, P, P],
+        "perm_c128_batched": [P, i32, i64, P, P, P],
+        "perm_int01_workspace_bytes": [i32, i64, ctypes.POINTER(sz)],
+        "perm_int01": [P, i32, i64, P, P, sz, P],
+        "perm_c128_seed": [P, i32, P, i32, P, P],
+        "perm_fp64_probe": [i32, i32, i32, P, P],
+    }
+    for name, args in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = ctypes.c_int
+    L.perm_status_string.argtypes = [ctypes.c_int]
+    L.perm_status_string.restype = ctypes.c_char_p
+    L.perm_last_error.argtypes = []
+    L.perm_last_error.restype = ctypes.c_char_p
+    L.perm_last_launches.argtypes = []
+    L.perm_last_launches.restype = ctypes.c_uint32
+    L.perm_version.argtypes = []
+    L.perm_version.restype = ctypes.c_int
+    _lib = L
+    return L
+
+
+def _check(st: int):
+    if st != 0:
+        detail = lib().perm_last_error().decode() if st == 5 else lib().perm_status_string(st).decode()
+        raise PermError(st, detail)
+
+
+def last_launches() -> int:
+    """Kernels enqueued by this thread's last successful library call."""
+    return int(lib().perm_last_launches())
+
+
+# ------------------------------------------------------------------------------------- marshalling
+
+def _torch():
+    import torch
+    return torch
+
+
+def _is_torch(x) -> bool:
+    try:
+        import torch
+        return isinstance(x, torch.Tensor)
+    except ImportError:  # pragma: no cover
+        return False
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        torch = _torch()
+        if torch.cuda.is_available():
+            return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+        return ctypes.c_void_p(0)
+    if isinstance(stream, int):
+        return ctypes.c_void_p(stream)
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _matrix_ptr(A):
+    """(pointer, n, keepalive) for a square complex128 matrix: numpy (host) or torch (host/device)."""
+    if _is_torch(A):
+        torch = _torch()
+        if A.dtype != torch.complex128:
+            A = A.to(torch.complex128)
+        A = A.contiguous()
+        if A.dim() != 2 or A.shape[0] != A.shape[1]:
+            raise ValueError("A must be a square matrix")
+        return ctypes.c_void_p(A.data_ptr()), int(A.shape[0]), A
+    A = np.ascontiguousarray(np.asarray(A, dtype=np.complex128))
+    if A.ndim != 2 or A.shape[0] != A.shape[1]:
+        raise ValueError("A must be a square matrix")
+    return A.ctypes.data_as(ctypes.c_void_p), int(A.shape[0]), A
+
+
+def workspace_bytes(n: int, k_begin: int = 0, k_end: int | None = None) -> int:
+    if k_end is None:
+        k_end = 1 << (n - 1) if 1 <= n <= 64 else 0
+    b = ctypes.c_size_t()
+    _check(lib().perm_workspace_bytes(n, k_begin, k_end, ctypes.byref(b)))
+    return int(b.value)
+
+
+def make_workspace(n: int, k_begin: int = 0, k_end: int | None = None, device=None):
+    """A torch uint8 CUDA tensor large enough for perm_c128 / perm_c128_range at order n."""
+    torch = _torch()
+    return torch.empty(workspace_bytes(n, k_begin, k_end), dtype=torch.uint8, device=device or "cuda")
+
+
+def _ws_args(workspace):
+    if workspace is None:
+        return ctypes.c_void_p(0), 0
+    return ctypes.c_void_p(workspace.data_ptr()), int(workspace.numel() * workspace.element_size())
+
+
+def perm_c128(A, *, workspace=None, stream=None, out=None, return_dd: bool = False, stats: bool = False):
+    """per(A) for one complex matrix (host numpy / torch CPU or CUDA tensor), 1 <= n <= 64.
+
+    With ``out`` (a CUDA complex128 tensor of 1 element) the call is stream-ordered and returns
+    ``out``; otherwise it synchronizes and returns a Python complex (plus DD / stats if asked)."""
+    ptr, n, keep = _matrix_ptr(A)
+    ws, wsb = _ws_args(workspace)
+    st = stats_t()
+    if out is not None:
+        _check(lib().perm_c128(ptr, n, ctypes.c_void_p(out.data_ptr()), None, ws, wsb, _stream_ptr(stream),
+                               ctypes.byref(st)))
+        return out
+    res = c128()
+    ddv = dd_c128()
+    _check(lib().perm_c128(ptr, n, ctypes.byref(res), ctypes.byref(ddv), ws, wsb, _stream_ptr(stream),
+                           ctypes.byref(st)))
+    del keep
+    val = complex(res.re, res.im)
+    extra = []
+    if return_dd:
+        extra.append(DD(ddv.hi_re, ddv.lo_re, ddv.hi_im, ddv.lo_im))
+    if stats:
+        extra.append({"terms": st.terms, "chunk_log2": st.chunk_log2, "threads": st.threads,
+                      "blocks": st.blocks, "launches": st.launches})
+    return (val, *extra) if extra else val
+
+
+def perm_c128_range(A, k_begin: int, k_end: int, *, workspace=None, stream=None, out=None, stats: bool = False):
+    """Raw partial P(k_begin, k_end) = sum_{r in [k_begin, k_end)} (-1)^{r+1} prod_i w_i(gray r) (no 2(-1)^n).
+
+    With ``out`` (a CUDA float64 tensor of 4 elements: hi_re, lo_re, hi_im, lo_im) the call is
+    stream-ordered and returns ``out``; otherwise it synchronizes and returns a :class:`DD`."""
+    ptr, n, keep = _matrix_ptr(A)
+    ws, wsb = _ws_args(workspace)
+    st = stats_t()
+    if out is not None:
+        _check(lib().perm_c128_range(ptr, n, int(k_begin), int(k_end), ctypes.c_void_p(out.data_ptr()), ws, wsb,
+                                     _stream_ptr(stream), ctypes.byref(st)))
+        return out
+    ddv = dd_c128()
+    _check(lib().perm_c128_range(ptr, n, int(k_begin), int(k_end), ctypes.byref(ddv), ws, wsb,
+                                 _stream_ptr(stream), ctypes.byref(st)))
+    del keep
+    d = DD(ddv.hi_re, ddv.lo_re, ddv.hi_im, ddv.lo_im)
+    if stats:
+        return d, {"terms": st.terms, "chunk_log2": st.chunk_log2, "threads": st.threads, "blocks": st.blocks,
+                   "launches": st.launches}
+    return d
+
+
+def perm_c128_finalize(partials, n: int, return_dd: bool = False):
+    """2(-1)^n * sum_k partials[k] in index order (double-double).  partials: sequence of DD / 4-tuples
+    or an (count, 4) float64 array."""
+    arr = np.ascontiguousarray(np.array([p.astuple() if isinstance(p, DD) else tuple(p) for p in partials],
+                                        dtype=np.float64).reshape(-1, 4))
+    res = c128()
+    ddv = dd_c128()
+    _check(lib().perm_c128_finalize(arr.ctypes.data_as(ctypes.c_void_p), arr.shape[0], n, ctypes.byref(res),
+                                    ctypes.byref(ddv)))
+    val = complex(res.re, res.im)
+    if return_dd:
+        return val, DD(ddv.hi_re, ddv.lo_re, ddv.hi_im, ddv.lo_im)
+    return val
+
+
+def perm_c128_batched(A, *, per=None, abs2=None, want_per: bool = True, want_abs2: bool = True, stream=None):
+    """per and |per|^2 of a (B, n, n) complex128 CUDA tensor, 1 <= n <= 32.  Stream-ordered.
+    Returns (per, abs2) CUDA tensors (either may be None if not requested)."""
+    torch = _torch()
+    if not (_is_torch(A) and A.is_cuda):
+        raise ValueError("perm_c128_batched expects a CUDA torch tensor (B, n, n) complex128")
+    if A.dtype != torch.complex128:
+        raise ValueError("A must be complex128")
+    A = A.contiguous()
+    B, n, n2 = A.shape
+    if n != n2:
+        raise ValueError("matrices must be square")
+    if per is None and want_per:
+        per = torch.empty(B, dtype=torch.complex128, device=A.device)
+    if abs2 is None and want_abs2:
+        abs2 = torch.empty(B, dtype=torch.float64, device=A.device)
+    _check(lib().perm_c128_batched(ctypes.c_void_p(A.data_ptr()), n, B,
+                                   ctypes.c_void_p(per.data_ptr() if per is not None else 0),
+                                   ctypes.c_void_p(abs2.data_ptr() if abs2 is not None else 0),
+                                   _stream_ptr(stream)))
+    return per, abs2
+
+
+def int01_workspace_bytes(n: int, B: int) -> int:
+    b = ctypes.c_size_t()
+    _check(lib().perm_int01_workspace_bytes(n, B, ctypes.byref(b)))
+    return int(b.value)
+
+
+def perm_int01(A, *, workspace=None, out=None, stream=None, as_int: bool = True):
+    """Exact per of a (B, n, n) uint8 0-1 CUDA tensor, n <= 28.  Synchronizes.  Returns a list of Python
+    ints (as_int) or the raw (B, 2) int64 CUDA tensor {lo, hi} of two's-complement int128."""
+    torch = _torch()
+    if not (_is_torch(A) and A.is_cuda and A.dtype == torch.uint8):
+        raise ValueError("perm_int01 expects a CUDA uint8 tensor (B, n, n)")
+    A = A.contiguous()
+    B, n, n2 = A.shape
+    if n != n2:
+        raise ValueError("matrices must be square")
+    if out is None:
+        out = torch.empty((B, 2), dtype=torch.int64, device=A.device)
+    ws, wsb = _ws_args(workspace)
+    _check(lib().perm_int01(ctypes.c_void_p(A.data_ptr()), n, B, ctypes.c_void_p(out.data_ptr()), ws, wsb,
+                            _stream_ptr(stream)))
+    if not as_int:
+        return out
+    raw = out.cpu().numpy()
+    vals = []
+    for lo, hi in raw:
+        vals.append((int(hi) << 64) + (int(lo) & ((1 << 64) - 1)))
+    return vals
+
+
+def perm_c128_seed(A, ranks) -> np.ndarray:
+    """w(r) (App. A steps 2, 5-8) computed by the device seeding code, for each rank r -> (count, n)."""
+    ptr, n, keep = _matrix_ptr(A)
+    r = np.ascontiguousarray(np.asarray(ranks, dtype=np.uint64))
+    out = np.zeros((r.shape[0], n), dtype=np.complex128)
+    _check(lib().perm_c128_seed(ptr, n, r.ctypes.data_as(ctypes.c_void_p), r.shape[0],
+                                out.ctypes.data_as(ctypes.c_void_p), _stream_ptr(None)))
+    del keep
+    return out
+
+
+def perm_fp64_probe(blocks: int, threads: int, iters: int, sink, stream=None):
+    """Enqueue the FP64 peak probe: blocks*threads*iters*32 DFMA (64 flops per thread-iteration)."""
+    _check(lib().perm_fp64_probe(blocks, threads, iters, ctypes.c_void_p(sink.data_ptr()), _stream_ptr(stream)))
+
+
+__all__ = ["perm_c128", "perm_c128_range", "perm_c128_finalize", "perm_c128_batched", "perm_int01",
+           "perm_c128_seed", "perm_fp64_probe", "workspace_bytes", "make_workspace", "int01_workspace_bytes",
+           "PermError", "DD", "lib", "header_functions", "last_launches"]

@@ -1,0 +1,453 @@
+// abi.cu -- the extern "C" boundary of libperm.so (include/perm.h): argument validation, launch
+// planning (partition of the Gray-rank range into aligned chunks), workspace
+// layout, stream handling and status codes.  All arithmetic of the method runs in the kernels.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "../../include/perm.h"
+#include "internal.h"
+
+namespace {
+
+using perm::ddc;
+using perm::Segment;
+
+thread_local char g_err[512] = "";
+thread_local uint32_t g_launches = 0;
+
+perm_status_t cuda_fail(cudaError_t e, const char* what) {
+    snprintf(g_err, sizeof(g_err), "%s: %s (%s)", what, cudaGetErrorString(e), cudaGetErrorName(e));
+    return PERM_E_CUDA;
+}
+
+#define PERM_CUDA(call, what)                              \
+    do {                                                   \
+        cudaError_t e_ = (call);                           \
+        if (e_ != cudaSuccess) return cuda_fail(e_, what); \
+    } while (0)
+
+bool is_device_ptr(const void* p) {
+    cudaPointerAttributes attr;
+    if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
+        cudaGetLastError();   // clear: plain host pointers may report an error on old runtimes
+        return false;
+    }
+    return attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged;
+}
+
+size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+struct WalkPlan {
+    int grid = 1;
+    int threads = 0;
+    int b = 0;
+    int nseg = 0;
+    Segment seg[perm::kMaxSegments];
+    uint64_t items = 0;
+};
+
+int floor_log2(uint64_t x) { return x ? 63 - __builtin_clzll(x) : -1; }
+
+// Chunk length 2^b for a span of `total` ranks and T resident threads: at least ~128 chunks per
+// thread so the static round-robin leaves < 1% tail, at least the unrolled block 2^U, at most 2^40.
+int choose_b(int n, uint64_t total, uint64_t T) {
+    const int U = perm::walk_inner_bits(n);
+    int b = floor_log2(total / (T * 128ull > 0 ? T * 128ull : 1));
+    if (b < U) b = U;
+    if (b > n - 1) b = n - 1;
+    if (b > 40) b = 40;
+    if (b < 0) b = 0;
+    return b;
+}
+
+// Cut [k0, k1) into maximal aligned pieces of 2^e ranks, e <= b; pieces with 0 < e < U become single
+// ranks (e = 0).  Consecutive equal-e pieces merge into one Segment.
+bool decompose(int n, uint64_t k0, uint64_t k1, int b, WalkPlan& p) {
+    const int U = perm::walk_inner_bits(n);
+    p.nseg = 0;
+    p.items = 0;
+    uint64_t r = k0;
+    auto emit = [&](uint64_t c0, uint64_t count, int e) -> bool {
+        if (p.nseg > 0) {
+            Segment& s = p.seg[p.nseg - 1];
+            if (s.e == e && s.c0 + s.count == c0) {
+                s.count += count;
+                p.items += count;
+                return true;
+            }
+        }
+        if (p.nseg >= perm::kMaxSegments) return false;
+        p.seg[p.nseg].c0 = c0;
+        p.seg[p.nseg].count = count;
+        p.seg[p.nseg].e = e;
+        p.nseg++;
+        p.items += count;
+        return true;
+    };
+    while (r < k1) {
+        int e = (r == 0) ? 63 : __builtin_ctzll(r);
+        if (e > b) e = b;
+        while (e > 0 && (k1 - r) < (1ull << e)) e--;
+        if (e < U) e = 0;
+        if (e == b && e > 0) {
+            const uint64_t cnt = (k1 - r) >> b;          // run of whole 2^b chunks
+            if (!emit(r >> b, cnt, b)) return false;
+            r += cnt << b;
+        } else {
+            if (!emit(r >> e, 1, e)) return false;
+            r += 1ull << e;
+        }
+    }
+    return true;
+}
+
+perm_status_t device_threads(int n, int* max_grid, int* nt) {
+    int dev = 0, sms = 0, bps = 0;
+    PERM_CUDA(cudaGetDevice(&dev), "cudaGetDevice");
+    PERM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "cudaDeviceGetAttribute");
+    PERM_CUDA(perm::walk_occupancy_n(n, &bps, nt), "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
+    if (bps < 1) bps = 1;
+    *max_grid = sms * bps;
+    return PERM_OK;
+}
+
+perm_status_t plan_walk(int n, uint64_t k0, uint64_t k1, WalkPlan& p) {
+    int max_grid = 0, nt = 0;
+    perm_status_t st = device_threads(n, &max_grid, &nt);
+    if (st != PERM_OK) return st;
+    p.threads = nt;
+    p.b = choose_b(n, k1 - k0, (uint64_t)max_grid * nt);
+    if (!decompose(n, k0, k1, p.b, p)) {
+        snprintf(g_err, sizeof(g_err), "range decomposition exceeded %d segments", perm::kMaxSegments);
+        return PERM_E_ARG;
+    }
+    uint64_t need = (p.items + nt - 1) / nt;
+    p.grid = (int)(need < (uint64_t)max_grid ? need : (uint64_t)max_grid);
+    if (p.grid < 1) p.grid = 1;
+    return PERM_OK;
+}
+
+struct WsLayout {
+    size_t a_off, part_off, res_dd_off, res_c_off, total;
+};
+
+WsLayout ws_layout(int n, int max_grid) {
+    WsLayout L;
+    L.a_off = 0;
+    L.part_off = align256((size_t)n * n * sizeof(double2));
+    L.res_dd_off = align256(L.part_off + (size_t)max_grid * sizeof(ddc));
+    L.res_c_off = L.res_dd_off + sizeof(ddc);
+    L.total = align256(L.res_c_off + sizeof(double2));
+    return L;
+}
+
+perm_status_t check_order(int n) { return (n < 1 || n > perm::kMaxN) ? PERM_E_ORDER : PERM_OK; }
+
+// Validates entries (host copy) and returns a host copy of A for the checks.
+perm_status_t load_and_check(const perm_c128_t* A, int n, bool a_dev, cudaStream_t s,
+                             std::vector<perm_c128_t>& host) {
+    const size_t cnt = (size_t)n * n;
+    const perm_c128_t* h = A;
+    if (a_dev) {
+        host.resize(cnt);
+        PERM_CUDA(cudaMemcpyAsync(host.data(), A, cnt * sizeof(perm_c128_t), cudaMemcpyDeviceToHost, s),
+                  "cudaMemcpyAsync(A D2H)");
+        PERM_CUDA(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+        h = host.data();
+    }
+    for (size_t k = 0; k < cnt; k++)
+        if (!std::isfinite(h[k].re) || !std::isfinite(h[k].im)) return PERM_E_NONFINITE;
+    return PERM_OK;
+}
+
+// Shared body of perm_c128 (n_final = n) and perm_c128_range (n_final = 0).
+perm_status_t run_walk(const perm_c128_t* A, int n, uint64_t k0, uint64_t k1, int n_final, void* out_c,
+                       void* out_dd, void* workspace, size_t workspace_bytes, void* stream,
+                       perm_stats_t* stats) {
+    g_launches = 0;
+    cudaStream_t s = (cudaStream_t)stream;
+    const bool a_dev = is_device_ptr(A);
+    std::vector<perm_c128_t> host;
+    perm_status_t st = load_and_check(A, n, a_dev, s, host);
+    if (st != PERM_OK) return st;
+
+    WalkPlan p;
+    st = plan_walk(n, k0, k1, p);
+    if (st != PERM_OK) return st;
+    int max_grid = 0, nt = 0;
+    st = device_threads(n, &max_grid, &nt);
+    if (st != PERM_OK) return st;
+    const WsLayout L = ws_layout(n, max_grid);
+
+    char* ws = (char*)workspace;
+    bool own_ws = false;
+    if (ws == nullptr) {
+        PERM_CUDA(cudaMallocAsync((void**)&ws, L.total, s), "cudaMallocAsync(workspace)");
+        own_ws = true;
+    } else if (workspace_bytes < L.total) {
+        return PERM_E_WORKSPACE;
+    }
+    perm_status_t result = PERM_OK;
+    uint32_t launches = 0;
+    do {
+        const double2* A_dev = (const double2*)A;
+        if (!a_dev) {
+            cudaError_t e = cudaMemcpyAsync(ws + L.a_off, A, (size_t)n * n * sizeof(double2),
+                                            cudaMemcpyHostToDevice, s);
+            if (e != cudaSuccess) { result = cuda_fail(e, "cudaMemcpyAsync(A H2D)"); break; }
+            A_dev = (const double2*)(ws + L.a_off);
+        }
+        ddc* partials = (ddc*)(ws + L.part_off);
+        ddc* res_dd = (ddc*)(ws + L.res_dd_off);
+        double2* res_c = (double2*)(ws + L.res_c_off);
+        if (k1 > k0) {
+            perm::WalkLaunch WL;
+            WL.A_dev = A_dev;
+            WL.A_host = a_dev ? (const double2*)host.data() : (const double2*)A;
+            WL.n = n;
+            WL.nseg = p.nseg;
+            for (int i = 0; i < p.nseg; i++) WL.seg[i] = p.seg[i];
+            WL.partials = partials;
+            WL.grid = p.grid;
+            WL.stream = s;
+            cudaError_t e = perm::walk_launch_n(n, WL);
+            if (e != cudaSuccess) { result = cuda_fail(e, "walk kernel launch"); break; }
+            launches++;
+            e = perm::reduce_launch(partials, p.grid, n_final, res_dd, res_c, s);
+            if (e != cudaSuccess) { result = cuda_fail(e, "reduce kernel launch"); break; }
+            launches++;
+        } else {
+            cudaError_t e = cudaMemsetAsync(ws + L.res_dd_off, 0, sizeof(ddc) + sizeof(double2), s);
+            if (e != cudaSuccess) { result = cuda_fail(e, "cudaMemsetAsync"); break; }
+        }
+        bool sync = false;
+        if (out_c) {
+            const bool d = is_device_ptr(out_c);
+            cudaError_t e = cudaMemcpyAsync(out_c, res_c, sizeof(double2),
+                                            d ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s);
+            if (e != cudaSuccess) { result = cuda_fail(e, "cudaMemcpyAsync(result)"); break; }
+            sync |= !d;
+        }
+        if (out_dd) {
+            const bool d = is_device_ptr(out_dd);
+            cudaError_t e = cudaMemcpyAsync(out_dd, res_dd, sizeof(ddc),
+                                            d ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s);
+            if (e != cudaSuccess) { result = cuda_fail(e, "cudaMemcpyAsync(result dd)"); break; }
+            sync |= !d;
+        }
+        if (own_ws) {
+            cudaError_t e = cudaFreeAsync(ws, s);
+            own_ws = false;
+            if (e != cudaSuccess) { result = cuda_fail(e, "cudaFreeAsync(workspace)"); break; }
+        }
+        if (sync) {
+            cudaError_t e = cudaStreamSynchronize(s);
+            if (e != cudaSuccess) { result = cuda_fail(e, "cudaStreamSynchronize"); break; }
+        }
+    } while (0);
+    if (own_ws) cudaFreeAsync(ws, s);
+    if (result == PERM_OK) {
+        g_launches = launches;
+        if (stats) {
+            stats->terms = k1 - k0;
+            stats->chunk_log2 = (uint32_t)p.b;
+            stats->threads = (uint32_t)(p.grid * p.threads);
+            stats->blocks = (uint32_t)p.grid;
+            stats->launches = launches;
+        }
+    }
+    return result;
+}
+
+}  // namespace
+
+extern "C" {
+
+int perm_version(void) { return 1; }
+
+uint32_t perm_last_launches(void) { return g_launches; }
+
+const char* perm_last_error(void) { return g_err; }
+
+const char* perm_status_string(perm_status_t s) {
+    switch (s) {
+        case PERM_OK: return "ok";
+        case PERM_E_ARG: return "invalid argument";
+        case PERM_E_ORDER: return "matrix order out of range";
+        case PERM_E_NONFINITE: return "non-finite matrix entry";
+        case PERM_E_NOT01: return "entry other than 0 or 1";
+        case PERM_E_CUDA: return "CUDA error";
+        case PERM_E_WORKSPACE: return "workspace too small";
+        case PERM_E_CHECK: return "integer self-check failed (sum not divisible by 2^(n-1))";
+    }
+    return "unknown status";
+}
+
+perm_status_t perm_workspace_bytes(int n, uint64_t k_begin, uint64_t k_end, size_t* bytes) {
+    if (!bytes) return PERM_E_ARG;
+    perm_status_t st = check_order(n);
+    if (st != PERM_OK) return st;
+    if (k_begin > k_end) return PERM_E_ARG;
+    if (n < 64 && k_end > (1ull << (n - 1))) return PERM_E_ORDER;
+    int max_grid = 0, nt = 0;
+    st = device_threads(n, &max_grid, &nt);
+    if (st != PERM_OK) return st;
+    *bytes = ws_layout(n, max_grid).total;
+    return PERM_OK;
+}
+
+perm_status_t perm_c128(const perm_c128_t* A, int n, perm_c128_t* out, perm_dd_c128_t* out_dd, void* workspace,
+                        size_t workspace_bytes, void* stream, perm_stats_t* stats) {
+    if (!A || !out) return PERM_E_ARG;
+    perm_status_t st = check_order(n);
+    if (st != PERM_OK) return st;
+    const uint64_t total = 1ull << (n - 1);
+    return run_walk(A, n, 0, total, n, out, out_dd, workspace, workspace_bytes, stream, stats);
+}
+
+perm_status_t perm_c128_range(const perm_c128_t* A, int n, uint64_t k_begin, uint64_t k_end,
+                              perm_dd_c128_t* partial, void* workspace, size_t workspace_bytes, void* stream,
+                              perm_stats_t* stats) {
+    if (!A || !partial) return PERM_E_ARG;
+    perm_status_t st = check_order(n);
+    if (st != PERM_OK) return st;
+    if (k_begin > k_end) return PERM_E_ARG;
+    if (k_end > (1ull << (n - 1))) return PERM_E_ORDER;
+    return run_walk(A, n, k_begin, k_end, 0, nullptr, partial, workspace, workspace_bytes, stream, stats);
+}
+
+perm_status_t perm_c128_finalize(const perm_dd_c128_t* partials, int count, int n, perm_c128_t* out,
+                                 perm_dd_c128_t* out_dd) {
+    if (!out || count < 0 || (count > 0 && !partials)) return PERM_E_ARG;
+    perm_status_t st = check_order(n);
+    if (st != PERM_OK) return st;
+    ddc acc;
+    acc.re.hi = acc.re.lo = acc.im.hi = acc.im.lo = 0.0;
+    for (int k = 0; k < count; k++) {
+        ddc v;
+        v.re.hi = partials[k].hi_re;
+        v.re.lo = partials[k].lo_re;
+        v.im.hi = partials[k].hi_im;
+        v.im.lo = partials[k].lo_im;
+        acc = perm::ddc_add(acc, v);
+    }
+    const double f = (n & 1) ? -2.0 : 2.0;
+    acc.re.hi *= f; acc.re.lo *= f; acc.im.hi *= f; acc.im.lo *= f;
+    out->re = acc.re.hi + acc.re.lo;
+    out->im = acc.im.hi + acc.im.lo;
+    if (out_dd) {
+        out_dd->hi_re = acc.re.hi;
+        out_dd->lo_re = acc.re.lo;
+        out_dd->hi_im = acc.im.hi;
+        out_dd->lo_im = acc.im.lo;
+    }
+    return PERM_OK;
+}
+
+perm_status_t perm_c128_batched(const perm_c128_t* A_dev, int n, int64_t B, perm_c128_t* per_dev,
+                                double* abs2_dev, void* stream) {
+    g_launches = 0;
+    if (B < 0) return PERM_E_ARG;
+    if (n < 1 || n > perm::kMaxBatchedN) return PERM_E_ORDER;
+    if (B == 0) return PERM_OK;
+    if (!A_dev || (!per_dev && !abs2_dev)) return PERM_E_ARG;
+    int launches = 0;
+    cudaError_t e = perm::batched_launch((const double2*)A_dev, n, B, (double2*)per_dev, abs2_dev,
+                                         (cudaStream_t)stream, &launches);
+    if (e != cudaSuccess) return cuda_fail(e, "batched kernel launch");
+    g_launches = (uint32_t)launches;
+    return PERM_OK;
+}
+
+perm_status_t perm_int01_workspace_bytes(int n, int64_t B, size_t* bytes) {
+    if (!bytes || B < 0) return PERM_E_ARG;
+    if (n < 1 || n > perm::kMaxInt01N) return PERM_E_ORDER;
+    const int64_t chunk = B < 65535 ? B : 65535;
+    *bytes = perm::int01_workspace_bytes(n, chunk > 0 ? chunk : 1);
+    return PERM_OK;
+}
+
+perm_status_t perm_int01(const uint8_t* A_dev, int n, int64_t B, perm_i128_t* out_dev, void* workspace,
+                         size_t workspace_bytes, void* stream) {
+    g_launches = 0;
+    if (B < 0) return PERM_E_ARG;
+    if (n < 1 || n > perm::kMaxInt01N) return PERM_E_ORDER;
+    if (B == 0) return PERM_OK;
+    if (!A_dev || !out_dev) return PERM_E_ARG;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t step = 65535;
+    const size_t need = perm::int01_workspace_bytes(n, B < step ? B : step);
+    char* ws = (char*)workspace;
+    bool own = false;
+    if (!ws) {
+        PERM_CUDA(cudaMallocAsync((void**)&ws, need, s), "cudaMallocAsync(workspace)");
+        own = true;
+    } else if (workspace_bytes < need) {
+        return PERM_E_WORKSPACE;
+    }
+    perm_status_t result = PERM_OK;
+    uint32_t launches = 0;
+    for (int64_t b0 = 0; b0 < B && result == PERM_OK; b0 += step) {
+        const int64_t nb = (B - b0) < step ? (B - b0) : step;
+        int flag = 0, l = 0;
+        cudaError_t e = perm::int01_launch(A_dev + b0 * n * n, n, nb, out_dev + b0, ws, need, s, &flag, &l);
+        launches += (uint32_t)l;
+        if (e != cudaSuccess) result = cuda_fail(e, "int01 kernel");
+        else if (flag & 1) result = PERM_E_NOT01;
+        else if (flag & 2) result = PERM_E_CHECK;
+    }
+    if (own) cudaFreeAsync(ws, s);
+    if (result == PERM_OK) g_launches = launches;
+    return result;
+}
+
+perm_status_t perm_c128_seed(const perm_c128_t* A, int n, const uint64_t* ranks, int count, perm_c128_t* w_out,
+                             void* stream) {
+    g_launches = 0;
+    if (!A || !ranks || !w_out || count < 0) return PERM_E_ARG;
+    perm_status_t st = check_order(n);
+    if (st != PERM_OK) return st;
+    for (int k = 0; k < count; k++)
+        if (n < 64 && ranks[k] >= (1ull << (n - 1))) return PERM_E_ORDER;
+    if (count == 0) return PERM_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t a_bytes = (size_t)n * n * sizeof(double2);
+    const size_t r_bytes = (size_t)count * sizeof(uint64_t);
+    const size_t w_bytes = (size_t)count * n * sizeof(double2);
+    char* ws = nullptr;
+    PERM_CUDA(cudaMallocAsync((void**)&ws, align256(a_bytes) + align256(r_bytes) + w_bytes, s), "cudaMallocAsync");
+    char* a_d = ws;
+    char* r_d = ws + align256(a_bytes);
+    char* w_d = r_d + align256(r_bytes);
+    perm_status_t result = PERM_OK;
+    do {
+        const bool a_dev = is_device_ptr(A);
+        cudaError_t e = cudaMemcpyAsync(a_d, A, a_bytes, a_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(r_d, ranks, r_bytes, cudaMemcpyHostToDevice, s);
+        if (e != cudaSuccess) { result = cuda_fail(e, "cudaMemcpyAsync"); break; }
+        const bool w_dev = is_device_ptr(w_out);
+        e = perm::walk_seed_launch_n(n, (const double2*)a_d, (const uint64_t*)r_d, count,
+                                     w_dev ? (double2*)w_out : (double2*)w_d, s);
+        if (e != cudaSuccess) { result = cuda_fail(e, "seed kernel launch"); break; }
+        if (!w_dev) {
+            e = cudaMemcpyAsync(w_out, w_d, w_bytes, cudaMemcpyDeviceToHost, s);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+            if (e != cudaSuccess) { result = cuda_fail(e, "cudaMemcpyAsync(w)"); break; }
+        }
+        g_launches = 1;
+    } while (0);
+    cudaFreeAsync(ws, s);
+    return result;
+}
+
+perm_status_t perm_fp64_probe(int blocks, int threads, int iters, double* sink_dev, void* stream) {
+    if (blocks < 1 || threads < 1 || threads > 1024 || iters < 0 || !sink_dev) return PERM_E_ARG;
+    cudaError_t e = perm::fp64_probe_launch(blocks, threads, iters, sink_dev, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "fp64 probe launch");
+    g_launches = 1;
+    return PERM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,282 @@
+// int01.cu -- exact permanents of 0-1 matrices (BASELINE config 3).
+//
+// Same Gray walk as the complex path (App. A), in integers: with g_i = 2 w_i,
+//     g_i(x) = a_{i,n} - sum_{j<n} a_ij + 2 sum_{j<n, x_j=1} a_ij    in [-n, n]   (int32)
+//     Sum = sum_r (-1)^{r+1} prod_i g_i(gray r)  =  2^n * P(0, 2^{n-1})
+//     per = 2 (-1)^n P  =  (-1)^n Sum / 2^{n-1}.
+// Products: rows in groups of 6 in int32 (n^6 < 2^31 for n <= 28), pairs of groups in int64,
+// then 64x64 -> 128 (and a further 128x64 for n > 24) modulo 2^128; the signed sum is kept mod 2^128
+// in unsigned __int128.  The result is exact when |Sum| = 2^{n-1} per <= 2^{n-1} n! < 2^127, i.e.
+// n <= 28 (R10); the low n-1 bits of Sum must be zero (self-check, PERM_E_CHECK).
+//
+// Mapping: grid (blocks_per_matrix, B); each block stages its matrix (validating 0/1 bytes) in shared
+// memory as int32 column increments 2 a_ij; each thread walks aligned chunks of 2^E ranks with the
+// unrolled inner block of 2^U steps (compile-time columns and signs, warp-uniform broadcast loads).
+// Per-block partial sums (exact, order-free) go to the workspace; a final kernel adds them per
+// matrix, checks divisibility and writes per as int128.
+#include "internal.h"
+
+namespace perm {
+
+typedef unsigned __int128 u128;
+
+template <int N>
+struct I01Cfg {
+    static constexpr int U = walk_inner_bits(N);
+    static constexpr int NT = 128;
+};
+
+__device__ __forceinline__ int lds_i(uint32_t addr) {
+    int v;
+    asm volatile("ld.volatile.shared.s32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+
+// prod_i g_i mod 2^128.
+template <int N>
+__device__ __forceinline__ u128 int_product(const int (&g)[N]) {
+    constexpr int NG = (N + 5) / 6;
+    int p[NG];
+#pragma unroll
+    for (int k = 0; k < NG; k++) {
+        p[k] = g[6 * k];
+#pragma unroll
+        for (int i = 6 * k + 1; i < 6 * k + 6 && i < N; i++) p[k] *= g[i];
+    }
+    if constexpr (NG == 1) {
+        return (u128)(__int128)(long long)p[0];
+    } else {
+        constexpr int NQ = (NG + 1) / 2;
+        long long q[NQ];
+#pragma unroll
+        for (int k = 0; k < NQ; k++)
+            q[k] = (2 * k + 1 < NG) ? (long long)p[2 * k] * (long long)p[2 * k + 1] : (long long)p[2 * k];
+        if constexpr (NQ == 1) {
+            return (u128)(__int128)q[0];
+        } else {
+            // signed 64 x 64 -> 128
+            unsigned long long lo = (unsigned long long)q[0] * (unsigned long long)q[1];
+            unsigned long long hi = (unsigned long long)__mul64hi(q[0], q[1]);
+#pragma unroll
+            for (int k = 2; k < NQ; k++) {
+                const unsigned long long yl = (unsigned long long)q[k];
+                const unsigned long long nl = lo * yl;
+                unsigned long long nh = __umul64hi(lo, yl) + hi * yl;
+                if (q[k] < 0) nh -= lo;
+                lo = nl;
+                hi = nh;
+            }
+            return ((u128)hi << 64) | (u128)lo;
+        }
+    }
+}
+
+template <int N, int SIGN>
+__device__ __forceinline__ void int_term(const int (&g)[N], u128& acc) {
+    const u128 p = int_product<N>(g);
+    if (SIGN > 0) acc += p; else acc -= p;
+}
+
+template <int N>
+__device__ __forceinline__ void int_flip_dyn(uint32_t col, int z, int (&g)[N]) {
+#pragma unroll
+    for (int i = 0; i < N; i++) g[i] += z * lds_i(col + 4 * i);
+}
+
+template <int N, int U, int T>
+struct IntInner {
+    static __device__ __forceinline__ void run(uint32_t sc, int (&g)[N], int zmid, u128& acc) {
+        if constexpr (T > 0) {
+            constexpr int J = ctz_c((unsigned)T);
+            if constexpr (J == U - 1) {
+                int_flip_dyn<N>(sc + 4u * (uint32_t)(J * N), zmid, g);
+            } else {
+                constexpr bool PLUS = ((T >> (J + 1)) & 1) == 0;
+#pragma unroll
+                for (int i = 0; i < N; i++) {
+                    const int a = lds_i(sc + 4u * (uint32_t)(J * N + i));
+                    if (PLUS) g[i] += a; else g[i] -= a;
+                }
+            }
+        }
+        if constexpr (T & 1) int_term<N, +1>(g, acc);
+        else                 int_term<N, -1>(g, acc);
+        if constexpr (T + 1 < (1 << U)) IntInner<N, U, T + 1>::run(sc, g, zmid, acc);
+    }
+};
+
+template <int N>
+__device__ __forceinline__ void int_seed(uint32_t sc, uint32_t sbase, uint64_t x, int j0, int (&g)[N]) {
+#pragma unroll
+    for (int i = 0; i < N; i++) g[i] = lds_i(sbase + 4 * i);
+    for (int j = j0; j < N - 1; j++) {
+        const int f = (int)((x >> j) & 1ull);
+        int_flip_dyn<N>(sc + 4u * (uint32_t)(j * N), f, g);
+    }
+}
+
+template <int N>
+__device__ __forceinline__ void int_chunk(uint32_t sc, uint32_t sbase, uint64_t c, int e, u128& acc) {
+    constexpr int U = I01Cfg<N>::U;
+    int g[N];
+    if (e == 0) {
+        int_seed<N>(sc, sbase, c ^ (c >> 1), 0, g);
+        if (c & 1ull) int_term<N, +1>(g, acc); else int_term<N, -1>(g, acc);
+        return;
+    }
+    if constexpr (U >= 1) {
+        const uint64_t x = ((c ^ (c >> 1)) << e) | ((c & 1ull) << (e - 1));
+        int_seed<N>(sc, sbase, x, e - 1, g);
+        const uint64_t nblk = 1ull << (e - U);
+        const uint64_t cpar = c & 1ull;
+        for (uint64_t q = 0; q < nblk; q++) {
+            if (q > 0) {
+                const int j = U + __ffsll((long long)q) - 1;
+                const uint64_t nb = (j + 1 < e) ? ((q >> (j + 1 - U)) & 1ull) : cpar;
+                int_flip_dyn<N>(sc + 4u * (uint32_t)(j * N), nb ? -1 : 1, g);
+            }
+            const uint64_t nbm = (U < e) ? (q & 1ull) : cpar;
+            IntInner<N, U, 0>::run(sc, g, nbm ? -1 : 1, acc);
+        }
+    }
+}
+
+// ws layout: [int flag][pad to 16][u128 partials[B][nblk]]
+template <int N>
+__global__ void __launch_bounds__(I01Cfg<N>::NT) int01_kernel(const uint8_t* __restrict__ A, int e,
+                                                              uint64_t chunks, u128* __restrict__ partials,
+                                                              int* __restrict__ flag) {
+    __shared__ int s_col[N * N];   // s_col[j*N + i] = 2 a_ij
+    __shared__ int s_base[N];      // a_{i,n} - sum_{j<n} a_ij
+    const int64_t m = blockIdx.y;
+    const uint8_t* a = A + m * (N * N);
+    for (int k = threadIdx.x; k < N * N; k += blockDim.x) {
+        const int v = a[k];
+        if (v > 1) atomicOr(flag, 1);
+        const int i = k / N, j = k - i * N;
+        s_col[j * N + i] = 2 * (v & 1);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < N; i += blockDim.x) {
+        int s = 0;
+        for (int j = 0; j < N - 1; j++) s += s_col[j * N + i];
+        s_base[i] = s_col[(N - 1) * N + i] / 2 - s / 2;
+    }
+    __syncthreads();
+    const uint32_t sc = (uint32_t)__cvta_generic_to_shared(s_col);
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(s_base);
+    u128 acc = 0;
+    const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; c < chunks; c += T)
+        int_chunk<N>(sc, sbase, c, e, acc);
+    // block reduction (exact; order irrelevant)
+    unsigned long long lo = (unsigned long long)acc, hi = (unsigned long long)(acc >> 64);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        const unsigned long long olo = __shfl_down_sync(0xffffffffu, lo, off);
+        const unsigned long long ohi = __shfl_down_sync(0xffffffffu, hi, off);
+        const u128 s = (((u128)hi << 64) | lo) + (((u128)ohi << 64) | olo);
+        lo = (unsigned long long)s;
+        hi = (unsigned long long)(s >> 64);
+    }
+    __shared__ u128 s_w[I01Cfg<N>::NT / 32];
+    if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = ((u128)hi << 64) | lo;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        u128 t = 0;
+        for (int w = 0; w < I01Cfg<N>::NT / 32; w++) t += s_w[w];
+        partials[m * gridDim.x + blockIdx.x] = t;
+    }
+}
+
+__global__ void int01_final_kernel(const u128* __restrict__ partials, int nblk, int64_t B, int n,
+                                   unsigned long long* __restrict__ out, int* __restrict__ flag) {
+    const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (m >= B) return;
+    u128 s = 0;
+    for (int k = 0; k < nblk; k++) s += partials[m * nblk + k];
+    const u128 mask = (((u128)1) << (n - 1)) - 1;
+    if (s & mask) atomicOr(flag, 2);
+    __int128 v = (__int128)s >> (n - 1);          // arithmetic shift: Sum / 2^{n-1}
+    if (n & 1) v = -v;                            // per = (-1)^n Sum / 2^{n-1}
+    out[2 * m] = (unsigned long long)v;
+    out[2 * m + 1] = (unsigned long long)((u128)v >> 64);
+}
+
+struct I01Plan {
+    int e;
+    int nblk;
+    uint64_t chunks;
+};
+
+static I01Plan int01_plan(int n, int64_t B) {
+    // threads per matrix ~ max(128, 148*16*128 / B) (a few waves of the whole chip), chunk >= 2^U
+    const int U = walk_inner_bits(n);
+    const uint64_t total = 1ull << (n - 1);
+    int64_t want_threads = (int64_t)148 * 16 * 128 / (B > 0 ? B : 1);
+    if (want_threads < 128) want_threads = 128;
+    int e = n - 1;
+    while (e > U && (total >> e) < (uint64_t)want_threads * 4) e--;
+    if (n == 1) e = 0;
+    I01Plan p;
+    p.e = e;
+    p.chunks = total >> e;
+    uint64_t blocks = (p.chunks + 127) / 128;
+    const uint64_t cap = (uint64_t)((want_threads + 127) / 128);
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    p.nblk = (int)blocks;
+    return p;
+}
+
+size_t int01_workspace_bytes(int n, int64_t B) {
+    const I01Plan p = int01_plan(n, B);
+    return 16 + (size_t)B * p.nblk * sizeof(u128);
+}
+
+template <int N>
+cudaError_t int01_launch_t(const uint8_t* A, int64_t B, const I01Plan& p, u128* partials, int* flag,
+                           cudaStream_t s) {
+    dim3 grid((unsigned)p.nblk, (unsigned)B);
+    int01_kernel<N><<<grid, I01Cfg<N>::NT, 0, s>>>(A, p.e, p.chunks, partials, flag);
+    return cudaGetLastError();
+}
+
+#define PERM_R8(M, b) M(b + 1) M(b + 2) M(b + 3) M(b + 4) M(b + 5) M(b + 6) M(b + 7) M(b + 8)
+
+cudaError_t int01_launch(const uint8_t* A, int n, int64_t B, void* out, void* ws, size_t ws_bytes,
+                         cudaStream_t s, int* flag_host_status, int* launches) {
+    *launches = 0;
+    *flag_host_status = 0;
+    if (B == 0) return cudaSuccess;
+    if (B > 65535) return cudaErrorInvalidValue;   // gridDim.y; the ABI layer splits larger batches
+    const I01Plan p = int01_plan(n, B);
+    int* flag = (int*)ws;
+    u128* partials = (u128*)((char*)ws + 16);
+    cudaError_t err = cudaMemsetAsync(flag, 0, sizeof(int), s);
+    if (err != cudaSuccess) return err;
+    switch (n) {
+#define PERM_CASE(N) case N: err = int01_launch_t<N>(A, B, p, partials, flag, s); break;
+        PERM_R8(PERM_CASE, 0) PERM_R8(PERM_CASE, 8) PERM_R8(PERM_CASE, 16)
+        PERM_CASE(25) PERM_CASE(26) PERM_CASE(27) PERM_CASE(28)
+#undef PERM_CASE
+        default: return cudaErrorInvalidValue;
+    }
+    if (err != cudaSuccess) return err;
+    const int threads = 128;
+    int01_final_kernel<<<(unsigned)((B + threads - 1) / threads), threads, 0, s>>>(
+        partials, p.nblk, B, n, (unsigned long long*)out, flag);
+    err = cudaGetLastError();
+    if (err != cudaSuccess) return err;
+    *launches = 2;
+    int hflag = 0;
+    err = cudaMemcpyAsync(&hflag, flag, sizeof(int), cudaMemcpyDeviceToHost, s);
+    if (err != cudaSuccess) return err;
+    err = cudaStreamSynchronize(s);
+    if (err != cudaSuccess) return err;
+    *flag_host_status = hflag;
+    (void)ws_bytes;
+    return cudaSuccess;
+}
+
+}  // namespace perm

@@ -1,0 +1,68 @@
+// internal.h -- host-side launch interfaces between the C-ABI layer (abi.cu) and the kernel
+// translation units.  Not part of the public ABI (see include/perm.h).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace perm {
+
+constexpr int kMaxN = 64;          // ranks are 64-bit words
+constexpr int kMaxBatchedN = 32;   // perm_c128_batched
+constexpr int kMaxInt01N = 28;     // exactness bound of the int128 Glynn sum (R10)
+constexpr int kMaxSegments = 96;
+
+// Inner unrolled Gray bits U(N) of the single-matrix walk: a block of 2^U consecutive ranks is
+// fully unrolled, so the columns 0..U-1 it touches are compile-time operands.
+#ifndef PERM_WALK_U
+#define PERM_WALK_U 3
+#endif
+__host__ __device__ constexpr int walk_inner_bits(int n) { return (n - 1) < PERM_WALK_U ? (n - 1) : PERM_WALK_U; }
+constexpr int kWalkThreads = 64;
+
+// A run of `count` aligned chunks of 2^e ranks: chunk k covers ranks [(c0+k) 2^e, (c0+k+1) 2^e).
+// e == 0 chunks are single terms (seeded from scratch).
+struct Segment {
+    uint64_t c0;
+    uint64_t count;
+    int e;
+};
+
+struct WalkLaunch {
+    const double2* A_dev;   // device, row-major n x n
+    const double2* A_host;  // host, row-major n x n (inner columns go into the kernel parameters)
+    int n;
+    int nseg;
+    Segment seg[kMaxSegments];
+    ddc* partials;          // device, one per block
+    int grid;
+    cudaStream_t stream;
+};
+
+// Defined in walk_inst.cu (explicit instantiations over N = 1..64).
+template <int N> cudaError_t walk_launch(const WalkLaunch& L);
+template <int N> cudaError_t walk_occupancy(int* blocks_per_sm, int* threads_per_block);
+template <int N> cudaError_t walk_seed_launch(const double2* A_dev, const uint64_t* ranks_dev, int count,
+                                              double2* w_out, cudaStream_t s);
+
+cudaError_t walk_launch_n(int n, const WalkLaunch& L);
+cudaError_t walk_occupancy_n(int n, int* blocks_per_sm, int* threads_per_block);
+cudaError_t walk_seed_launch_n(int n, const double2* A_dev, const uint64_t* ranks_dev, int count,
+                               double2* w_out, cudaStream_t s);
+
+// reduce.cu
+cudaError_t reduce_launch(const ddc* parts, int count, int n_final, ddc* out_dd, double2* out_c,
+                          cudaStream_t s);
+cudaError_t fp64_probe_launch(int blocks, int threads, int iters, double* sink, cudaStream_t s);
+
+// batched.cu
+cudaError_t batched_launch(const double2* A, int n, int64_t B, double2* per, double* abs2, cudaStream_t s,
+                           int* launches);
+
+// int01.cu
+size_t int01_workspace_bytes(int n, int64_t B);
+cudaError_t int01_launch(const uint8_t* A, int n, int64_t B, void* out, void* ws, size_t ws_bytes,
+                         cudaStream_t s, int* flag_host_status, int* launches);
+
+}  // namespace perm

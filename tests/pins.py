@@ -87,3 +87,10 @@ def scaled_error(got: complex, ref: complex, A: np.ndarray) -> float:
 def scaled_floor(A: np.ndarray) -> float:
     n = A.shape[0]
     return 2.0 ** (-n / 2) * float(np.prod(np.linalg.norm(A, axis=1)))
+
+
+def range_scale(A: np.ndarray, length: int) -> float:
+    """Typical magnitude of a sum of `length` Gray terms: sqrt(length) * 2^{-n} prod_i ||a_i||_2
+    (each |w_i| ~ ||a_i||/2, random signs)."""
+    n = A.shape[0]
+    return float(np.sqrt(max(length, 1))) * 2.0 ** (-n) * float(np.prod(np.linalg.norm(A, axis=1)))

@@ -1,0 +1,69 @@
+"""CPU-side checks of the C-ABI library: it loads, exports every symbol include/perm.h declares, and
+the host-only logic (argument validation, status strings, perm_c128_finalize) behaves as documented.
+No compute call is made (no GPU here)."""
+from __future__ import annotations
+
+import ctypes
+import math
+
+import numpy as np
+import pytest
+
+import paper_1904_06229_b200 as pb
+
+
+def test_library_exports_every_header_symbol():
+    L = pb.lib()
+    names = pb.header_functions()
+    assert len(names) >= 12
+    for name in names:
+        assert hasattr(L, name), name
+    assert L.perm_version() == 1
+
+
+def test_status_strings():
+    L = pb.lib()
+    for code in range(8):
+        assert L.perm_status_string(code).decode()
+    assert L.perm_status_string(0).decode() == "ok"
+
+
+def test_validation_without_gpu():
+    L = pb.lib()
+    A = np.eye(3, dtype=np.complex128)
+    out = pb.c128()
+    p = A.ctypes.data_as(ctypes.c_void_p)
+    assert L.perm_c128(p, 0, ctypes.byref(out), None, None, 0, None, None) == 2          # n < 1
+    assert L.perm_c128(p, 65, ctypes.byref(out), None, None, 0, None, None) == 2         # n > 64
+    assert L.perm_c128(None, 3, ctypes.byref(out), None, None, 0, None, None) == 1       # null A
+    assert L.perm_c128(p, 3, None, None, None, 0, None, None) == 1                       # null out
+    d = pb.dd_c128()
+    assert L.perm_c128_range(p, 3, 3, 2, ctypes.byref(d), None, 0, None, None) == 1      # k0 > k1
+    assert L.perm_c128_range(p, 3, 0, 5, ctypes.byref(d), None, 0, None, None) == 2      # k1 > 2^{n-1}
+    assert L.perm_c128_batched(None, 33, 1, None, None, None) == 2                       # n > 32
+    assert L.perm_c128_batched(None, 8, -1, None, None, None) == 1                       # B < 0
+    assert L.perm_c128_batched(None, 8, 0, None, None, None) == 0                        # B == 0: no-op
+    assert L.perm_int01(None, 29, 1, None, None, 0, None) == 2                           # n > 28
+    assert L.perm_int01(None, 24, 0, None, None, 0, None) == 0                           # B == 0: no-op
+    b = ctypes.c_size_t()
+    assert L.perm_int01_workspace_bytes(24, 64, ctypes.byref(b)) == 0 and b.value > 16
+
+
+def test_finalize_ordered_dd():
+    # 2(-1)^n * sum of partials; the dd sum recovers the sentinel {1e16, 1, -1e16} -> 1 (C7 / S:162)
+    parts = [(1e16, 0.0, 0.0, 0.0), (1.0, 0.0, 0.0, 0.0), (-1e16, 0.0, 0.0, 0.0)]
+    assert pb.perm_c128_finalize(parts, 2) == 2.0
+    assert pb.perm_c128_finalize(parts, 3) == -2.0
+    # App. A n = 3 trace: S = -463/2 split over four ranks
+    terms = [0.0, 45 / 4, -1125 / 4, 77 / 2]
+    assert pb.perm_c128_finalize([(t, 0.0, 0.0, 0.0) for t in terms], 3) == 463
+    v, d = pb.perm_c128_finalize([(1.0, 2.0 ** -60, -3.0, 0.0)], 4, return_dd=True)
+    assert v == complex(2.0, -6.0) and d.lo_re == 2.0 ** -59
+    assert pb.perm_c128_finalize([], 5) == 0
+
+
+def test_finalize_errors():
+    with pytest.raises(pb.PermError):
+        pb.perm_c128_finalize([(1, 0, 0, 0)], 0)
+    with pytest.raises(pb.PermError):
+        pb.perm_c128_finalize([(1, 0, 0, 0)], 65)

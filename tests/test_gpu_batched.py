@@ -1,0 +1,106 @@
+"""GPU parity of perm_c128_batched (BASELINE config 2) against the CPU oracle."""
+from __future__ import annotations
+
+import itertools
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_1904_06229_b200 as pb
+from paper_1904_06229_b200 import inputs
+from tests import pins
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-9
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch
+    assert torch.cuda.is_available()
+    return torch
+
+
+def _check_batch(torch, A, ref):
+    per, abs2 = pb.perm_c128_batched(torch.from_numpy(A).cuda())
+    torch.cuda.synchronize()
+    per = per.cpu().numpy()
+    abs2 = abs2.cpu().numpy()
+    for b in range(A.shape[0]):
+        assert pins.scaled_error(per[b], ref[b], A[b]) <= TOL, (b, per[b], ref[b])
+        assert abs2[b] == per[b].real ** 2 + per[b].imag ** 2
+
+
+@pytest.mark.parametrize("n", list(range(1, 15)))
+def test_random_small_batches(torch, n):
+    B = 37 if n <= 10 else 9          # ragged: not a multiple of matrices-per-warp
+    A = inputs.complex_gaussian((B, n, n), 500 + n)
+    _check_batch(torch, A, oracle.ryser_batch(A))
+
+
+@pytest.mark.parametrize("n", [16, 20, 24])
+def test_larger_orders(torch, n):
+    A = inputs.complex_gaussian((3, n, n), 600 + n)
+    ref = np.array([oracle.permanent_hr(A[b]).value for b in range(3)])
+    _check_batch(torch, A, ref)
+
+
+def test_empty_batch_and_errors(torch):
+    A = torch.zeros((0, 8, 8), dtype=torch.complex128, device="cuda")
+    per, abs2 = pb.perm_c128_batched(A)
+    assert per.numel() == 0
+    with pytest.raises(pb.PermError):
+        pb.perm_c128_batched(torch.zeros((1, 33, 33), dtype=torch.complex128, device="cuda"))
+
+
+def test_identity_and_ones(torch):
+    for n in (1, 4, 8, 12, 16):
+        A = np.stack([np.eye(n), np.ones((n, n))]).astype(np.complex128)
+        per, _ = pb.perm_c128_batched(torch.from_numpy(A).cuda())
+        per = per.cpu().numpy()
+        assert per[0] == 1
+        assert abs(per[1] - math.factorial(n)) <= 1e-13 * math.factorial(n)
+
+
+@pytest.mark.parametrize("m,n", [(9, 3), (16, 4), (25, 5)])
+def test_boson_sampling_normalization(torch, m, n):
+    """P13: sum_T |per(U_{S,T})|^2 / prod t_j! = 1 over all output multisets T (unitarity)."""
+    U = inputs.haar_unitary(m, 900 + m)
+    S = np.arange(n)
+    mats, w = [], []
+    for T in itertools.combinations_with_replacement(range(m), n):
+        mats.append(U[np.ix_(S, list(T))])
+        cnt = np.bincount(np.array(T), minlength=m)
+        w.append(1.0 / float(np.prod([math.factorial(int(k)) for k in cnt])))
+    A = torch.from_numpy(np.ascontiguousarray(np.array(mats))).cuda()
+    _, abs2 = pb.perm_c128_batched(A, want_per=False)
+    total = float(np.sum(abs2.cpu().numpy() * np.array(w)))
+    assert abs(total - 1.0) < 1e-12, total
+
+
+@pytest.mark.parametrize("n", [8, 12, 16, 20])
+def test_cfg2_full_batch_samples(torch, golden_dir, n):
+    """Config 2 at full size (10^5 submatrices, the bench launch): sampled outputs vs the oracle,
+    plus the Haar expectation E|per|^2 = n!(m-1)!/(m+n-1)! (P14) as a statistical check."""
+    A = inputs.cfg2(n)
+    per, abs2 = pb.perm_c128_batched(torch.from_numpy(A).cuda())
+    per = per.cpu().numpy()
+    abs2 = abs2.cpu().numpy()
+    p = os.path.join(golden_dir, "oracle_values.json")
+    g = json.load(open(p)).get("cfg2", {}).get(str(n)) if os.path.exists(p) else None
+    if g:
+        idx = np.array(g["index"])
+        ref = np.array(g["re"]) + 1j * np.array(g["im"])
+    else:
+        idx = np.sort(np.random.default_rng(9000 + n).choice(A.shape[0], 8, replace=False))
+        ref = np.array([oracle.permanent_hr(A[i]).value for i in idx])
+    for i, r in zip(idx, ref):
+        assert pins.scaled_error(per[i], r, A[i]) <= TOL, (n, i)
+    m = n * n
+    expect = math.exp(math.lgamma(n + 1) + math.lgamma(m) - math.lgamma(m + n))
+    se = np.std(abs2) / np.sqrt(len(abs2))
+    assert abs(np.mean(abs2) - expect) < 6 * se, (np.mean(abs2), expect, se)

@@ -1,0 +1,68 @@
+"""GPU parity of perm_int01 (BASELINE config 3): bit-exact against the CPU oracle."""
+from __future__ import annotations
+
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_1904_06229_b200 as pb
+from paper_1904_06229_b200 import inputs
+from tests import pins
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch
+    assert torch.cuda.is_available()
+    return torch
+
+
+def _run(torch, A):
+    return pb.perm_int01(torch.from_numpy(np.ascontiguousarray(A, dtype=np.uint8)).cuda())
+
+
+@pytest.mark.parametrize("n", list(range(1, 15)))
+def test_random_vs_oracle(torch, n):
+    A = inputs.bernoulli01((13, n, n), 700 + n)
+    assert _run(torch, A) == oracle.ryser_i01_batch(A)
+
+
+def test_dense_and_sparse(torch):
+    rng = np.random.default_rng(5)
+    for p in (0.1, 0.5, 0.9):
+        A = (rng.random((5, 12, 12)) < p).astype(np.uint8)
+        assert _run(torch, A) == oracle.ryser_i01_batch(A)
+
+
+@pytest.mark.parametrize("n", [20, 24, 26, 28])
+def test_closed_forms(torch, n):
+    mats = [np.ones((n, n), np.uint8), np.eye(n, dtype=np.uint8), pins.j_minus_i(n), pins.tridiagonal_ones(n),
+            pins.hessenberg_ones(n), pins.identity_plus_shift(n), pins.menage_matrix(n),
+            np.zeros((n, n), np.uint8)]
+    expect = [math.factorial(n), 1, pins.derangements(n), pins.fibonacci(n + 1), 2 ** (n - 1), 2, pins.menage(n), 0]
+    assert _run(torch, np.stack(mats)) == expect
+
+
+def test_cfg3_bit_exact(torch, golden_dir):
+    A = inputs.cfg3()
+    p = os.path.join(golden_dir, "oracle_values.json")
+    g = json.load(open(p)).get("cfg3") if os.path.exists(p) else None
+    ref = [int(v) for v in g["values"]] if g else oracle.ryser_i01_batch(A)
+    assert _run(torch, A) == ref
+
+
+def test_not01_and_empty(torch):
+    A = np.ones((2, 6, 6), np.uint8)
+    A[1, 2, 3] = 2
+    with pytest.raises(pb.PermError) as e:
+        _run(torch, A)
+    assert e.value.name == "PERM_E_NOT01"
+    assert pb.perm_int01(torch.zeros((0, 5, 5), dtype=torch.uint8, device="cuda")) == []
+    with pytest.raises(pb.PermError):
+        _run(torch, np.ones((1, 29, 29), np.uint8))
