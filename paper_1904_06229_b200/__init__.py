@@ -23,7 +23,7 @@ from dataclasses import dataclass
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_PKG, "libperm.so")
+_LIB_PATH = os.environ.get("PERM_LIB") or os.path.join(_PKG, "libperm.so")
 _HEADER = os.path.join(os.path.dirname(_PKG), "include", "perm.h")
 
 STATUS = {0: "PERM_OK", 1: "PERM_E_ARG", 2: "PERM_E_ORDER", 3: "PERM_E_NONFINITE", 4: "PERM_E_NOT01",

@@ -17,8 +17,12 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-BUILD = os.path.join(PKG, "build")
-LIB = os.path.join(PKG, "libperm.so")
+# Development variants: PERM_VARIANT=<name> PERM_EXTRA_FLAGS="-DPERM_WALK_U=2 ..." builds
+# build_<name>/ and libperm_<name>.so (loaded when PERM_LIB points at it); the default build has neither.
+_VARIANT = os.environ.get("PERM_VARIANT", "")
+BUILD = os.path.join(PKG, "build" + (f"_{_VARIANT}" if _VARIANT else ""))
+LIB = os.path.join(PKG, "libperm" + (f"_{_VARIANT}" if _VARIANT else "") + ".so")
+EXTRA = os.environ.get("PERM_EXTRA_FLAGS", "").split() if _VARIANT else []
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -47,7 +51,7 @@ def _stale(obj: str, src: str) -> bool:
 def _compile(obj, src, extra):
     objp = os.path.join(BUILD, obj)
     srcp = os.path.join(CSRC, src)
-    cmd = [NVCC, *FLAGS, *extra, "-c", srcp, "-o", objp]
+    cmd = [NVCC, *FLAGS, *EXTRA, *extra, "-c", srcp, "-o", objp]
     r = subprocess.run(cmd, capture_output=True, text=True)
     with open(objp + ".log", "w") as f:
         f.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)

@@ -103,6 +103,7 @@ bool decompose(int n, uint64_t k0, uint64_t k1, int b, WalkPlan& p) {
     return true;
 }
 
+// max_grid: resident blocks of the walk kernel; nt: chunk walkers (lane groups) per block.
 perm_status_t device_threads(int n, int* max_grid, int* nt) {
     int dev = 0, sms = 0, bps = 0;
     PERM_CUDA(cudaGetDevice(&dev), "cudaGetDevice");
@@ -253,7 +254,7 @@ perm_status_t run_walk(const perm_c128_t* A, int n, uint64_t k0, uint64_t k1, in
         if (stats) {
             stats->terms = k1 - k0;
             stats->chunk_log2 = (uint32_t)p.b;
-            stats->threads = (uint32_t)(p.grid * p.threads);
+            stats->threads = (uint32_t)(p.grid * perm::kWalkThreads);
             stats->blocks = (uint32_t)p.grid;
             stats->launches = launches;
         }

@@ -63,12 +63,13 @@ __global__ void __launch_bounds__(BatCfg<N>::NT) batched_kernel(const double2* _
     ddc acc;
     acc.re.hi = acc.re.lo = acc.im.hi = acc.im.lo = 0.0;
     if (g < gcount) {
+        using WC = WCfg<N, 1>;   // one lane per chunk; column stride N (no padding)
         const uint32_t sc = (uint32_t)__cvta_generic_to_shared(wbase + g * C::SLOT);
         const uint32_t sbase = sc + (uint32_t)(N * N) * 16u;
         if constexpr (C::E == 0) {
-            single_term<N>(sc, sbase, (uint64_t)l, acc);
+            single_term<WC>(sc, sbase, 0u, (uint64_t)l, acc);
         } else {
-            walk_chunk<N>(sc, sbase, (uint64_t)l, C::E, acc);
+            walk_chunk<WC>(sc, sbase, 0u, (uint64_t)l, C::E, acc);
         }
     }
     // fixed-order tree over the L lanes of each group
@@ -80,14 +81,14 @@ __global__ void __launch_bounds__(BatCfg<N>::NT) batched_kernel(const double2* _
         const double im = (acc.im.hi + acc.im.lo) * f;
         const int64_t m = m0 + g;
         if (per) per[m] = make_double2(re, im);
-        if (abs2) abs2[m] = re * re + im * im;
+        if (abs2) abs2[m] = __dadd_rn(__dmul_rn(re, re), __dmul_rn(im, im));   // no FMA: fl(fl(re^2) + fl(im^2))
     }
 }
 
 template <int N>
 cudaError_t batched_launch_t(const double2* A, int64_t B, double2* per, double* abs2, cudaStream_t s) {
     using C = BatCfg<N>;
-    static_assert(C::E >= WalkCfg<N>::U || C::E == 0, "lane chunk shorter than the unrolled block");
+    static_assert(C::E >= WCfg<N, 1>::U || C::E == 0, "lane chunk shorter than the unrolled block");
     cudaError_t err = cudaFuncSetAttribute(batched_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)C::smem_bytes);
     if (err != cudaSuccess) return err;

@@ -20,6 +20,25 @@ constexpr int kMaxSegments = 96;
 #endif
 __host__ __device__ constexpr int walk_inner_bits(int n) { return (n - 1) < PERM_WALK_U ? (n - 1) : PERM_WALK_U; }
 constexpr int kWalkThreads = 64;
+// Lanes that share one chunk in the single-matrix walk (rows split between them, K1).  The n
+// complex row sums take 4n registers; beyond n = 48 one lane cannot hold them without spilling, so
+// two lanes split the rows.  (Splitting earlier, to raise occupancy, measured no faster on B200: the
+// walk is bound by FP64 operand bandwidth, not latency -- DESIGN.md "Walk kernel".)
+#ifndef PERM_WALK_S2_MIN
+#define PERM_WALK_S2_MIN 49
+#endif
+#ifndef PERM_WALK_S4_MIN
+#define PERM_WALK_S4_MIN 65
+#endif
+__host__ __device__ constexpr int walk_lanes_per_chunk(int n) {
+    return n >= PERM_WALK_S4_MIN ? 4 : (n >= PERM_WALK_S2_MIN ? 2 : 1);
+}
+// Plain-double partial sums are folded into the per-thread double-double accumulator every
+// 2^kWalkFoldBits terms (R7).
+#ifndef PERM_WALK_FOLD
+#define PERM_WALK_FOLD 5
+#endif
+constexpr int kWalkFoldBits = PERM_WALK_FOLD;
 
 // A run of `count` aligned chunks of 2^e ranks: chunk k covers ranks [(c0+k) 2^e, (c0+k+1) 2^e).
 // e == 0 chunks are single terms (seeded from scratch).
@@ -42,12 +61,12 @@ struct WalkLaunch {
 
 // Defined in walk_inst.cu (explicit instantiations over N = 1..64).
 template <int N> cudaError_t walk_launch(const WalkLaunch& L);
-template <int N> cudaError_t walk_occupancy(int* blocks_per_sm, int* threads_per_block);
+template <int N> cudaError_t walk_occupancy(int* blocks_per_sm, int* walkers_per_block);
 template <int N> cudaError_t walk_seed_launch(const double2* A_dev, const uint64_t* ranks_dev, int count,
                                               double2* w_out, cudaStream_t s);
 
 cudaError_t walk_launch_n(int n, const WalkLaunch& L);
-cudaError_t walk_occupancy_n(int n, int* blocks_per_sm, int* threads_per_block);
+cudaError_t walk_occupancy_n(int n, int* blocks_per_sm, int* walkers_per_block);
 cudaError_t walk_seed_launch_n(int n, const double2* A_dev, const uint64_t* ranks_dev, int count,
                                double2* w_out, cudaStream_t s);
 

@@ -8,36 +8,59 @@
 //   * step s -> s+1 flips Gray bit j = ctz(s+1) to 1 ^ bit_{j+1}(c 2^e + s + 1)        (nextset)
 //   * the term sign is (-1)^{s+1} because c 2^e is even                               (steps 3, 11-12)
 // so every step except the one at s+1 = 2^{e-1} is IDENTICAL for all chunks: the lanes of a warp walk
-// 32 different chunks in lock-step and every column operand is warp-uniform (a broadcast LDS.128 with
-// a uniform-register address).  Within a chunk a block of 2^U ranks is fully unrolled, so its flips
-// (columns 0..U-1) use compile-time shared-memory offsets and compile-time signs; the flip at the
-// block boundary (column j >= U, once per 2^U terms) uses a dynamic column and sign.
+// different chunks in lock-step and every column index is warp-uniform.  Within a chunk a block of
+// 2^U ranks is fully unrolled, so its flips (columns 0..U-1) use compile-time shared-memory offsets
+// and compile-time signs; the flip at the block boundary (column j >= U, once per 2^U terms) uses a
+// dynamic column and sign.
+//
+// Lanes per chunk S (1 or 2).  With S = 2 the two lanes of a pair walk the SAME chunk and split the
+// rows: lane h keeps the row sums of rows [hR, hR+R), R = ceil(n/2) (an odd n is padded with a
+// neutral row w = 1).  Each lane multiplies its R row sums; after every two terms the pair swaps one
+// partial product with a single shuffle (lane 0 finishes the even term, lane 1 the odd one), so the
+// FP64 work per term is unchanged (6n-4) while registers per thread halve -- at n = 44 that doubles
+// the resident warps, which is what the FP64 pipe needs to hide its latency.
 //
 // Per term: 2n DADD/DFMA (row-sum update) + 4(n-2) DMUL/DFMA (product, split
 // into K independent chains) + 4 DFMA (last multiply fused with the signed accumulation)
-// = 6n-4 FP64 instructions for ~8n flops.  The n row sums live in registers (4n 32-bit registers).
-// Column operands are loaded with ld.volatile.shared right before use: this keeps ptxas from
-// hoisting/CSE-ing the (loop-invariant) columns into registers, which at n = 44 would need another
-// 4n registers per column and spill.  Each 2^U-term block is summed in plain double and folded into
-// a per-thread double-double accumulator (TwoSum), then reduced warp -> block -> per-block partial
-// in HBM; reduce.cu adds the partials in a fixed order.
+// = 6n-4 FP64 instructions for ~8n flops.  Column operands are loaded with ld.volatile.shared right
+// before use: this keeps ptxas from hoisting/CSE-ing the (loop-invariant) columns into registers,
+// which at n = 44 would spill.  Plain-double sums over 2^kWalkFoldBits terms are folded into a
+// per-thread double-double accumulator (TwoSum), then reduced warp -> block -> per-block partial in
+// HBM; reduce.cu adds the partials in a fixed order.
 #pragma once
 #include "common.cuh"
 #include "internal.h"
 
 namespace perm {
 
-template <int N>
-struct WalkCfg {
+template <int N_, int S_>
+struct WCfg {
+    static constexpr int N = N_;
     static constexpr int U = walk_inner_bits(N);
+    static constexpr int S = S_;                             // lanes per chunk
+    static constexpr int R = (N + S - 1) / S;                // rows per lane
+    static constexpr int P = R * S;                          // padded rows per column in shared memory
     static constexpr int NT = kWalkThreads;
 #ifdef PERM_WALK_K
-    static constexpr int K = N >= 16 ? PERM_WALK_K : (N >= 4 ? 2 : 1);
+    static constexpr int K = R >= 16 ? PERM_WALK_K : (R >= 4 ? 2 : 1);
 #else
-    static constexpr int K = N >= 16 ? 2 : (N >= 4 ? 2 : 1);  // independent product chains
+    static constexpr int K = R >= 4 ? 2 : 1;                 // independent product chains per lane
 #endif
-    static constexpr size_t smem_bytes = (size_t)(N * N + N) * sizeof(double2);
+    static constexpr size_t smem_bytes = (size_t)(N * P + P) * sizeof(double2);
+    // Register budget per thread for S > 1: the 4R row-sum registers plus working set; it sets the
+    // minimum resident blocks in __launch_bounds__ so ptxas does not trade occupancy for scheduling
+    // freedom.  S = 1 is left uncapped (4n + ~30 registers).
+#ifdef PERM_WALK_REG_EXTRA
+    static constexpr int REGS = ((4 * R + PERM_WALK_REG_EXTRA + 7) / 8) * 8;
+#else
+    static constexpr int REGS = ((4 * R + 80 + 7) / 8) * 8;
+#endif
+    static constexpr int MINB_RAW = (S == 1) ? 1 : 65536 / (NT * (REGS < 255 ? REGS : 255));
+    static constexpr int MINB = MINB_RAW < 1 ? 1 : MINB_RAW;
 };
+
+template <int N>
+using WalkCfg = WCfg<N, walk_lanes_per_chunk(N)>;
 
 struct WalkParams {
     const double2* A;                      // device, row-major
@@ -48,7 +71,7 @@ struct WalkParams {
     int32_t nseg;
 };
 
-// Broadcast load of one complex entry from shared memory (volatile: never hoisted or merged).
+// Load of one complex entry from shared memory (volatile: never hoisted or merged).
 __device__ __forceinline__ double2 lds_c(uint32_t addr) {
     double2 v;
     asm volatile("ld.volatile.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
@@ -65,191 +88,303 @@ __device__ __forceinline__ void cmul2(double& xr, double& xi, double yr, double 
 }
 
 // Product of rows [B, E) into (pr, pi).
-template <int B, int E, int N>
-__device__ __forceinline__ void chain(const double (&wr)[N], const double (&wi)[N], double& pr, double& pi) {
+template <int B, int E, int R>
+__device__ __forceinline__ void chain(const double (&wr)[R], const double (&wi)[R], double& pr, double& pi) {
     pr = wr[B];
     pi = wi[B];
 #pragma unroll
     for (int i = B + 1; i < E; i++) cmul2(pr, pi, wr[i], wi[i]);
 }
 
-// acc += SIGN * prod_i w_i.   The last complex multiply is fused with the accumulation (4 DFMA).
-template <int N, int SIGN>
-__device__ __forceinline__ void term_acc(const double (&wr)[N], const double (&wi)[N], double& ar, double& ai) {
-    constexpr int K = WalkCfg<N>::K;
-    if constexpr (N == 1) {
+// Split prod_i w_i into two factors X * Y (K chains).
+template <int R, int K>
+__device__ __forceinline__ void two_factors(const double (&wr)[R], const double (&wi)[R], double& xr, double& xi,
+                                            double& yr, double& yi) {
+    if constexpr (K == 1) {
+        chain<0, R - 1, R>(wr, wi, xr, xi);
+        yr = wr[R - 1];
+        yi = wi[R - 1];
+    } else if constexpr (K == 2) {
+        chain<0, R / 2, R>(wr, wi, xr, xi);
+        chain<R / 2, R, R>(wr, wi, yr, yi);
+    } else {
+        constexpr int q = R / 4;
+        double r0, i0, r1, i1, r2, i2, r3, i3;
+        chain<0, q, R>(wr, wi, r0, i0);
+        chain<q, 2 * q, R>(wr, wi, r1, i1);
+        chain<2 * q, 3 * q, R>(wr, wi, r2, i2);
+        chain<3 * q, R, R>(wr, wi, r3, i3);
+        cmul2(r0, i0, r1, i1);
+        cmul2(r2, i2, r3, i3);
+        xr = r0; xi = i0; yr = r2; yi = i2;
+    }
+}
+
+// Full product of the lane's rows.
+template <int R, int K>
+__device__ __forceinline__ void lane_product(const double (&wr)[R], const double (&wi)[R], double& pr, double& pi) {
+    if constexpr (R == 1) {
+        pr = wr[0];
+        pi = wi[0];
+    } else {
+        double yr, yi;
+        two_factors<R, K>(wr, wi, pr, pi, yr, yi);
+        cmul2(pr, pi, yr, yi);
+    }
+}
+
+// acc += SIGN * X * Y as 4 DFMA (the last complex multiply fused with the accumulation).
+template <int SIGN>
+__device__ __forceinline__ void fused_acc(double xr, double xi, double yr, double yi, double& ar, double& ai) {
+    if (SIGN > 0) {
+        ar = fma(xr, yr, ar);
+        ar = fma(-xi, yi, ar);
+        ai = fma(xr, yi, ai);
+        ai = fma(xi, yr, ai);
+    } else {
+        ar = fma(-xr, yr, ar);
+        ar = fma(xi, yi, ar);
+        ai = fma(-xr, yi, ai);
+        ai = fma(-xi, yr, ai);
+    }
+}
+
+// S = 1: acc += SIGN * prod_i w_i.
+template <int R, int K, int SIGN>
+__device__ __forceinline__ void term_acc(const double (&wr)[R], const double (&wi)[R], double& ar, double& ai) {
+    if constexpr (R == 1) {
         if (SIGN > 0) { ar += wr[0]; ai += wi[0]; } else { ar -= wr[0]; ai -= wi[0]; }
     } else {
         double xr, xi, yr, yi;
-        if constexpr (K == 1) {
-            chain<0, N - 1, N>(wr, wi, xr, xi);
-            yr = wr[N - 1];
-            yi = wi[N - 1];
-        } else if constexpr (K == 2) {
-            chain<0, N / 2, N>(wr, wi, xr, xi);
-            chain<N / 2, N, N>(wr, wi, yr, yi);
-        } else {
-            constexpr int q = N / 4;
-            double r0, i0, r1, i1, r2, i2, r3, i3;
-            chain<0, q, N>(wr, wi, r0, i0);
-            chain<q, 2 * q, N>(wr, wi, r1, i1);
-            chain<2 * q, 3 * q, N>(wr, wi, r2, i2);
-            chain<3 * q, N, N>(wr, wi, r3, i3);
-            cmul2(r0, i0, r1, i1);
-            cmul2(r2, i2, r3, i3);
-            xr = r0; xi = i0; yr = r2; yi = i2;
-        }
-        if (SIGN > 0) {
-            ar = fma(xr, yr, ar);
-            ar = fma(-xi, yi, ar);
-            ai = fma(xr, yi, ai);
-            ai = fma(xi, yr, ai);
-        } else {
-            ar = fma(-xr, yr, ar);
-            ar = fma(xi, yi, ar);
-            ai = fma(-xr, yi, ai);
-            ai = fma(-xi, yr, ai);
+        two_factors<R, K>(wr, wi, xr, xi, yr, yi);
+        fused_acc<SIGN>(xr, xi, yr, yi, ar, ai);
+    }
+}
+
+__device__ __forceinline__ double flip_sign_if(double v, uint32_t mask_hi) {
+    // v with its sign bit XOR-ed by mask_hi (0 or 0x80000000): an integer op, not an FP64 instruction
+    const long long b = __double_as_longlong(v) ^ ((long long)mask_hi << 32);
+    return __longlong_as_double(b);
+}
+
+// Shuffle mask of this thread's lane group (S consecutive lanes).
+template <int S>
+__device__ __forceinline__ unsigned group_mask() {
+    return (S >= 32) ? 0xffffffffu : (((1u << S) - 1u) << ((threadIdx.x & 31u) & ~(unsigned)(S - 1)));
+}
+
+// S > 1, after the last term of an aligned group of S terms: (vr, vi)[t] is this lane's partial product
+// (its R rows) of term t of the group.  Recursive halving over the S lanes: at round k the lane keeps the
+// terms whose bit k equals its own bit k, ships the others to lane ^ 2^k and multiplies what it receives
+// into what it kept; after log2 S rounds lane h holds the full product of term h of the group and adds it
+// with the term's sign (-1)^{h+1} (groups start at even ranks) -- the last multiply fused with the sum.
+// FP64 work per term is exactly that of S = 1 (n-1 complex multiplies per term in total).
+template <int S>
+__device__ __forceinline__ void group_finish(double (&vr)[S], double (&vi)[S], uint32_t h, double& ar, double& ai) {
+    const unsigned gm = group_mask<S>();
+#pragma unroll
+    for (int k = 0, cnt = S; cnt > 1; k++, cnt >>= 1) {
+        const uint32_t hb = (h >> k) & 1u;
+#pragma unroll
+        for (int j = 0; j < cnt / 2; j++) {
+            const double kr = hb ? vr[2 * j + 1] : vr[2 * j];
+            const double ki = hb ? vi[2 * j + 1] : vi[2 * j];
+            const double sr = hb ? vr[2 * j] : vr[2 * j + 1];
+            const double si = hb ? vi[2 * j] : vi[2 * j + 1];
+            const double qr = __shfl_xor_sync(gm, sr, 1 << k);
+            const double qi = __shfl_xor_sync(gm, si, 1 << k);
+            if (cnt > 2) {
+                vr[j] = kr;
+                vi[j] = ki;
+                cmul2(vr[j], vi[j], qr, qi);
+            } else {
+                const uint32_t neg = (h & 1u) ? 0u : 0x80000000u;   // even term: sign -
+                fused_acc<+1>(flip_sign_if(kr, neg), flip_sign_if(ki, neg), qr, qi, ar, ai);
+            }
         }
     }
 }
 
-// w += z * column (column at shared address col), z = +-1 (or 0/1 when seeding) as a double.
-template <int N>
-__device__ __forceinline__ void flip_dyn(uint32_t col, double z, double (&wr)[N], double (&wi)[N]) {
+// w += z * column (lane's slice at shared address col), z = +-1 (or 0/1 when seeding).
+template <int R>
+__device__ __forceinline__ void flip_dyn(uint32_t col, double z, double (&wr)[R], double (&wi)[R]) {
 #pragma unroll
-    for (int i = 0; i < N; i++) {
+    for (int i = 0; i < R; i++) {
         const double2 a = lds_c(col + i * 16);
         wr[i] = fma(z, a.x, wr[i]);
         wi[i] = fma(z, a.y, wi[i]);
     }
 }
 
-// w += column J (PLUS) or w -= column J, compile-time column and sign.
-template <int N, int J, bool PLUS>
-__device__ __forceinline__ void flip_static(uint32_t sc, double (&wr)[N], double (&wi)[N]) {
+// w += column (PLUS) or w -= column, compile-time sign; col = lane's slice of the column.
+template <int R, bool PLUS>
+__device__ __forceinline__ void flip_static(uint32_t col, double (&wr)[R], double (&wi)[R]) {
 #pragma unroll
-    for (int i = 0; i < N; i++) {
-        const double2 a = lds_c(sc + (J * N + i) * 16);
+    for (int i = 0; i < R; i++) {
+        const double2 a = lds_c(col + i * 16);
         if (PLUS) { wr[i] += a.x; wi[i] += a.y; }
         else      { wr[i] -= a.x; wi[i] -= a.y; }
     }
 }
 
 // Inner block: ranks t = 0 .. 2^U - 1 of the current block (t = 0 already seeded/flipped).
-template <int N, int U, int T>
+// lc = this lane's address of row 0 of column 0 (columns are P rows apart).
+template <class C, int T>
 struct InnerStep {
-    static __device__ __forceinline__ void run(uint32_t sc, double (&wr)[N], double (&wi)[N], double zmid,
-                                               double& ar, double& ai) {
+    static constexpr int R = C::R;
+    static __device__ __forceinline__ void run(uint32_t lc, uint32_t h, double (&wr)[R], double (&wi)[R],
+                                               double zmid, double& ar, double& ai, double (&pr)[C::S],
+                                               double (&pi)[C::S]) {
+        constexpr int U = C::U;
         if constexpr (T > 0) {
             constexpr int J = ctz_c((unsigned)T);
             if constexpr (J == U - 1) {
                 // new bit = 1 ^ bit_U(rank): depends on the block (or chunk) parity -> signed by zmid
-                flip_dyn<N>(sc + (uint32_t)(J * N) * 16u, zmid, wr, wi);
+                flip_dyn<R>(lc + (uint32_t)(J * C::P) * 16u, zmid, wr, wi);
             } else {
                 constexpr bool PLUS = ((T >> (J + 1)) & 1) == 0;  // new bit = 1 ^ bit_{J+1}(t)
-                flip_static<N, J, PLUS>(sc, wr, wi);
+                flip_static<R, PLUS>(lc + (uint32_t)(J * C::P) * 16u, wr, wi);
             }
         }
-        if constexpr (T & 1) term_acc<N, +1>(wr, wi, ar, ai);   // sign (-1)^{r+1}, r == t (mod 2)
-        else                 term_acc<N, -1>(wr, wi, ar, ai);
-        if constexpr (T + 1 < (1 << U)) InnerStep<N, U, T + 1>::run(sc, wr, wi, zmid, ar, ai);
+        if constexpr (C::S == 1) {
+            if constexpr (T & 1) term_acc<R, C::K, +1>(wr, wi, ar, ai);   // sign (-1)^{r+1}, r == t (mod 2)
+            else                 term_acc<R, C::K, -1>(wr, wi, ar, ai);
+        } else {
+            lane_product<R, C::K>(wr, wi, pr[T % C::S], pi[T % C::S]);
+            if constexpr (T % C::S == C::S - 1) group_finish<C::S>(pr, pi, h, ar, ai);
+        }
+        if constexpr (T + 1 < (1 << U)) InnerStep<C, T + 1>::run(lc, h, wr, wi, zmid, ar, ai, pr, pi);
     }
 };
 
 // Seed w = base + sum_{j in [j0, N-1), bit_j(x) = 1} column_j   (App. A steps 5-8; branch-free in j).
-template <int N>
-__device__ __forceinline__ void seed_rows(uint32_t sc, uint32_t sbase, uint64_t x, int j0, double (&wr)[N],
-                                          double (&wi)[N]) {
+// lc / lb = this lane's addresses of column 0 and of the base vector.
+template <class C>
+__device__ __forceinline__ void seed_rows(uint32_t lc, uint32_t lb, uint64_t x, int j0, double (&wr)[C::R],
+                                          double (&wi)[C::R]) {
+    constexpr int N = C::N, R = C::R, P = C::P;
 #pragma unroll
-    for (int i = 0; i < N; i++) {
-        const double2 b = lds_c(sbase + i * 16);
+    for (int i = 0; i < R; i++) {
+        const double2 b = lds_c(lb + i * 16);
         wr[i] = b.x;
         wi[i] = b.y;
     }
     for (int j = j0; j < N - 1; j++) {
         const double f = (double)((x >> j) & 1ull);
-        flip_dyn<N>(sc + (uint32_t)(j * N) * 16u, f, wr, wi);
+        flip_dyn<R>(lc + (uint32_t)(j * P) * 16u, f, wr, wi);
     }
 }
 
-// One aligned chunk of 2^e ranks (e >= U >= 1).
-template <int N>
-__device__ __forceinline__ void walk_chunk(uint32_t sc, uint32_t sbase, uint64_t c, int e, ddc& acc) {
-    constexpr int U = WalkCfg<N>::U;
-    double wr[N], wi[N];
+// One aligned chunk of 2^e ranks (e >= U >= 1), walked by the S lanes of a group (h = lane in group).
+template <class C>
+__device__ __forceinline__ void walk_chunk(uint32_t lc, uint32_t lb, uint32_t h, uint64_t c, int e, ddc& acc) {
+    constexpr int U = C::U, R = C::R;
+    double wr[R], wi[R];
     const uint64_t x = ((c ^ (c >> 1)) << e) | ((c & 1ull) << (e - 1));
-    seed_rows<N>(sc, sbase, x, e - 1, wr, wi);
+    seed_rows<C>(lc, lb, x, e - 1, wr, wi);
     const uint64_t nblk = 1ull << (e - U);
     const uint64_t cpar = c & 1ull;
+    constexpr uint64_t kFoldMask = (U >= kWalkFoldBits) ? 0ull : ((1ull << (kWalkFoldBits - U)) - 1ull);
+    double ar = 0.0, ai = 0.0, pr[C::S], pi[C::S];
     for (uint64_t q = 0; q < nblk; q++) {
         if (q > 0) {
             // block boundary: Gray bit j = U + ctz(q) flips to 1 ^ bit_{j+1}(rank)
             const int j = U + __ffsll((long long)q) - 1;
             const uint64_t nb = (j + 1 < e) ? ((q >> (j + 1 - U)) & 1ull) : cpar;
-            flip_dyn<N>(sc + (uint32_t)(j * N) * 16u, nb ? -1.0 : 1.0, wr, wi);
+            flip_dyn<R>(lc + (uint32_t)(j * C::P) * 16u, nb ? -1.0 : 1.0, wr, wi);
         }
         const uint64_t nbm = (U < e) ? (q & 1ull) : cpar;   // bit_U(rank) for the mid-block flip
         const double zmid = nbm ? -1.0 : 1.0;
-        double ar = 0.0, ai = 0.0;
-        InnerStep<N, U, 0>::run(sc, wr, wi, zmid, ar, ai);
-        acc.re = dd_add_d(acc.re, ar);
-        acc.im = dd_add_d(acc.im, ai);
+        InnerStep<C, 0>::run(lc, h, wr, wi, zmid, ar, ai, pr, pi);
+        // fold the plain block sums into the dd accumulator every 2^kWalkFoldBits terms (and at the end)
+        if (((q + 1) & kFoldMask) == 0 || q + 1 == nblk) {
+            acc.re = dd_add_d(acc.re, ar);
+            acc.im = dd_add_d(acc.im, ai);
+            ar = 0.0;
+            ai = 0.0;
+        }
     }
 }
 
-// A single rank r, seeded from scratch.
-template <int N>
-__device__ __forceinline__ void single_term(uint32_t sc, uint32_t sbase, uint64_t r, ddc& acc) {
-    double wr[N], wi[N];
-    seed_rows<N>(sc, sbase, r ^ (r >> 1), 0, wr, wi);
+// A single rank r, seeded from scratch (all S lanes of the group call it; one accumulates).
+template <class C>
+__device__ __forceinline__ void single_term(uint32_t lc, uint32_t lb, uint32_t h, uint64_t r, ddc& acc) {
+    constexpr int R = C::R;
+    double wr[R], wi[R];
+    seed_rows<C>(lc, lb, r ^ (r >> 1), 0, wr, wi);
     double ar = 0.0, ai = 0.0;
-    if (r & 1ull) term_acc<N, +1>(wr, wi, ar, ai);
-    else          term_acc<N, -1>(wr, wi, ar, ai);
+    if constexpr (C::S == 1) {
+        if (r & 1ull) term_acc<R, C::K, +1>(wr, wi, ar, ai);
+        else          term_acc<R, C::K, -1>(wr, wi, ar, ai);
+    } else {
+        double pr, pi;
+        lane_product<R, C::K>(wr, wi, pr, pi);
+        const unsigned gm = group_mask<C::S>();
+#pragma unroll
+        for (int k = 1; k < C::S; k <<= 1) {      // butterfly: every lane ends with the full product
+            const double qr = __shfl_xor_sync(gm, pr, k);
+            const double qi = __shfl_xor_sync(gm, pi, k);
+            cmul2(pr, pi, qr, qi);
+        }
+        if (h == 0) {
+            if (r & 1ull) { ar += pr; ai += pi; }
+            else          { ar -= pr; ai -= pi; }
+        }
+    }
     acc.re = dd_add_d(acc.re, ar);
     acc.im = dd_add_d(acc.im, ai);
 }
 
-// Stage A column-major into shared memory (sc[j*N + i] = a_ij) and compute the App. A step-5 base
-// vector w_i(0) = a_{i,n} - 1/2 sum_j a_ij (summed in column order j = 0..n-1).
-template <int N>
+// Stage A column-major into shared memory, sc[j*P + i] = a_ij (rows i >= N zero), and compute the
+// App. A step-5 base vector w_i(0) = a_{i,n} - 1/2 sum_j a_ij (summed in column order j = 0..n-1);
+// padding rows get w = 1 (a neutral factor).
+template <class C>
 __device__ __forceinline__ void stage_matrix(const double2* __restrict__ A, double2* sc, double2* sbase) {
-    for (int k = threadIdx.x; k < N * N; k += blockDim.x) {
-        const int i = k / N, j = k - i * N;
-        sc[j * N + i] = A[k];
+    constexpr int N = C::N, P = C::P;
+    for (int k = threadIdx.x; k < N * P; k += blockDim.x) {
+        const int j = k / P, i = k - j * P;
+        sc[k] = (i < N) ? A[i * N + j] : make_double2(0.0, 0.0);
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < N; i += blockDim.x) {
+    for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        if (i >= N) {
+            sbase[i] = make_double2(1.0, 0.0);
+            continue;
+        }
         double sr = 0.0, si = 0.0;
         for (int j = 0; j < N; j++) {
-            sr += sc[j * N + i].x;
-            si += sc[j * N + i].y;
+            sr += sc[j * P + i].x;
+            si += sc[j * P + i].y;
         }
-        sbase[i] = make_double2(sc[(N - 1) * N + i].x - 0.5 * sr, sc[(N - 1) * N + i].y - 0.5 * si);
+        sbase[i] = make_double2(sc[(N - 1) * P + i].x - 0.5 * sr, sc[(N - 1) * P + i].y - 0.5 * si);
     }
     __syncthreads();
 }
 
 template <int N>
-__global__ void __launch_bounds__(WalkCfg<N>::NT) walk_kernel(const __grid_constant__ WalkParams P) {
+__global__ void __launch_bounds__(WalkCfg<N>::NT, WalkCfg<N>::MINB) walk_kernel(const __grid_constant__ WalkParams P) {
+    using C = WalkCfg<N>;
     extern __shared__ double2 smem[];
-    stage_matrix<N>(P.A, smem, smem + N * N);
-    const uint32_t sc = (uint32_t)__cvta_generic_to_shared(smem);
-    const uint32_t sbase = sc + (uint32_t)(N * N) * 16u;
+    stage_matrix<C>(P.A, smem, smem + N * C::P);
+    const uint32_t h = threadIdx.x % C::S;
+    const uint32_t hoff = h * (uint32_t)C::R * 16u;
+    const uint32_t lc = (uint32_t)__cvta_generic_to_shared(smem) + hoff;
+    const uint32_t lb = (uint32_t)__cvta_generic_to_shared(smem + N * C::P) + hoff;
 
     ddc acc;
     acc.re.hi = acc.re.lo = acc.im.hi = acc.im.lo = 0.0;
-    const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t W = (uint64_t)gridDim.x * (blockDim.x / C::S);     // walkers (lane groups)
     const uint64_t total = P.seg_pre[P.nseg];
     int s = 0;
-    for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < total; g += T) {
+    for (uint64_t g = (uint64_t)blockIdx.x * (blockDim.x / C::S) + threadIdx.x / C::S; g < total; g += W) {
         while (g >= P.seg_pre[s + 1]) s++;
         const uint64_t c = P.seg_c0[s] + (g - P.seg_pre[s]);
         const int e = P.seg_e[s];
-        if constexpr (WalkCfg<N>::U >= 1) {
-            if (e == 0) single_term<N>(sc, sbase, c, acc);
-            else        walk_chunk<N>(sc, sbase, c, e, acc);
+        if constexpr (C::U >= 1) {
+            if (e == 0) single_term<C>(lc, lb, h, c, acc);
+            else        walk_chunk<C>(lc, lb, h, c, e, acc);
         } else {
-            single_term<N>(sc, sbase, c, acc);
+            single_term<C>(lc, lb, h, c, acc);
         }
     }
 
@@ -267,20 +402,27 @@ __global__ void __launch_bounds__(WalkCfg<N>::NT) walk_kernel(const __grid_const
     }
 }
 
-// Diagnostic: w(ranks[k]) via the same seeding code (perm_c128_seed).
+// Diagnostic: w(ranks[k]) via the same seeding code (perm_c128_seed); one lane group per rank.
 template <int N>
 __global__ void seed_kernel(const double2* __restrict__ A, const uint64_t* __restrict__ ranks, int count,
                             double2* __restrict__ out) {
+    using C = WalkCfg<N>;
     extern __shared__ double2 smem[];
-    stage_matrix<N>(A, smem, smem + N * N);
-    const uint32_t sc = (uint32_t)__cvta_generic_to_shared(smem);
-    const uint32_t sbase = sc + (uint32_t)(N * N) * 16u;
-    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < count; k += gridDim.x * blockDim.x) {
+    stage_matrix<C>(A, smem, smem + N * C::P);
+    const uint32_t h = threadIdx.x % C::S;
+    const uint32_t hoff = h * (uint32_t)C::R * 16u;
+    const uint32_t lc = (uint32_t)__cvta_generic_to_shared(smem) + hoff;
+    const uint32_t lb = (uint32_t)__cvta_generic_to_shared(smem + N * C::P) + hoff;
+    const int groups = (int)(gridDim.x * (blockDim.x / C::S));
+    for (int k = (int)(blockIdx.x * (blockDim.x / C::S) + threadIdx.x / C::S); k < count; k += groups) {
         const uint64_t r = ranks[k];
-        double wr[N], wi[N];
-        seed_rows<N>(sc, sbase, r ^ (r >> 1), 0, wr, wi);
+        double wr[C::R], wi[C::R];
+        seed_rows<C>(lc, lb, r ^ (r >> 1), 0, wr, wi);
 #pragma unroll
-        for (int i = 0; i < N; i++) out[(size_t)k * N + i] = make_double2(wr[i], wi[i]);
+        for (int i = 0; i < C::R; i++) {
+            const int row = (int)h * C::R + i;
+            if (row < N) out[(size_t)k * N + row] = make_double2(wr[i], wi[i]);
+        }
     }
 }
 
@@ -311,13 +453,14 @@ cudaError_t walk_launch(const WalkLaunch& L) {
     return cudaGetLastError();
 }
 
+// blocks_per_sm: occupancy; walkers_per_block: independent chunk walkers (lane groups) per block.
 template <int N>
-cudaError_t walk_occupancy(int* blocks_per_sm, int* threads_per_block) {
+cudaError_t walk_occupancy(int* blocks_per_sm, int* walkers_per_block) {
     using C = WalkCfg<N>;
     cudaError_t err = cudaFuncSetAttribute(walk_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)C::smem_bytes);
     if (err != cudaSuccess) return err;
-    *threads_per_block = C::NT;
+    *walkers_per_block = C::NT / C::S;
     return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, walk_kernel<N>, C::NT, C::smem_bytes);
 }
 
@@ -328,7 +471,7 @@ cudaError_t walk_seed_launch(const double2* A_dev, const uint64_t* ranks_dev, in
     cudaError_t err = cudaFuncSetAttribute(seed_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)C::smem_bytes);
     if (err != cudaSuccess) return err;
-    int grid = (count + 127) / 128;
+    int grid = (count * C::S + 127) / 128;
     if (grid < 1) grid = 1;
     seed_kernel<N><<<grid, 128, C::smem_bytes, s>>>(A_dev, ranks_dev, count, w_out);
     return cudaGetLastError();

@@ -13,8 +13,8 @@ cudaError_t walk_launch_n(int n, const WalkLaunch& L) {
 #undef PERM_CASE
 }
 
-cudaError_t walk_occupancy_n(int n, int* blocks_per_sm, int* threads_per_block) {
-#define PERM_CASE(N) case N: return walk_occupancy<N>(blocks_per_sm, threads_per_block);
+cudaError_t walk_occupancy_n(int n, int* blocks_per_sm, int* walkers_per_block) {
+#define PERM_CASE(N) case N: return walk_occupancy<N>(blocks_per_sm, walkers_per_block);
     switch (n) { PERM_R64(PERM_CASE) default: return cudaErrorInvalidValue; }
 #undef PERM_CASE
 }

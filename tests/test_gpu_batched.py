@@ -32,7 +32,7 @@ def _check_batch(torch, A, ref):
     abs2 = abs2.cpu().numpy()
     for b in range(A.shape[0]):
         assert pins.scaled_error(per[b], ref[b], A[b]) <= TOL, (b, per[b], ref[b])
-        assert abs2[b] == per[b].real ** 2 + per[b].imag ** 2
+        assert abs2[b] == per[b].real * per[b].real + per[b].imag * per[b].imag
 
 
 @pytest.mark.parametrize("n", list(range(1, 15)))

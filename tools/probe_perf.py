@@ -5,8 +5,12 @@ from __future__ import annotations
 import sys
 import time
 
-import numpy as np
-import torch
+import os
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
 
 import paper_1904_06229_b200 as pb
 from paper_1904_06229_b200 import inputs
