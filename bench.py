@@ -1,0 +1,507 @@
+#!/usr/bin/env python
+"""bench.py -- B200 benchmark of the Gray-code Ryser/Glynn permanent (arXiv 1904.06229).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg5] [--impl ours|reference]
+
+N > 1 is launched by the driver as `torchrun --nproc-per-node N ... bench.py --gpus N ...` (one rank per
+GPU, NCCL).  Rank 0 prints ONE JSON line.
+
+Workloads (BASELINE.json configs; synthetic inputs from paper_1904_06229_b200/inputs.py):
+  cfg5 (default): one 44x44 complex Gaussian matrix, 2^43 Gray terms, range-sharded over the N GPUs with
+                  one NCCL all-gather of the double-double partials -- the metric's headline case.
+  cfg4: 32x32 block of a 1024x1024 Haar unitary, 2^31 terms, range-sharded.
+  cfg1: one 16x16 complex Gaussian (latency-bound).
+  cfg2: 10^5 submatrices of an n^2 x n^2 Haar unitary for each n in {8,12,16,20}; batched perms/s.
+  cfg3: 64 Bernoulli 0-1 matrices of order 24; exact int128; perms/s.
+
+A step is one pass of the whole hot path over the config's input: walk + in-GPU reduction + (N > 1)
+the all-gather + ordered combine.  `value` is timed with CUDA events on the compute stream from the
+first kernel to the end of the collective (inputs already in HBM); `e2e` times the same steps through
+the public API from pinned host input to the host result (H2D and D2H inside).  The roofline object
+uses the walk kernel's own duration, taken with CUDA events that the library records around that
+launch.  `--impl reference` times the CPU oracle (oracle/) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Gray-code terms/sec and % FP64 peak at n=44 on 1/2/4/8 B200; batched perms/sec"
+SMS_NOMINAL = 148
+FP64_LANES_PER_SM = 64           # FP64 FMA units per SM (B200)
+SM_MAX_MHZ = 1965.0
+
+
+def fp64_nominal_tflops(sm_mhz: float = SM_MAX_MHZ, sms: int = SMS_NOMINAL) -> float:
+    return sms * FP64_LANES_PER_SM * 2 * sm_mhz * 1e6 / 1e12
+
+
+# ------------------------------------------------------------------------------------------ clocks
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms while running (B200_PROFILING recipe)."""
+
+    FIELDS = ["clocks.sm", "clocks.max.sm", "power.draw", "clocks_event_reasons.active",
+              "clocks_event_reasons.hw_slowdown", "clocks_event_reasons.hw_thermal_slowdown",
+              "clocks_event_reasons.sw_thermal_slowdown", "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines: list[str] = []
+        self.thread = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={','.join(self.FIELDS)}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            if self.thread:
+                self.thread.join(timeout=2)
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < len(self.FIELDS):
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        loaded = [s for s in sm if s > 0.5 * max(sm)] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------------------ helpers
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def flush_l2(buf):
+    buf.fill_(1)   # 256 MiB write > 126 MB L2
+
+
+def max_over_ranks(x: float, world: int, device) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def measure_fp64_peak(pb, torch) -> float:
+    """Live FP64 DFMA probe: TFLOP/s of independent DFMA chains on all SMs."""
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    sink = torch.empty(sms * 8 * 256, dtype=torch.float64, device="cuda")
+    iters = 20000
+    pb.perm_fp64_probe(sms * 8, 256, 100, sink)
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    best = 0.0
+    for _ in range(3):
+        s.record()
+        pb.perm_fp64_probe(sms * 8, 256, iters, sink)
+        e.record()
+        torch.cuda.synchronize()
+        best = max(best, sms * 8 * 256 * iters * 64 / (s.elapsed_time(e) * 1e-3) / 1e12)
+    return best
+
+
+# ------------------------------------------------------------------------------------------ CPU oracle
+
+def oracle_rate_cfg(cfg: str, seconds: float = 12.0) -> dict:
+    """Time the CPU oracle (oracle/, as it stands) on a bounded sample of the workload.  Returns the
+    rate in the workload's metric unit and a description of the sample."""
+    import oracle
+    from paper_1904_06229_b200 import inputs
+    cores = oracle.num_threads()
+    if cfg in ("cfg5", "cfg4", "cfg1"):
+        A = {"cfg5": inputs.cfg5, "cfg4": inputs.cfg4, "cfg1": inputs.cfg1}[cfg]()
+        n = A.shape[0]
+        total = 1 << (n - 1)
+        span = min(total, 1 << 14)
+        while True:
+            t0 = time.perf_counter()
+            oracle.subpermanent(A, total // 3, min(span, total - total // 3) if total > 1 else 1,
+                                parts=4 * cores)
+            dt = time.perf_counter() - t0
+            if dt > seconds / 8 or span >= total:
+                break
+            span = min(total, span * 4)
+        if dt < seconds / 2 and span < total:
+            span = min(total, int(span * seconds / max(dt, 1e-3)))
+            t0 = time.perf_counter()
+            oracle.subpermanent(A, 0, span, parts=4 * cores)
+            dt = time.perf_counter() - t0
+        return {"value": span / dt, "unit": "terms/s", "cores": cores, "kind": "oracle",
+                "sample": f"App. A subpermanent (binary128) over {span} of the {total} Gray ranks of the {cfg} "
+                          f"matrix, {dt:.1f} s on {cores} host threads; rate extrapolates linearly"}
+    if cfg == "cfg2":
+        rates, parts = [], []
+        for n in (8, 12, 16, 20):
+            A = inputs.cfg2(n, 200 if n <= 12 else 4)
+            t0 = time.perf_counter()
+            k = 0
+            while time.perf_counter() - t0 < seconds / 4 and k < A.shape[0]:
+                step = min(A.shape[0] - k, 50 if n <= 12 else 1)
+                if n <= 12:
+                    oracle.ryser_batch(A[k:k + step])
+                else:
+                    oracle.permanent_hr(A[k])
+                k += step
+            dt = time.perf_counter() - t0
+            rates.append(dt / k)
+            parts.append(f"n={n}: {k} matrices in {dt:.1f} s")
+        per_step = sum(r * 100000 for r in rates)      # seconds for 4 x 10^5 permanents
+        return {"value": 400000 / per_step, "unit": "perms/s", "cores": cores, "kind": "oracle",
+                "sample": "Eq. (3)/App. A binary128 oracle on the first config-2 submatrices; " + "; ".join(parts)}
+    if cfg == "cfg3":
+        A = inputs.cfg3()
+        t0 = time.perf_counter()
+        k = 0
+        while time.perf_counter() - t0 < seconds and k < A.shape[0]:
+            oracle.ryser_i01(A[k])
+            k += 1
+        dt = time.perf_counter() - t0
+        return {"value": k / dt, "unit": "perms/s", "cores": cores, "kind": "oracle",
+                "sample": f"Eq. (3) int128 oracle on {k} of the 64 config-3 matrices, {dt:.1f} s"}
+    raise ValueError(cfg)
+
+
+# ------------------------------------------------------------------------------------------ GPU arm
+
+def run_ours(args):
+    import torch
+    world, rank, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    device = torch.device("cuda", torch.cuda.current_device())
+    import paper_1904_06229_b200 as pb
+    from paper_1904_06229_b200 import inputs, shard
+
+    pb.lib()
+    stream = torch.cuda.current_stream()
+    l2buf = torch.empty(256 << 20, dtype=torch.uint8, device=device)
+    cfg = args.config
+
+    def ev():
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        return e
+
+    result = {}
+    gpu_launches_per_step = 0
+    h2d = d2h = 0
+    walk_launches_per_step = 0
+    roofline_units = None          # (flops per walk launch)
+
+    if cfg in ("cfg5", "cfg4", "cfg1"):
+        A_np = {"cfg5": inputs.cfg5, "cfg4": inputs.cfg4, "cfg1": inputs.cfg1}[cfg]()
+        n = A_np.shape[0]
+        total = 1 << (n - 1)
+        k0, k1 = shard.rank_span(total, world, rank)
+        A_pin = torch.from_numpy(A_np).pin_memory()
+        ws = pb.make_workspace(n, k0, k1, device=device)
+        part = torch.empty(4, dtype=torch.float64, device=device)
+        gathered = torch.empty(4 * world, dtype=torch.float64, device=device)
+        gathered_host = torch.empty(4 * world, dtype=torch.float64).pin_memory()
+        ew0, ew1, ec1, es0, es1 = ev(), ev(), ev(), ev(), ev()
+        h2d, d2h = A_np.nbytes, 4 * world * 8
+        walk_launches_per_step = 1
+        roofline_units = 8.0 * n * (k1 - k0)       # algorithmic flops of this rank's walk launch
+
+        def step():
+            es0.record(stream)
+            pb.perm_c128_range(A_pin, k0, k1, workspace=ws, out=part, events=(ew0, ew1), stream=stream)
+            if world > 1:
+                import torch.distributed as dist
+                dist.all_gather_into_tensor(gathered, part)
+                src = gathered
+            else:
+                src = part
+            ec1.record(stream)
+            gathered_host.copy_(src, non_blocking=True)
+            es1.record(stream)
+            torch.cuda.synchronize()
+            val = shard.combine(gathered_host.numpy(), n)
+            return {"dev": ew0.elapsed_time(ec1), "e2e": es0.elapsed_time(es1), "walk": ew0.elapsed_time(ew1),
+                    "result": val}
+
+        units_per_step = total
+        unit = "terms/s"
+        gpu_launches_per_step = 2
+        workload = {"cfg5": "one 44x44 complex Gaussian matrix (re, im ~ N(0,1/2), seed 44): per(A) via 2^43 Gray terms",
+                    "cfg4": "32x32 leading block of a 1024x1024 Haar unitary (seed 1024): per(A) via 2^31 Gray terms",
+                    "cfg1": "one 16x16 complex Gaussian matrix (seed 16): per(A) via 2^15 Gray terms"}[cfg]
+        config = {"workload": workload, "n": n, "terms_per_step": total, "parallelism": f"Gray-range x{world}",
+                  "shard_terms_rank0": shard.rank_span(total, world, 0)[1], "input_bytes": A_np.nbytes,
+                  "l2": "flushed between steps (256 MiB write)"}
+        scaling = "strong"
+    elif cfg == "cfg2":
+        ns = (8, 12, 16, 20)
+        count = 100000
+        mats = {n: inputs.cfg2(n, count) for n in ns}
+        # weak scaling: every rank processes its contiguous share of each batch
+        host = {}
+        dev_in = {}
+        outs = {}
+        for n in ns:
+            b0, b1 = shard.rank_span(count, world, rank)
+            host[n] = torch.from_numpy(np.ascontiguousarray(mats[n][b0:b1])).pin_memory()
+            dev_in[n] = host[n].to(device)
+            outs[n] = (torch.empty(b1 - b0, dtype=torch.complex128, device=device),
+                       torch.empty(b1 - b0, dtype=torch.float64, device=device))
+        abs2_host = {n: torch.empty(outs[n][1].shape[0], dtype=torch.float64).pin_memory() for n in ns}
+        e0, e1, e2 = ev(), ev(), ev()
+        h2d = sum(h.numel() * 16 for h in host.values())
+        d2h = sum(a.numel() * 8 for a in abs2_host.values())
+        walk_launches_per_step = len(ns)
+        roofline_units = None
+
+        def step():
+            # device-resident pass
+            e0.record(stream)
+            for n in ns:
+                pb.perm_c128_batched(dev_in[n], per=outs[n][0], abs2=outs[n][1], stream=stream)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            # end-to-end pass through the public API from pinned host memory
+            es = torch.cuda.Event(enable_timing=True)
+            ee = torch.cuda.Event(enable_timing=True)
+            es.record(stream)
+            for n in ns:
+                dev_in[n].copy_(host[n], non_blocking=True)
+                pb.perm_c128_batched(dev_in[n], per=outs[n][0], abs2=outs[n][1], stream=stream)
+                abs2_host[n].copy_(outs[n][1], non_blocking=True)
+            ee.record(stream)
+            torch.cuda.synchronize()
+            return {"dev": e0.elapsed_time(e1), "e2e": es.elapsed_time(ee), "walk": e0.elapsed_time(e1),
+                    "result": float(abs2_host[20][0])}
+
+        units_per_step = count * len(ns)
+        unit = "perms/s"
+        gpu_launches_per_step = 2 * len(ns)
+        config = {"workload": "Boson-sampling |per|^2 of 10^5 submatrices (distinct rows/cols) of an n^2 x n^2 "
+                              "Haar unitary for each n in {8,12,16,20}", "batch_per_n": count,
+                  "parallelism": f"batch x{world}", "l2": "inputs 1.4 GB > L2"}
+        scaling = "weak" if world > 1 else "strong"
+        if world > 1:
+            units_per_step = count * len(ns)   # every rank does its share of the same global batch
+    elif cfg == "cfg3":
+        A_np = inputs.cfg3()
+        B, n = A_np.shape[0], A_np.shape[1]
+        b0, b1 = shard.rank_span(B, world, rank)
+        host = torch.from_numpy(np.ascontiguousarray(A_np[b0:b1])).pin_memory()
+        dev_in = host.to(device)
+        out = torch.empty((b1 - b0, 2), dtype=torch.int64, device=device)
+        out_host = torch.empty((b1 - b0, 2), dtype=torch.int64).pin_memory()
+        ws = torch.empty(pb.int01_workspace_bytes(n, b1 - b0), dtype=torch.uint8, device=device)
+        e0, e1 = ev(), ev()
+        h2d, d2h = host.numel(), out_host.numel() * 8
+        walk_launches_per_step = 1
+
+        def step():
+            e0.record(stream)
+            pb.perm_int01(dev_in, workspace=ws, out=out, stream=stream, as_int=False)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            es = torch.cuda.Event(enable_timing=True)
+            ee = torch.cuda.Event(enable_timing=True)
+            es.record(stream)
+            dev_in.copy_(host, non_blocking=True)
+            pb.perm_int01(dev_in, workspace=ws, out=out, stream=stream, as_int=False)
+            out_host.copy_(out, non_blocking=True)
+            ee.record(stream)
+            torch.cuda.synchronize()
+            return {"dev": e0.elapsed_time(e1), "e2e": es.elapsed_time(ee), "walk": e0.elapsed_time(e1),
+                    "result": int(out_host[0, 0])}
+
+        units_per_step = B
+        unit = "perms/s"
+        gpu_launches_per_step = 2 * 2
+        config = {"workload": "64 Bernoulli(1/2) 0-1 matrices of order 24 (seed 24), exact int128 permanents",
+                  "parallelism": f"batch x{world}", "l2": "input 37 KB; compute-bound"}
+        scaling = "weak" if world > 1 else "strong"
+    else:
+        raise SystemExit(f"unknown config {cfg}")
+
+    # warm-up (untimed)
+    for _ in range(args.warmup):
+        step()
+        flush_l2(l2buf)
+    torch.cuda.synchronize()
+    peak_meas = measure_fp64_peak(pb, torch) if rank == 0 else None
+
+    # timed region: barrier + synchronize on both sides
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize()
+    devs, e2es, walks, res = [], [], [], None
+    with ClockSampler(local) as clk:
+        t_wall0 = time.perf_counter()
+        for _ in range(args.steps):
+            r = step()
+            devs.append(r["dev"])
+            e2es.append(r["e2e"])
+            walks.append(r["walk"])
+            res = r["result"]
+            flush_l2(l2buf)
+        torch.cuda.synchronize()
+        t_wall = time.perf_counter() - t_wall0
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    dev_ms = max_over_ranks(sum(devs), world, device)
+    e2e_ms = max_over_ranks(sum(e2es), world, device)
+    walk_ms_local = sum(walks) / len(walks)
+    walk_ms = max_over_ranks(walk_ms_local, world, device)
+    clocks = clk.summary()
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    K = args.steps
+    value = units_per_step * K / (dev_ms * 1e-3)
+    e2e_val = units_per_step * K / (e2e_ms * 1e-3)
+    out = {"metric": METRIC, "value": value, "unit": unit, "n_gpus": world, "steps": K, "warmup": args.warmup,
+           "ms_per_step": dev_ms / K, "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
+           "dtype": "f64", "data": "synthetic (seeded generators, paper_1904_06229_b200/inputs.py)",
+           "config": config}
+    nominal = fp64_nominal_tflops()
+    if roofline_units is not None:
+        achieved = roofline_units / (walk_ms * 1e-3) / 1e12
+        out["roofline"] = {"bound": "alu", "achieved": achieved, "peak": nominal, "unit": "TFLOP/s",
+                           "frac": achieved / nominal, "traffic": None,
+                           "kernel": "walk_kernel<n> (FP64 vector pipe)",
+                           "algorithmic": "8n flops per Gray term x terms per launch (rank 0)",
+                           "peak_note": "derived: 148 SMs x 64 FP64 FMA/clk x 2 x 1965 MHz",
+                           "peak_measured_probe": peak_meas, "frac_of_measured": achieved / peak_meas,
+                           "walk_ms_per_launch": walk_ms}
+        if cfg == "cfg5":
+            out["fp64_peak_frac"] = achieved / nominal
+    else:
+        # batched / int: report the device time of the batch kernels against the FP64 (or INT) pipe
+        if cfg == "cfg2":
+            fl = sum(100000 / world * (1 << (n - 1)) * 8 * n for n in (8, 12, 16, 20))
+            achieved = fl / (dev_ms / K * 1e-3) / 1e12
+            out["roofline"] = {"bound": "alu", "achieved": achieved, "peak": nominal, "unit": "TFLOP/s",
+                               "frac": achieved / nominal, "traffic": None,
+                               "kernel": "batched_kernel<n> x4 (FP64 vector pipe)",
+                               "algorithmic": "8n flops per Gray term x 2^(n-1) terms x 10^5 per n",
+                               "peak_measured_probe": peak_meas}
+        else:
+            terms = units_per_step * (1 << 23) / world
+            out["roofline"] = {"bound": "alu", "achieved": terms / (dev_ms / K * 1e-3) / 1e12,
+                               "peak": None, "unit": "Tterms/s", "frac": None, "traffic": None,
+                               "kernel": "int01_kernel<24> (INT pipes)"}
+    out["e2e"] = {"value": e2e_val, "unit": unit, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
+    out["gpu_launches"] = gpu_launches_per_step * K
+    out["clocks"] = clocks
+    out["wall_s_timed_region"] = t_wall
+    out["result_sample"] = str(res)
+    if not args.no_cpu_baseline and world == 1:
+        out["cpu_baseline"] = oracle_rate_cfg(cfg, seconds=args.cpu_seconds)
+    print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return          # the reference arm runs on rank 0 only
+    cfg = args.config
+    unit = "perms/s" if cfg in ("cfg2", "cfg3") else "terms/s"
+    for _ in range(max(0, args.warmup)):
+        oracle_rate_cfg(cfg, seconds=1.0)
+    rates, samples = [], []
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        r = oracle_rate_cfg(cfg, seconds=args.cpu_seconds)
+        rates.append(r["value"])
+        samples.append(r)
+    wall = time.perf_counter() - t0
+    value = statistics.median(rates)
+    last = samples[-1]
+    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": unit, "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall / args.steps * 1e3,
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "binary128",
+           "data": "synthetic (seeded generators, paper_1904_06229_b200/inputs.py)",
+           "config": {"workload": cfg, "reference": "CPU oracle (oracle/oracle.c), bounded sample per step"},
+           "cpu_baseline": {"value": value, "unit": unit, "cores": last["cores"], "kind": "oracle",
+                            "sample": last["sample"]},
+           "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="cfg5", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -45,11 +45,14 @@ typedef struct { double hi_re, lo_re, hi_im, lo_im; } perm_dd_c128_t; /* value =
 typedef struct { uint64_t lo; int64_t hi; } perm_i128_t;             /* two's-complement int128 = hi*2^64 + lo */
 
 typedef struct {
-    uint64_t terms;        /* Gray-code terms evaluated (2^{n-1} for a whole permanent, C20)      */
-    uint32_t chunk_log2;   /* b: the walk's aligned chunk length is 2^b                           */
-    uint32_t threads;      /* walker threads launched                                             */
-    uint32_t blocks;       /* walker blocks launched                                              */
-    uint32_t launches;     /* kernels launched by this call                                        */
+    uint64_t terms;        /* out: Gray-code terms evaluated (2^{n-1} for a whole permanent, C20) */
+    uint32_t chunk_log2;   /* out: b, the walk's aligned chunk length is 2^b                      */
+    uint32_t threads;      /* out: walker threads launched                                        */
+    uint32_t blocks;       /* out: walker blocks launched                                         */
+    uint32_t launches;     /* out: kernels launched by this call                                  */
+    void* ev_walk_begin;   /* in, optional cudaEvent_t: recorded on `stream` just before the walk
+                              kernel is launched (NULL = not recorded)                            */
+    void* ev_walk_end;     /* in, optional cudaEvent_t: recorded just after the walk kernel        */
 } perm_stats_t;
 
 typedef enum {

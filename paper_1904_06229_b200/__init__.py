@@ -52,7 +52,16 @@ class i128(ctypes.Structure):
 
 class stats_t(ctypes.Structure):
     _fields_ = [("terms", ctypes.c_uint64), ("chunk_log2", ctypes.c_uint32), ("threads", ctypes.c_uint32),
-                ("blocks", ctypes.c_uint32), ("launches", ctypes.c_uint32)]
+                ("blocks", ctypes.c_uint32), ("launches", ctypes.c_uint32),
+                ("ev_walk_begin", ctypes.c_void_p), ("ev_walk_end", ctypes.c_void_p)]
+
+
+def _make_stats(events):
+    st = stats_t()
+    if events is not None:
+        st.ev_walk_begin = events[0]._as_parameter_.value if hasattr(events[0], "_as_parameter_") else events[0]
+        st.ev_walk_end = events[1]._as_parameter_.value if hasattr(events[1], "_as_parameter_") else events[1]
+    return st
 
 
 @dataclass
@@ -190,14 +199,16 @@ def _ws_args(workspace):
     return ctypes.c_void_p(workspace.data_ptr()), int(workspace.numel() * workspace.element_size())
 
 
-def perm_c128(A, *, workspace=None, stream=None, out=None, return_dd: bool = False, stats: bool = False):
+def perm_c128(A, *, workspace=None, stream=None, out=None, return_dd: bool = False, stats: bool = False,
+              events=None):
     """per(A) for one complex matrix (host numpy / torch CPU or CUDA tensor), 1 <= n <= 64.
 
     With ``out`` (a CUDA complex128 tensor of 1 element) the call is stream-ordered and returns
-    ``out``; otherwise it synchronizes and returns a Python complex (plus DD / stats if asked)."""
+    ``out``; otherwise it synchronizes and returns a Python complex (plus DD / stats if asked).
+    ``events=(e0, e1)`` (torch.cuda.Event, created) are recorded around the walk kernel."""
     ptr, n, keep = _matrix_ptr(A)
     ws, wsb = _ws_args(workspace)
-    st = stats_t()
+    st = _make_stats(events)
     if out is not None:
         _check(lib().perm_c128(ptr, n, ctypes.c_void_p(out.data_ptr()), None, ws, wsb, _stream_ptr(stream),
                                ctypes.byref(st)))
@@ -217,14 +228,16 @@ def perm_c128(A, *, workspace=None, stream=None, out=None, return_dd: bool = Fal
     return (val, *extra) if extra else val
 
 
-def perm_c128_range(A, k_begin: int, k_end: int, *, workspace=None, stream=None, out=None, stats: bool = False):
+def perm_c128_range(A, k_begin: int, k_end: int, *, workspace=None, stream=None, out=None, stats: bool = False,
+                    events=None):
     """Raw partial P(k_begin, k_end) = sum_{r in [k_begin, k_end)} (-1)^{r+1} prod_i w_i(gray r) (no 2(-1)^n).
 
     With ``out`` (a CUDA float64 tensor of 4 elements: hi_re, lo_re, hi_im, lo_im) the call is
-    stream-ordered and returns ``out``; otherwise it synchronizes and returns a :class:`DD`."""
+    stream-ordered and returns ``out``; otherwise it synchronizes and returns a :class:`DD`.
+    ``events=(e0, e1)`` (torch.cuda.Event, created) are recorded around the walk kernel."""
     ptr, n, keep = _matrix_ptr(A)
     ws, wsb = _ws_args(workspace)
-    st = stats_t()
+    st = _make_stats(events)
     if out is not None:
         _check(lib().perm_c128_range(ptr, n, int(k_begin), int(k_end), ctypes.c_void_p(out.data_ptr()), ws, wsb,
                                      _stream_ptr(stream), ctypes.byref(st)))

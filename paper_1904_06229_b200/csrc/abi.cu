@@ -213,8 +213,12 @@ perm_status_t run_walk(const perm_c128_t* A, int n, uint64_t k0, uint64_t k1, in
             WL.partials = partials;
             WL.grid = p.grid;
             WL.stream = s;
-            cudaError_t e = perm::walk_launch_n(n, WL);
+            cudaError_t e = cudaSuccess;
+            if (stats && stats->ev_walk_begin) e = cudaEventRecord((cudaEvent_t)stats->ev_walk_begin, s);
+            if (e == cudaSuccess) e = perm::walk_launch_n(n, WL);
             if (e != cudaSuccess) { result = cuda_fail(e, "walk kernel launch"); break; }
+            if (stats && stats->ev_walk_end) e = cudaEventRecord((cudaEvent_t)stats->ev_walk_end, s);
+            if (e != cudaSuccess) { result = cuda_fail(e, "cudaEventRecord"); break; }
             launches++;
             e = perm::reduce_launch(partials, p.grid, n_final, res_dd, res_c, s);
             if (e != cudaSuccess) { result = cuda_fail(e, "reduce kernel launch"); break; }
