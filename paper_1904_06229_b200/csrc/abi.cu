@@ -40,10 +40,13 @@ bool is_device_ptr(const void* p) {
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct WalkPlan {
-    int grid = 1;
+    int grid = 1;        // blocks of the main launch
+    int grid_edge = 0;   // blocks of the edge launch (constant-bank path with unaligned pieces)
     int threads = 0;
     int b = 0;
     int nseg = 0;
+    int use_const = 0;
+    int body = 0;
     Segment seg[perm::kMaxSegments];
     uint64_t items = 0;
 };
@@ -51,13 +54,13 @@ struct WalkPlan {
 int floor_log2(uint64_t x) { return x ? 63 - __builtin_clzll(x) : -1; }
 
 // Chunk length 2^b for a span of `total` ranks and T resident threads: at least ~128 chunks per
-// thread so the static round-robin leaves < 1% tail, at least the unrolled block 2^U, at most 2^40.
+// thread so the static round-robin leaves < 1% tail, at least the unrolled block 2^U, at most 2^30.
 int choose_b(int n, uint64_t total, uint64_t T) {
     const int U = perm::walk_inner_bits(n);
     int b = floor_log2(total / (T * 128ull > 0 ? T * 128ull : 1));
     if (b < U) b = U;
     if (b > n - 1) b = n - 1;
-    if (b > 40) b = 40;
+    if (b > 30) b = 30;
     if (b < 0) b = 0;
     return b;
 }
@@ -103,30 +106,58 @@ bool decompose(int n, uint64_t k0, uint64_t k1, int b, WalkPlan& p) {
     return true;
 }
 
-// max_grid: resident blocks of the walk kernel; nt: chunk walkers (lane groups) per block.
-perm_status_t device_threads(int n, int* max_grid, int* nt) {
+// max_grid: resident blocks of the walk kernel; nt: chunk walkers (lane groups) per block;
+// max_grid_c: resident blocks of the constant-bank kernel (0 if that path does not exist for n).
+perm_status_t device_threads(int n, int* max_grid, int* nt, int* max_grid_c = nullptr) {
     int dev = 0, sms = 0, bps = 0;
     PERM_CUDA(cudaGetDevice(&dev), "cudaGetDevice");
     PERM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "cudaDeviceGetAttribute");
     PERM_CUDA(perm::walk_occupancy_n(n, &bps, nt), "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
     if (bps < 1) bps = 1;
     *max_grid = sms * bps;
+    if (max_grid_c) {
+        int bc = 0;
+        PERM_CUDA(perm::walk_occupancy_c_n(n, &bc), "cudaOccupancyMaxActiveBlocksPerMultiprocessor(c)");
+        *max_grid_c = sms * bc;
+    }
     return PERM_OK;
 }
 
 perm_status_t plan_walk(int n, uint64_t k0, uint64_t k1, WalkPlan& p) {
-    int max_grid = 0, nt = 0;
-    perm_status_t st = device_threads(n, &max_grid, &nt);
+    int max_grid = 0, nt = 0, max_grid_c = 0;
+    perm_status_t st = device_threads(n, &max_grid, &nt, &max_grid_c);
     if (st != PERM_OK) return st;
     p.threads = nt;
-    p.b = choose_b(n, k1 - k0, (uint64_t)max_grid * nt);
+    const uint64_t T = (uint64_t)(max_grid_c > 0 ? max_grid_c * perm::kWalkThreads : max_grid * nt);
+    p.b = choose_b(n, k1 - k0, T);
     if (!decompose(n, k0, k1, p.b, p)) {
         snprintf(g_err, sizeof(g_err), "range decomposition exceeded %d segments", perm::kMaxSegments);
         return PERM_E_ARG;
     }
+    // constant-bank path for the biggest walked segment (the aligned body)
+    p.use_const = 0;
+    if (max_grid_c > 0) {
+        int best = -1;
+        for (int s = 0; s < p.nseg; s++)
+            if (p.seg[s].e > 0 && (best < 0 || p.seg[s].count > p.seg[best].count)) best = s;
+        if (best >= 0) {
+            p.use_const = 1;
+            p.body = best;
+            const uint64_t body = p.seg[best].count;
+            const uint64_t wc = perm::kWalkThreads;
+            uint64_t need = (body + wc - 1) / wc;
+            p.grid = (int)(need < (uint64_t)max_grid_c ? need : (uint64_t)max_grid_c);
+            if (p.grid < 1) p.grid = 1;
+            const uint64_t rest = p.items - body;
+            need = (rest + nt - 1) / nt;
+            p.grid_edge = rest == 0 ? 0 : (int)(need < (uint64_t)max_grid ? need : (uint64_t)max_grid);
+            return PERM_OK;
+        }
+    }
     uint64_t need = (p.items + nt - 1) / nt;
     p.grid = (int)(need < (uint64_t)max_grid ? need : (uint64_t)max_grid);
     if (p.grid < 1) p.grid = 1;
+    p.grid_edge = 0;
     return PERM_OK;
 }
 
@@ -177,10 +208,10 @@ perm_status_t run_walk(const perm_c128_t* A, int n, uint64_t k0, uint64_t k1, in
     WalkPlan p;
     st = plan_walk(n, k0, k1, p);
     if (st != PERM_OK) return st;
-    int max_grid = 0, nt = 0;
-    st = device_threads(n, &max_grid, &nt);
+    int max_grid = 0, nt = 0, max_grid_c = 0;
+    st = device_threads(n, &max_grid, &nt, &max_grid_c);
     if (st != PERM_OK) return st;
-    const WsLayout L = ws_layout(n, max_grid);
+    const WsLayout L = ws_layout(n, max_grid + max_grid_c);
 
     char* ws = (char*)workspace;
     bool own_ws = false;
@@ -212,6 +243,9 @@ perm_status_t run_walk(const perm_c128_t* A, int n, uint64_t k0, uint64_t k1, in
             for (int i = 0; i < p.nseg; i++) WL.seg[i] = p.seg[i];
             WL.partials = partials;
             WL.grid = p.grid;
+            WL.use_const = p.use_const;
+            WL.body = p.body;
+            WL.grid_edge = p.grid_edge;
             WL.stream = s;
             cudaError_t e = cudaSuccess;
             if (stats && stats->ev_walk_begin) e = cudaEventRecord((cudaEvent_t)stats->ev_walk_begin, s);
@@ -219,8 +253,8 @@ perm_status_t run_walk(const perm_c128_t* A, int n, uint64_t k0, uint64_t k1, in
             if (e != cudaSuccess) { result = cuda_fail(e, "walk kernel launch"); break; }
             if (stats && stats->ev_walk_end) e = cudaEventRecord((cudaEvent_t)stats->ev_walk_end, s);
             if (e != cudaSuccess) { result = cuda_fail(e, "cudaEventRecord"); break; }
-            launches++;
-            e = perm::reduce_launch(partials, p.grid, n_final, res_dd, res_c, s);
+            launches += 1 + (p.grid_edge > 0 ? 1 : 0);
+            e = perm::reduce_launch(partials, p.grid + p.grid_edge, n_final, res_dd, res_c, s);
             if (e != cudaSuccess) { result = cuda_fail(e, "reduce kernel launch"); break; }
             launches++;
         } else {
@@ -258,8 +292,8 @@ perm_status_t run_walk(const perm_c128_t* A, int n, uint64_t k0, uint64_t k1, in
         if (stats) {
             stats->terms = k1 - k0;
             stats->chunk_log2 = (uint32_t)p.b;
-            stats->threads = (uint32_t)(p.grid * perm::kWalkThreads);
-            stats->blocks = (uint32_t)p.grid;
+            stats->threads = (uint32_t)((p.grid + p.grid_edge) * perm::kWalkThreads);
+            stats->blocks = (uint32_t)(p.grid + p.grid_edge);
             stats->launches = launches;
         }
     }
@@ -296,10 +330,10 @@ perm_status_t perm_workspace_bytes(int n, uint64_t k_begin, uint64_t k_end, size
     if (st != PERM_OK) return st;
     if (k_begin > k_end) return PERM_E_ARG;
     if (n < 64 && k_end > (1ull << (n - 1))) return PERM_E_ORDER;
-    int max_grid = 0, nt = 0;
-    st = device_threads(n, &max_grid, &nt);
+    int max_grid = 0, nt = 0, max_grid_c = 0;
+    st = device_threads(n, &max_grid, &nt, &max_grid_c);
     if (st != PERM_OK) return st;
-    *bytes = ws_layout(n, max_grid).total;
+    *bytes = ws_layout(n, max_grid + max_grid_c).total;
     return PERM_OK;
 }
 

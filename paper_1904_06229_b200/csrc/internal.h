@@ -48,25 +48,33 @@ struct Segment {
     int e;
 };
 
+// Largest order whose whole matrix fits the 32 KB kernel-parameter space (walk_kernel_c).
+constexpr int kConstMaxN = 45;
+
 struct WalkLaunch {
     const double2* A_dev;   // device, row-major n x n
-    const double2* A_host;  // host, row-major n x n (inner columns go into the kernel parameters)
+    const double2* A_host;  // host, row-major n x n (walk_kernel_c takes the matrix as a kernel parameter)
     int n;
     int nseg;
     Segment seg[kMaxSegments];
-    ddc* partials;          // device, one per block
-    int grid;
+    ddc* partials;          // device, grid + grid_edge entries
+    int grid;               // blocks of the main launch
+    int use_const;          // run segment `body` in walk_kernel_c
+    int body;               // index of the body segment (use_const)
+    int grid_edge;          // blocks of the edge launch (use_const and nseg > 1), else 0
     cudaStream_t stream;
 };
 
 // Defined in walk_inst.cu (explicit instantiations over N = 1..64).
 template <int N> cudaError_t walk_launch(const WalkLaunch& L);
 template <int N> cudaError_t walk_occupancy(int* blocks_per_sm, int* walkers_per_block);
+template <int N> cudaError_t walk_occupancy_c(int* blocks_per_sm);
 template <int N> cudaError_t walk_seed_launch(const double2* A_dev, const uint64_t* ranks_dev, int count,
                                               double2* w_out, cudaStream_t s);
 
 cudaError_t walk_launch_n(int n, const WalkLaunch& L);
 cudaError_t walk_occupancy_n(int n, int* blocks_per_sm, int* walkers_per_block);
+cudaError_t walk_occupancy_c_n(int n, int* blocks_per_sm);
 cudaError_t walk_seed_launch_n(int n, const double2* A_dev, const uint64_t* ranks_dev, int count,
                                double2* w_out, cudaStream_t s);
 

@@ -78,10 +78,19 @@ __device__ __forceinline__ double2 lds_c(uint32_t addr) {
     return v;
 }
 
-// (xr + i xi) *= (yr + i yi): 2 DMUL + 2 DFMA.
+// (xr + i xi) *= (yr + i yi): 4 FP64 instructions.  With PERM_CMUL_FMA0 the two products are
+// written as fma(a, b, +0.0) (bit-identical to a*b except for the sign of an exact zero), so all four
+// are DFMA and ptxas can serve a repeated operand from the operand-reuse cache across consecutive
+// DFMAs (DMUL -> DFMA pairs do not share it); three-vector-operand DFMAs issue at ~0.7 of the FP64
+// pipe rate on B200 (tools/micro/fp64_banks2.cu), so reuse is what keeps the chain at pipe speed.
 __device__ __forceinline__ void cmul2(double& xr, double& xi, double yr, double yi) {
+#ifdef PERM_CMUL_FMA0
+    const double t = fma(xi, yi, 0.0);
+    const double u = fma(xi, yr, 0.0);
+#else
     const double t = xi * yi;
     const double u = xi * yr;
+#endif
     const double nr = fma(xr, yr, -t);
     xi = fma(xr, yi, u);
     xr = nr;
@@ -402,6 +411,141 @@ __global__ void __launch_bounds__(WalkCfg<N>::NT, WalkCfg<N>::MINB) walk_kernel(
     }
 }
 
+// ------------------------------------------------------------------------------------------------
+// Constant-bank path (one lane per chunk, n <= kConstMaxN): the whole matrix rides in the kernel
+// parameters, so every column entry is a warp-uniform LDCU.64 into a uniform register and the row-sum
+// update is DADD R, R, UR -- no shared-memory load, no vector register for the column, and one vector
+// operand fewer per update.  Only the aligned body of a range (all chunks of length 2^eb) runs here;
+// the few unaligned head/tail pieces go to walk_kernel.  ptxas keeps parameter loads as LDCU only for
+// warp-uniform addresses, so the block loop counter is a 32-bit uniform value and each use of an
+// inner column gets its own opaque zero offset (z * (T+1), z = q >> 31 == 0): without it the
+// loop-invariant columns are hoisted into vector registers and the kernel spills.
+template <int N>
+struct WalkParamsC {
+    double2 col[N][N];                     // col[j][i] = a_ij
+    ddc* partials;                         // [gridDim.x]
+    uint64_t c0;                           // first body chunk
+    uint64_t count;                        // body chunks
+    int32_t eb;                            // log2 body chunk length (>= U)
+};
+
+template <class C, int T>
+struct InnerStepC {
+    static constexpr int N = C::N;
+    static __device__ __forceinline__ void run(const WalkParamsC<N>& P, int z, double (&wr)[N], double (&wi)[N],
+                                               double zmid, double& ar, double& ai) {
+        constexpr int U = C::U;
+        if constexpr (T > 0) {
+            constexpr int J = ctz_c((unsigned)T);
+            const int jj = J + z * (T + 1);          // == J; distinct expression per use (no CSE/hoist)
+            if constexpr (J == U - 1) {
+#pragma unroll
+                for (int i = 0; i < N; i++) {
+                    const double2 a = P.col[jj][i];
+                    wr[i] = fma(zmid, a.x, wr[i]);
+                    wi[i] = fma(zmid, a.y, wi[i]);
+                }
+            } else {
+                constexpr bool PLUS = ((T >> (J + 1)) & 1) == 0;  // new bit = 1 ^ bit_{J+1}(t)
+#pragma unroll
+                for (int i = 0; i < N; i++) {
+                    const double2 a = P.col[jj][i];
+                    if (PLUS) { wr[i] += a.x; wi[i] += a.y; }
+                    else      { wr[i] -= a.x; wi[i] -= a.y; }
+                }
+            }
+        }
+        if constexpr (T & 1) term_acc<N, C::K, +1>(wr, wi, ar, ai);
+        else                 term_acc<N, C::K, -1>(wr, wi, ar, ai);
+        if constexpr (T + 1 < (1 << U)) InnerStepC<C, T + 1>::run(P, z, wr, wi, zmid, ar, ai);
+    }
+};
+
+template <class C>
+__device__ __forceinline__ void walk_chunk_const(const WalkParamsC<C::N>& P, uint32_t lc, uint32_t lb, uint64_t c,
+                                                 ddc& acc) {
+    constexpr int N = C::N, U = C::U;
+    const int e = P.eb;                                   // warp-uniform (kernel parameter)
+    double wr[N], wi[N];
+#pragma unroll
+    for (int i = 0; i < N; i++) {
+        const double2 b = lds_c(lb + i * 16);
+        wr[i] = b.x;
+        wi[i] = b.y;
+    }
+    const uint64_t x = ((c ^ (c >> 1)) << e) | ((c & 1ull) << (e - 1));
+    for (int j = e - 1; j < N - 1; j++) {                 // seed, App. A steps 5-8 (shared memory)
+        const double f = (double)((x >> j) & 1ull);
+        flip_dyn<N>(lc + (uint32_t)(j * N) * 16u, f, wr, wi);
+    }
+    const int nblk = 1 << (e - U);
+    const uint64_t cpar = c & 1ull;
+    constexpr int kFoldMask = (U >= kWalkFoldBits) ? 0 : ((1 << (kWalkFoldBits - U)) - 1);
+    double ar = 0.0, ai = 0.0;
+    for (int q = 0; q < nblk; q++) {
+        const int z = q >> 30;                            // 0 (nblk <= 2^27); uniform, loop-variant
+        if (q > 0) {
+            const int j = U + __ffs(q) - 1;
+            const uint64_t nb = (j + 1 < e) ? (uint64_t)((q >> (j + 1 - U)) & 1) : cpar;
+            flip_dyn<N>(lc + (uint32_t)(j * N) * 16u, nb ? -1.0 : 1.0, wr, wi);
+        }
+        const uint64_t nbm = (U < e) ? (uint64_t)(q & 1) : cpar;
+        InnerStepC<C, 0>::run(P, z, wr, wi, nbm ? -1.0 : 1.0, ar, ai);
+        if (((q + 1) & kFoldMask) == 0 || q + 1 == nblk) {
+            acc.re = dd_add_d(acc.re, ar);
+            acc.im = dd_add_d(acc.im, ai);
+            ar = 0.0;
+            ai = 0.0;
+        }
+    }
+}
+
+template <int N>
+__global__ void __launch_bounds__(kWalkThreads) walk_kernel_c(const __grid_constant__ WalkParamsC<N> P) {
+    using C = WCfg<N, 1>;
+    __shared__ double2 scol[N * N];                          // scol[j*N + i] = a_ij (seeding, outer flips)
+    __shared__ double2 sbase[N];
+    for (int k = threadIdx.x; k < N * N; k += blockDim.x) scol[k] = P.col[k / N][k % N];
+    __syncthreads();
+    for (int i = threadIdx.x; i < N; i += blockDim.x) {     // App. A step 5, summed in column order
+        double sr = 0.0, si = 0.0;
+        for (int j = 0; j < N; j++) {
+            sr += scol[j * N + i].x;
+            si += scol[j * N + i].y;
+        }
+        sbase[i] = make_double2(scol[(N - 1) * N + i].x - 0.5 * sr, scol[(N - 1) * N + i].y - 0.5 * si);
+    }
+    __syncthreads();
+    const uint32_t lc = (uint32_t)__cvta_generic_to_shared(scol);
+    const uint32_t lb = (uint32_t)__cvta_generic_to_shared(sbase);
+    ddc acc;
+    acc.re.hi = acc.re.lo = acc.im.hi = acc.im.lo = 0.0;
+    // warp-uniform item loop (every lane runs every iteration; lanes past the end walk a valid chunk
+    // and drop the result), so all control flow and column addresses stay on the uniform datapath
+    const uint32_t ln = threadIdx.x & 31u;
+    const uint64_t wid = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (uint64_t)__shfl_sync(0xffffffffu, threadIdx.x >> 5, 0);
+    const uint64_t nw = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    for (uint64_t base = wid * 32u; base < P.count; base += nw * 32u) {
+        const uint64_t g = base + ln;
+        const bool valid = g < P.count;
+        ddc part;
+        part.re.hi = part.re.lo = part.im.hi = part.im.lo = 0.0;
+        walk_chunk_const<C>(P, lc, lb, P.c0 + (valid ? g : 0), part);
+        if (valid) acc = ddc_add(acc, part);
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) acc = ddc_add(acc, shfl_down_ddc(acc, off));
+    __shared__ ddc swarp[32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) swarp[warp] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        ddc b = swarp[0];
+        for (int w = 1; w < (int)(blockDim.x >> 5); w++) b = ddc_add(b, swarp[w]);
+        P.partials[blockIdx.x] = b;
+    }
+}
+
 // Diagnostic: w(ranks[k]) via the same seeding code (perm_c128_seed); one lane group per rank.
 template <int N>
 __global__ void seed_kernel(const double2* __restrict__ A, const uint64_t* __restrict__ ranks, int count,
@@ -427,30 +571,67 @@ __global__ void seed_kernel(const double2* __restrict__ A, const uint64_t* __res
 }
 
 template <int N>
-cudaError_t walk_launch(const WalkLaunch& L) {
+cudaError_t walk_launch_smem(const WalkLaunch& L, const Segment* seg, int nseg, ddc* partials, int grid) {
     using C = WalkCfg<N>;
     WalkParams P;
     P.A = L.A_dev;
-    P.partials = L.partials;
+    P.partials = partials;
     uint64_t pre = 0;
     for (int s = 0; s < kMaxSegments; s++) {
         P.seg_pre[s] = pre;
-        if (s < L.nseg) {
-            P.seg_c0[s] = L.seg[s].c0;
-            P.seg_e[s] = L.seg[s].e;
-            pre += L.seg[s].count;
+        if (s < nseg) {
+            P.seg_c0[s] = seg[s].c0;
+            P.seg_e[s] = seg[s].e;
+            pre += seg[s].count;
         } else {
             P.seg_c0[s] = 0;
             P.seg_e[s] = 0;
         }
     }
     P.seg_pre[kMaxSegments] = pre;
-    P.nseg = L.nseg;
+    P.nseg = nseg;
     cudaError_t err = cudaFuncSetAttribute(walk_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)C::smem_bytes);
     if (err != cudaSuccess) return err;
-    walk_kernel<N><<<L.grid, C::NT, C::smem_bytes, L.stream>>>(P);
+    walk_kernel<N><<<grid, C::NT, C::smem_bytes, L.stream>>>(P);
     return cudaGetLastError();
+}
+
+// Launches the walk over L.seg.  For n <= kConstMaxN the largest segment (the aligned body) runs in
+// walk_kernel_c (matrix in the constant bank) on L.grid blocks and the remaining segments, if any, in
+// walk_kernel on L.grid_edge blocks; partials land in L.partials[0 .. L.grid + L.grid_edge).
+template <int N>
+cudaError_t walk_launch(const WalkLaunch& L) {
+    if constexpr (N <= kConstMaxN && walk_lanes_per_chunk(N) == 1 && walk_inner_bits(N) >= 1) {
+        if (L.use_const) {
+            const Segment& b = L.seg[L.body];
+            WalkParamsC<N> P;
+            for (int j = 0; j < N; j++)
+                for (int i = 0; i < N; i++) P.col[j][i] = L.A_host[(size_t)i * N + j];
+            P.partials = L.partials;
+            P.c0 = b.c0;
+            P.count = b.count;
+            P.eb = b.e;
+            walk_kernel_c<N><<<L.grid, kWalkThreads, 0, L.stream>>>(P);
+            cudaError_t err = cudaGetLastError();
+            if (err != cudaSuccess || L.grid_edge == 0) return err;
+            Segment rest[kMaxSegments];
+            int nr = 0;
+            for (int s = 0; s < L.nseg; s++)
+                if (s != L.body) rest[nr++] = L.seg[s];
+            return walk_launch_smem<N>(L, rest, nr, L.partials + L.grid, L.grid_edge);
+        }
+    }
+    return walk_launch_smem<N>(L, L.seg, L.nseg, L.partials, L.grid);
+}
+
+// Occupancy of walk_kernel_c (0 when the constant-bank path does not exist for this order).
+template <int N>
+cudaError_t walk_occupancy_c(int* blocks_per_sm) {
+    *blocks_per_sm = 0;
+    if constexpr (N <= kConstMaxN && walk_lanes_per_chunk(N) == 1 && walk_inner_bits(N) >= 1)
+        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, walk_kernel_c<N>, kWalkThreads, 0);
+    return cudaSuccess;
 }
 
 // blocks_per_sm: occupancy; walkers_per_block: independent chunk walkers (lane groups) per block.

@@ -19,6 +19,12 @@ cudaError_t walk_occupancy_n(int n, int* blocks_per_sm, int* walkers_per_block) 
 #undef PERM_CASE
 }
 
+cudaError_t walk_occupancy_c_n(int n, int* blocks_per_sm) {
+#define PERM_CASE(N) case N: return walk_occupancy_c<N>(blocks_per_sm);
+    switch (n) { PERM_R64(PERM_CASE) default: return cudaErrorInvalidValue; }
+#undef PERM_CASE
+}
+
 cudaError_t walk_seed_launch_n(int n, const double2* A_dev, const uint64_t* ranks_dev, int count, double2* w_out,
                                cudaStream_t s) {
 #define PERM_CASE(N) case N: return walk_seed_launch<N>(A_dev, ranks_dev, count, w_out, s);

@@ -11,6 +11,7 @@ namespace perm {
 #define PERM_INST(N)                                                                             \
     template cudaError_t walk_launch<N>(const WalkLaunch&);                                      \
     template cudaError_t walk_occupancy<N>(int*, int*);                                          \
+    template cudaError_t walk_occupancy_c<N>(int*);                                              \
     template cudaError_t walk_seed_launch<N>(const double2*, const uint64_t*, int, double2*, cudaStream_t);
 #define PERM_P(b) PERM_INST(b + 1) PERM_INST(b + 2) PERM_INST(b + 3) PERM_INST(b + 4) \
                   PERM_INST(b + 5) PERM_INST(b + 6) PERM_INST(b + 7) PERM_INST(b + 8)
