@@ -50,6 +50,16 @@ struct Segment {
 
 // Largest order whose whole matrix fits the 32 KB kernel-parameter space (walk_kernel_c).
 constexpr int kConstMaxN = 45;
+// Orders that use the constant-bank walk.  ptxas keeps the per-use parameter loads on the uniform
+// datapath (LDCU -> DADD R, R, UR) only for some orders; for the others it emits vector LDCs and the
+// shared-memory walk is faster.  Measured on B200 (profiles/round1_walk_variants.md): n = 32 +7%,
+// n = 44 -7%.  PERM_CONST_ORDERS=-1 disables the path, 0 enables it for every n <= kConstMaxN.
+#ifndef PERM_CONST_ORDERS
+#define PERM_CONST_ORDERS 32
+#endif
+__host__ __device__ constexpr bool walk_const_path(int n) {
+    return n <= kConstMaxN && (PERM_CONST_ORDERS == 0 || n == PERM_CONST_ORDERS);
+}
 
 struct WalkLaunch {
     const double2* A_dev;   // device, row-major n x n

@@ -602,7 +602,7 @@ cudaError_t walk_launch_smem(const WalkLaunch& L, const Segment* seg, int nseg, 
 // walk_kernel on L.grid_edge blocks; partials land in L.partials[0 .. L.grid + L.grid_edge).
 template <int N>
 cudaError_t walk_launch(const WalkLaunch& L) {
-    if constexpr (N <= kConstMaxN && walk_lanes_per_chunk(N) == 1 && walk_inner_bits(N) >= 1) {
+    if constexpr (walk_const_path(N) && walk_lanes_per_chunk(N) == 1 && walk_inner_bits(N) >= 1) {
         if (L.use_const) {
             const Segment& b = L.seg[L.body];
             WalkParamsC<N> P;
@@ -629,7 +629,7 @@ cudaError_t walk_launch(const WalkLaunch& L) {
 template <int N>
 cudaError_t walk_occupancy_c(int* blocks_per_sm) {
     *blocks_per_sm = 0;
-    if constexpr (N <= kConstMaxN && walk_lanes_per_chunk(N) == 1 && walk_inner_bits(N) >= 1)
+    if constexpr (walk_const_path(N) && walk_lanes_per_chunk(N) == 1 && walk_inner_bits(N) >= 1)
         return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, walk_kernel_c<N>, kWalkThreads, 0);
     return cudaSuccess;
 }
