@@ -2,6 +2,7 @@
 // planning (partition of the Gray-rank range into aligned chunks), workspace
 // layout, stream handling and status codes.  All arithmetic of the method runs in the kernels.
 #include <cmath>
+#include <mutex>
 #include <cstdio>
 #include <cstring>
 #include <vector>
@@ -106,20 +107,36 @@ bool decompose(int n, uint64_t k0, uint64_t k1, int b, WalkPlan& p) {
     return true;
 }
 
-// max_grid: resident blocks of the walk kernel; nt: chunk walkers (lane groups) per block;
-// max_grid_c: resident blocks of the constant-bank kernel (0 if that path does not exist for n).
+// Per-(device, n) launch geometry, computed once: resident blocks of the walk kernel, chunk walkers
+// (lane groups) per block, resident blocks of the constant-bank kernel (0 if that path does not exist
+// for n).  The first query also sets the walk kernel's dynamic shared-memory attribute on that device.
+// Read-only after initialisation (std::call_once), so concurrent calls stay safe.
+constexpr int kMaxDevices = 64;
+struct Geometry {
+    std::once_flag once;
+    cudaError_t err = cudaSuccess;
+    int max_grid = 0, nt = 0, max_grid_c = 0;
+};
+Geometry g_geom[kMaxDevices][perm::kMaxN + 1];
+
 perm_status_t device_threads(int n, int* max_grid, int* nt, int* max_grid_c = nullptr) {
-    int dev = 0, sms = 0, bps = 0;
+    int dev = 0;
     PERM_CUDA(cudaGetDevice(&dev), "cudaGetDevice");
-    PERM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "cudaDeviceGetAttribute");
-    PERM_CUDA(perm::walk_occupancy_n(n, &bps, nt), "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
-    if (bps < 1) bps = 1;
-    *max_grid = sms * bps;
-    if (max_grid_c) {
-        int bc = 0;
-        PERM_CUDA(perm::walk_occupancy_c_n(n, &bc), "cudaOccupancyMaxActiveBlocksPerMultiprocessor(c)");
-        *max_grid_c = sms * bc;
-    }
+    if (dev < 0 || dev >= kMaxDevices) return cuda_fail(cudaErrorInvalidDevice, "device index");
+    Geometry& G = g_geom[dev][n];
+    std::call_once(G.once, [&] {
+        int sms = 0, bps = 0, bc = 0;
+        G.err = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (G.err == cudaSuccess) G.err = perm::walk_occupancy_n(n, &bps, &G.nt);
+        if (G.err == cudaSuccess) G.err = perm::walk_occupancy_c_n(n, &bc);
+        if (bps < 1) bps = 1;
+        G.max_grid = sms * bps;
+        G.max_grid_c = sms * bc;
+    });
+    if (G.err != cudaSuccess) return cuda_fail(G.err, "walk geometry");
+    *max_grid = G.max_grid;
+    *nt = G.nt;
+    if (max_grid_c) *max_grid_c = G.max_grid_c;
     return PERM_OK;
 }
 

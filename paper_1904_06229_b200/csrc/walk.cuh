@@ -422,7 +422,9 @@ __global__ void __launch_bounds__(WalkCfg<N>::NT, WalkCfg<N>::MINB) walk_kernel(
 // loop-invariant columns are hoisted into vector registers and the kernel spills.
 template <int N>
 struct WalkParamsC {
-    double2 col[N][N];                     // col[j][i] = a_ij
+    static constexpr int NC = walk_inner_bits(N);   // columns held in the constant bank (the inner flips)
+    double2 col[NC][N];                    // col[j][i] = a_ij, j < U
+    const double2* A;                      // device, row-major (staged to shared memory)
     ddc* partials;                         // [gridDim.x]
     uint64_t c0;                           // first body chunk
     uint64_t count;                        // body chunks
@@ -483,7 +485,11 @@ __device__ __forceinline__ void walk_chunk_const(const WalkParamsC<C::N>& P, uin
     constexpr int kFoldMask = (U >= kWalkFoldBits) ? 0 : ((1 << (kWalkFoldBits - U)) - 1);
     double ar = 0.0, ai = 0.0;
     for (int q = 0; q < nblk; q++) {
+#ifdef PERM_CONST_SHFL_Z
+        const int z = __shfl_sync(0xffffffffu, q >> 30, 0);   // 0; explicitly warp-uniform, loop-variant
+#else
         const int z = q >> 30;                            // 0 (nblk <= 2^27); uniform, loop-variant
+#endif
         if (q > 0) {
             const int j = U + __ffs(q) - 1;
             const uint64_t nb = (j + 1 < e) ? (uint64_t)((q >> (j + 1 - U)) & 1) : cpar;
@@ -505,7 +511,10 @@ __global__ void __launch_bounds__(kWalkThreads) walk_kernel_c(const __grid_const
     using C = WCfg<N, 1>;
     __shared__ double2 scol[N * N];                          // scol[j*N + i] = a_ij (seeding, outer flips)
     __shared__ double2 sbase[N];
-    for (int k = threadIdx.x; k < N * N; k += blockDim.x) scol[k] = P.col[k / N][k % N];
+    for (int k = threadIdx.x; k < N * N; k += blockDim.x) {
+        const int i = k / N, j = k - i * N;
+        scol[j * N + i] = P.A[k];
+    }
     __syncthreads();
     for (int i = threadIdx.x; i < N; i += blockDim.x) {     // App. A step 5, summed in column order
         double sr = 0.0, si = 0.0;
@@ -590,9 +599,7 @@ cudaError_t walk_launch_smem(const WalkLaunch& L, const Segment* seg, int nseg, 
     }
     P.seg_pre[kMaxSegments] = pre;
     P.nseg = nseg;
-    cudaError_t err = cudaFuncSetAttribute(walk_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)C::smem_bytes);
-    if (err != cudaSuccess) return err;
+    // the dynamic shared-memory attribute was set by walk_occupancy<N> (abi.cu geometry cache)
     walk_kernel<N><<<grid, C::NT, C::smem_bytes, L.stream>>>(P);
     return cudaGetLastError();
 }
@@ -606,8 +613,9 @@ cudaError_t walk_launch(const WalkLaunch& L) {
         if (L.use_const) {
             const Segment& b = L.seg[L.body];
             WalkParamsC<N> P;
-            for (int j = 0; j < N; j++)
+            for (int j = 0; j < WalkParamsC<N>::NC; j++)
                 for (int i = 0; i < N; i++) P.col[j][i] = L.A_host[(size_t)i * N + j];
+            P.A = L.A_dev;
             P.partials = L.partials;
             P.c0 = b.c0;
             P.count = b.count;
