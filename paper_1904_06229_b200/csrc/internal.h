@@ -15,10 +15,13 @@ constexpr int kMaxSegments = 96;
 
 // Inner unrolled Gray bits U(N) of the single-matrix walk: a block of 2^U consecutive ranks is
 // fully unrolled, so the columns 0..U-1 it touches are compile-time operands.
-#ifndef PERM_WALK_U
-#define PERM_WALK_U 3
-#endif
+// U = 3 (8-term blocks) up to n = 39, U = 2 from n = 40 (the 4n-register row sums leave ptxas less room
+// to overlap an 8-term block; measured +4% at n = 44, profiles/round1_walk_variants.md).
+#ifdef PERM_WALK_U
 __host__ __device__ constexpr int walk_inner_bits(int n) { return (n - 1) < PERM_WALK_U ? (n - 1) : PERM_WALK_U; }
+#else
+__host__ __device__ constexpr int walk_inner_bits(int n) { return n >= 40 ? 2 : ((n - 1) < 3 ? (n - 1) : 3); }
+#endif
 constexpr int kWalkThreads = 64;
 // Lanes that share one chunk in the single-matrix walk (rows split between them, K1).  The n
 // complex row sums take 4n registers; beyond n = 48 one lane cannot hold them without spilling, so
