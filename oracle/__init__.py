@@ -60,6 +60,7 @@ def _L():
             "oracle_range_c128": [P, i32, u64, u64, P],
             "oracle_distribute": [u64, u64, u64, P, P],
             "oracle_gray": [u64],
+            "oracle_ryser_weighted_c128": [P, P, i32, i32, P, P],
             "oracle_num_threads": [],
         }
         for name, args in sig.items():
@@ -218,3 +219,17 @@ def ryser_i01_batch(A) -> list[int]:
     if _L().oracle_ryser_i01_batch(_ptr(A), n, B, _ptr(out)) != 0:
         raise ValueError("oracle_ryser_i01_batch failed")
     return [_u128_to_int(out[b, 0], out[b, 1]) for b in range(B)]
+
+
+def ryser_weighted(C, mult) -> tuple[QC, float]:
+    """Eq. (4): per(A) of the n x n matrix whose distinct columns are the R columns of
+    C (n x R), column k repeated mult[k] times (sum mult = n).  Returns (value, sum_f |term_f|);
+    the second number is the scale of the rounding error of any evaluation of the sum."""
+    C = _c128(C)
+    m = np.ascontiguousarray(np.asarray(mult, dtype=np.int32))
+    n, R = C.shape
+    out = np.zeros(4, dtype=np.float64)
+    a = np.zeros(2, dtype=np.float64)
+    if _L().oracle_ryser_weighted_c128(_ptr(C), _ptr(m), n, R, _ptr(out), _ptr(a)) != 0:
+        raise ValueError("oracle_ryser_weighted_c128 failed")
+    return QC(out), float(a[0] + a[1])

@@ -25,11 +25,15 @@
  *   oracle_seed_c128      App. A steps 2,5-8: w(r)
  *   oracle_naive_i01 / oracle_ryser_i01   Eq. (1) / Eq. (3) in exact integers
  *   oracle_distribute, oracle_gray        App. A distribute P:1077-1095, Gray unrank P:1097-1106
+ *   oracle_ryser_weighted_c128  Eq. (4), P:137-158 (repeated columns); pinned against Eq. (3) on the
+ *                                expanded matrix, R = 1 (n! prod c_i) and the Boson-sampling
+ *                                normalisation with collisions
  */
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
 #include <omp.h>
+#include <quadmath.h>
 
 typedef __float128 quad;
 typedef struct { quad re, im; } qc;            /* complex binary128 */
@@ -382,6 +386,77 @@ int oracle_range_c128(const double* A, int n, uint64_t k0, uint64_t k1, double* 
     for (int k = 0; k < nt; k++) S = qc_add(S, part[k]);
     free(part);
     put_qc(out4, S);
+    return 0;
+}
+
+/* ---------------- Eq. (4): weighted Ryser for repeated columns ----------------
+ * A has R distinct columns cbar_1..cbar_R, column cbar_k repeated m_k times (sum m_k = n).
+ * per(A) = (-1)^n sum_{f in Omega} (-1)^{sum_t f_t} (prod_j C(m_j, f_j)) prod_{i=1}^n sum_{k=1}^R f_k cbar_i(k),
+ * Omega = {f : 0 <= f_k <= m_k}.  Written out literally: Omega is enumerated in plain odometer
+ * order (digit 0 fastest), every row sum is recomputed from its definition, binomials are exact
+ * integers (Pascal's triangle in unsigned __int128), arithmetic is binary128.  The outermost digit's
+ * values are split over OpenMP threads; the partial sums are added in digit order.
+ * C is n x R row-major (cbar_i(k) = C[i][k]); out4 = value (hi,lo re, hi,lo im); out2 (optional) =
+ * sum_f |term_f| as (hi, lo), the scale of the rounding error of any evaluation of the sum. */
+static quad binom_q(int m, int f) {
+    u128 c = 1;
+    for (int t = 1; t <= f; t++) c = c * (u128)(m - f + t) / (u128)t;   /* exact at every step */
+    return (quad)c;
+}
+
+int oracle_ryser_weighted_c128(const double* C, const int* mult, int n, int R, double* out4, double* out2) {
+    if (n < 1 || n > 40 || R < 1 || R > n) return 1;
+    int tot = 0;
+    for (int k = 0; k < R; k++) {
+        if (mult[k] < 0) return 1;
+        tot += mult[k];
+    }
+    if (tot != n) return 1;
+    const int top = R - 1;
+    const int nt = mult[top] + 1;
+    qc* part = (qc*)calloc((size_t)nt, sizeof(qc));
+    quad* apart = (quad*)calloc((size_t)nt, sizeof(quad));
+    #pragma omp parallel for schedule(dynamic, 1)
+    for (int ftop = 0; ftop < nt; ftop++) {
+        int f[64];
+        for (int k = 0; k < R; k++) f[k] = 0;
+        f[top] = ftop;
+        qc S = { 0, 0 };
+        quad Sa = 0;
+        for (;;) {
+            quad W = 1;
+            int fs = 0;
+            for (int k = 0; k < R; k++) { W *= binom_q(mult[k], f[k]); fs += f[k]; }
+            qc p = { 1, 0 };
+            for (int i = 0; i < n; i++) {
+                qc rs = { 0, 0 };
+                for (int k = 0; k < R; k++) {
+                    qc c = { (quad)C[2 * ((size_t)i * R + k)], (quad)C[2 * ((size_t)i * R + k) + 1] };
+                    rs = qc_add(rs, qc_scale(c, (quad)f[k]));
+                }
+                p = qc_mul(p, rs);
+            }
+            p = qc_scale(p, W);
+            if (fs & 1) S = qc_sub(S, p); else S = qc_add(S, p);
+            quad ab = p.re * p.re + p.im * p.im;
+            Sa += sqrtq(ab);
+            /* odometer over digits 0 .. R-2 */
+            int k = 0;
+            while (k < top && f[k] == mult[k]) { f[k] = 0; k++; }
+            if (k == top) break;
+            f[k]++;
+        }
+        part[ftop] = S;
+        apart[ftop] = Sa;
+    }
+    qc S = { 0, 0 };
+    quad Sa = 0;
+    for (int t = 0; t < nt; t++) { S = qc_add(S, part[t]); Sa += apart[t]; }
+    free(part);
+    free(apart);
+    if (n & 1) S = qc_scale(S, -1);
+    put_qc(out4, S);
+    if (out2) put_q(out2, Sa);
     return 0;
 }
 

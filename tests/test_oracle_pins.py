@@ -304,3 +304,70 @@ def test_ryser_batch_matches_single():
     for b in range(5):
         ref = oracle.naive(A[b]).value
         assert _close(got[b], ref, 1e-14, max(abs(ref), pins.scaled_floor(A[b])))
+
+
+# ------------------------------------------------------------------ Eq. (4) weighted Ryser pins (NEXT-1)
+
+def _expand(C, mult):
+    return np.repeat(np.asarray(C), np.asarray(mult), axis=1)
+
+
+@pytest.mark.parametrize("mult", [(1, 1, 1, 1, 1), (2, 1, 1), (3, 2, 2), (1, 4), (2, 2, 2, 2), (5, 0, 2, 1)])
+def test_weighted_matches_eq3_on_expanded_matrix(mult):
+    # Eq. (4) against Eq. (3) / Eq. (1) of the matrix with the columns repeated: different formulas
+    # (2^n subsets vs prod (m_k+1) multiplicity vectors), same permanent
+    n = sum(mult)
+    rng = np.random.default_rng(400 + n + len(mult))
+    C = (rng.standard_normal((n, len(mult))) + 1j * rng.standard_normal((n, len(mult)))) / np.sqrt(2)
+    val, asum = oracle.ryser_weighted(C, mult)
+    A = _expand(C, mult)
+    ref = oracle.naive(A).value if n <= 9 else oracle.ryser(A).value
+    assert abs(val.value - ref) <= 1e-25 * asum + 1e-28
+
+
+def test_weighted_all_distinct_is_eq3():
+    # all m_k = 1: every weight is 1 and Omega = subsets, i.e. Eq. (4) is Eq. (3) term by term
+    rng = np.random.default_rng(9)
+    for n in (1, 2, 5, 10):
+        C = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+        val, asum = oracle.ryser_weighted(C, [1] * n)
+        assert abs(val.value - oracle.ryser(C).value) <= 1e-25 * asum
+
+
+def test_weighted_single_column_factorial():
+    # R = 1: per of n copies of one column = n! prod_i c_i (every permutation gives the same product);
+    # Eq. (4) then reads (-1)^n sum_f (-1)^f C(n,f) f^n prod c_i, a Stirling-number identity
+    for n in (1, 2, 3, 7, 12, 20):
+        val, _ = oracle.ryser_weighted(np.ones((n, 1)), [n])
+        assert val.value == complex(math.factorial(n))
+        c = np.arange(1, n + 1, dtype=float) * (1 - 0.5j)
+        val, asum = oracle.ryser_weighted(c[:, None], [n])
+        ref = math.factorial(n) * np.prod(c.astype(np.complex128))
+        assert abs(val.value - ref) <= 1e-25 * asum + 1e-14 * abs(ref)
+
+
+def test_weighted_integer_brute_force():
+    # small integer columns: exact brute force over all n! permutations in Python integers
+    rng = np.random.default_rng(5)
+    for mult in ((2, 1), (1, 2, 1), (3, 1, 1), (2, 2, 1)):
+        n = sum(mult)
+        C = rng.integers(-3, 4, size=(n, len(mult)))
+        A = _expand(C, mult)
+        ref = sum(math.prod(int(A[i, p[i]]) for i in range(n)) for p in itertools.permutations(range(n)))
+        val, _ = oracle.ryser_weighted(C.astype(np.complex128), mult)
+        assert val.value == complex(ref)
+
+
+def test_weighted_boson_sampling_normalization_with_collisions():
+    # P13 with repeated output modes computed directly by Eq. (4): for a Haar unitary U (m x m) and
+    # input rows S, sum over output multisets T of |per(U_{S,T})|^2 / prod_j t_j! = 1, where each
+    # per(U_{S,T}) is evaluated from the DISTINCT columns of T and their multiplicities
+    for (m, n) in ((4, 2), (5, 3), (6, 4)):
+        U = inputs.haar_unitary(m, 177 + m)
+        S = np.arange(n)
+        tot = 0.0
+        for T in itertools.combinations_with_replacement(range(m), n):
+            modes, counts = np.unique(np.array(T), return_counts=True)
+            val, _ = oracle.ryser_weighted(U[np.ix_(S, modes)], counts)
+            tot += abs(val.value) ** 2 / math.prod(math.factorial(int(c)) for c in counts)
+        assert abs(tot - 1.0) < 1e-13
