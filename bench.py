@@ -48,6 +48,27 @@ def fp64_nominal_tflops(sm_mhz: float = SM_MAX_MHZ, sms: int = SMS_NOMINAL) -> f
     return sms * FP64_LANES_PER_SM * 2 * sm_mhz * 1e6 / 1e12
 
 
+INT_LANES_PER_SM = 128           # 4 SMSPs x (16-lane fma pipe + 16-lane alu pipe) = 1 warp-instr/clk/SMSP
+
+
+def int_nominal_tops(sm_mhz: float = SM_MAX_MHZ, sms: int = SMS_NOMINAL) -> float:
+    """Integer-op peak (T ops/s): every SMSP issues one 32-lane integer instruction per clock, split
+    over the fma pipe (IMAD) and the alu pipe (IADD3/LOP3), each 16 lanes wide (B300_MICROARCH
+    "Pipe rates": rt_SMSP = 2 for both)."""
+    return sms * INT_LANES_PER_SM * sm_mhz * 1e6 / 1e12
+
+
+def ncu_traffic(cfg: str):
+    """DRAM bytes (read + write) per launch of the config's dominant kernel from the committed
+    `ncu --set full` capture summary (profiles/ncu_traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            t = json.load(f).get(cfg)
+        return None if t is None else float(t["dram_bytes_per_launch"])
+    except (OSError, ValueError, KeyError):
+        return None
+
+
 # ------------------------------------------------------------------------------------------ clocks
 
 class ClockSampler:
@@ -422,7 +443,7 @@ def run_ours(args):
     if roofline_units is not None:
         achieved = roofline_units / (walk_ms * 1e-3) / 1e12
         out["roofline"] = {"bound": "alu", "achieved": achieved, "peak": nominal, "unit": "TFLOP/s",
-                           "frac": achieved / nominal, "traffic": None,
+                           "frac": achieved / nominal, "traffic": ncu_traffic(cfg),
                            "kernel": "walk_kernel<n> (FP64 vector pipe)",
                            "algorithmic": "8n flops per Gray term x terms per launch (rank 0)",
                            "peak_note": "derived: 148 SMs x 64 FP64 FMA/clk x 2 x 1965 MHz",
@@ -436,15 +457,21 @@ def run_ours(args):
             fl = sum(100000 / world * (1 << (n - 1)) * 8 * n for n in (8, 12, 16, 20))
             achieved = fl / (dev_ms / K * 1e-3) / 1e12
             out["roofline"] = {"bound": "alu", "achieved": achieved, "peak": nominal, "unit": "TFLOP/s",
-                               "frac": achieved / nominal, "traffic": None,
+                               "frac": achieved / nominal, "traffic": ncu_traffic(cfg),
                                "kernel": "batched_kernel<n> x4 (FP64 vector pipe)",
                                "algorithmic": "8n flops per Gray term x 2^(n-1) terms x 10^5 per n",
                                "peak_measured_probe": peak_meas}
         else:
-            terms = units_per_step * (1 << 23) / world
-            out["roofline"] = {"bound": "alu", "achieved": terms / (dev_ms / K * 1e-3) / 1e12,
-                               "peak": None, "unit": "Tterms/s", "frac": None, "traffic": None,
-                               "kernel": "int01_kernel<24> (INT pipes)"}
+            # algorithmic integer ops per Gray term: n row-sum adds + (n-1) multiplies + 1 signed add
+            n3 = 24
+            ops = units_per_step / world * (1 << (n3 - 1)) * 2 * n3
+            achieved = ops / (dev_ms / K * 1e-3) / 1e12
+            ipeak = int_nominal_tops()
+            out["roofline"] = {"bound": "alu", "achieved": achieved, "peak": ipeak, "unit": "Tops/s",
+                               "frac": achieved / ipeak, "traffic": ncu_traffic(cfg),
+                               "kernel": "int01_kernel<24> (INT fma + alu pipes)",
+                               "algorithmic": "2n integer ops per Gray term x 2^(n-1) terms x 64 matrices",
+                               "peak_note": "derived: 148 SMs x 128 int lanes/clk (issue-bound) x 1965 MHz"}
     out["e2e"] = {"value": e2e_val, "unit": unit, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
     out["gpu_launches"] = gpu_launches_per_step * K
     out["clocks"] = clocks

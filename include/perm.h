@@ -116,6 +116,26 @@ perm_status_t perm_c128_batched(const perm_c128_t* A_dev, int n, int64_t B, perm
                                 double* abs2_dev, void* stream);
 
 /* ------------------------------------------------------------------------------------------
+ * Repeated columns: the weighted Ryser formula, Eq. (4).
+ * ------------------------------------------------------------------------------------------ */
+
+/* per and |per|^2 of B matrices with repeated columns, each given by its R distinct columns and their
+ * multiplicities (Boson-sampling output patterns with collisions):
+ *     per(A) = (-1)^n sum_{0<=f_k<=m_k} (-1)^{sum f} prod_k C(m_k, f_k) prod_i sum_k f_k cbar_i(k),
+ * prod_k (m_k + 1) terms instead of 2^{n-1}, walked in reflected mixed-radix Gray order.
+ *   C_dev      device, B*n*R perm_c128_t; problem b's distinct columns at C_dev + b*n*R, row-major
+ *              n x R (entry (i, k) = cbar_i(k)).
+ *   mult_dev   device, B*R int32 multiplicities m_k >= 0 with sum_k m_k == n (zeros allowed, so one R
+ *              serves a batch of patterns with different numbers of distinct modes).
+ *   per_dev    device, B perm_c128_t, or NULL.       abs2_dev   device, B doubles |per|^2, or NULL.
+ * 1 <= n <= 32, 1 <= R <= 64.  Stream-ordered: returns after enqueueing.  B == 0 is a no-op.  A problem
+ * whose multiplicities are invalid (negative, > n, or not summing to n) gets NaN outputs; non-finite
+ * entries propagate to that problem's outputs only.
+ * Errors: PERM_E_ARG (NULL input, B < 0, R outside 1..64, both outputs NULL), PERM_E_ORDER, PERM_E_CUDA. */
+perm_status_t perm_c128_weighted_batched(const perm_c128_t* C_dev, const int32_t* mult_dev, int n, int R,
+                                         int64_t B, perm_c128_t* per_dev, double* abs2_dev, void* stream);
+
+/* ------------------------------------------------------------------------------------------
  * Exact permanents of 0-1 matrices (BASELINE config 3; #P-hard even for 0-1).
  * ------------------------------------------------------------------------------------------ */
 

@@ -11,6 +11,7 @@ Names follow the C ABI:
 * :func:`perm_c128_range`    -- raw partial over a Gray-rank span (App. A subpermanent)
 * :func:`perm_c128_finalize` -- 2(-1)^n * ordered dd sum of partials
 * :func:`perm_c128_batched`  -- per and |per|^2 of a batch of small matrices
+* :func:`perm_c128_weighted_batched` -- repeated columns, weighted Ryser Eq. (4)
 * :func:`perm_int01`         -- exact int128 permanents of 0-1 matrices
 """
 from __future__ import annotations
@@ -105,6 +106,7 @@ def lib() -> ctypes.CDLL:
         "perm_c128_range": [P, i32, u64, u64, P, P, sz, P, P],
         "perm_c128_finalize": [P, i32, i32, P, P],
         "perm_c128_batched": [P, i32, i64, P, P, P],
+        "perm_c128_weighted_batched": [P, P, i32, i32, i64, P, P, P],
         "perm_int01_workspace_bytes": [i32, i64, ctypes.POINTER(sz)],
         "perm_int01": [P, i32, i64, P, P, sz, P],
         "perm_c128_seed": [P, i32, P, i32, P, P],
@@ -291,6 +293,32 @@ def perm_c128_batched(A, *, per=None, abs2=None, want_per: bool = True, want_abs
     return per, abs2
 
 
+def perm_c128_weighted_batched(C, mult, *, per=None, abs2=None, want_per: bool = True, want_abs2: bool = True,
+                               stream=None):
+    """per and |per|^2 of B matrices with repeated columns (Eq. (4)): C is a (B, n, R)
+    complex128 CUDA tensor of distinct columns, mult a (B, R) int32 CUDA tensor of multiplicities
+    (sum over R == n; zeros allowed).  Stream-ordered.  Returns (per, abs2) CUDA tensors."""
+    torch = _torch()
+    if not (_is_torch(C) and C.is_cuda and _is_torch(mult) and mult.is_cuda):
+        raise ValueError("perm_c128_weighted_batched expects CUDA torch tensors C (B, n, R), mult (B, R)")
+    if C.dtype != torch.complex128 or mult.dtype != torch.int32:
+        raise ValueError("C must be complex128 and mult int32")
+    C = C.contiguous()
+    mult = mult.contiguous()
+    B, n, R = C.shape
+    if tuple(mult.shape) != (B, R):
+        raise ValueError("mult must have shape (B, R)")
+    if per is None and want_per:
+        per = torch.empty(B, dtype=torch.complex128, device=C.device)
+    if abs2 is None and want_abs2:
+        abs2 = torch.empty(B, dtype=torch.float64, device=C.device)
+    _check(lib().perm_c128_weighted_batched(ctypes.c_void_p(C.data_ptr()), ctypes.c_void_p(mult.data_ptr()), n, R, B,
+                                            ctypes.c_void_p(per.data_ptr() if per is not None else 0),
+                                            ctypes.c_void_p(abs2.data_ptr() if abs2 is not None else 0),
+                                            _stream_ptr(stream)))
+    return per, abs2
+
+
 def int01_workspace_bytes(n: int, B: int) -> int:
     b = ctypes.c_size_t()
     _check(lib().perm_int01_workspace_bytes(n, B, ctypes.byref(b)))
@@ -337,6 +365,7 @@ def perm_fp64_probe(blocks: int, threads: int, iters: int, sink, stream=None):
     _check(lib().perm_fp64_probe(blocks, threads, iters, ctypes.c_void_p(sink.data_ptr()), _stream_ptr(stream)))
 
 
-__all__ = ["perm_c128", "perm_c128_range", "perm_c128_finalize", "perm_c128_batched", "perm_int01",
+__all__ = ["perm_c128", "perm_c128_range", "perm_c128_finalize", "perm_c128_batched", "perm_c128_weighted_batched",
+           "perm_int01",
            "perm_c128_seed", "perm_fp64_probe", "workspace_bytes", "make_workspace", "int01_workspace_bytes",
            "PermError", "DD", "lib", "header_functions", "last_launches"]

@@ -4,6 +4,7 @@
 #include <cmath>
 #include <mutex>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -63,6 +64,11 @@ int choose_b(int n, uint64_t total, uint64_t T) {
     if (b > n - 1) b = n - 1;
     if (b > 30) b = 30;
     if (b < 0) b = 0;
+    // development override (profiling a sub-range at the full run's chunk length)
+    if (const char* f = getenv("PERM_FORCE_CHUNK_LOG2")) {
+        const int fb = atoi(f);
+        if (fb >= U && fb <= n - 1 && fb <= 30) b = fb;
+    }
     return b;
 }
 
@@ -145,7 +151,7 @@ perm_status_t plan_walk(int n, uint64_t k0, uint64_t k1, WalkPlan& p) {
     perm_status_t st = device_threads(n, &max_grid, &nt, &max_grid_c);
     if (st != PERM_OK) return st;
     p.threads = nt;
-    const uint64_t T = (uint64_t)(max_grid_c > 0 ? max_grid_c * perm::kWalkThreads : max_grid * nt);
+    const uint64_t T = (uint64_t)(max_grid_c > 0 ? max_grid_c * perm::walk_block_threads(n) : max_grid * nt);
     p.b = choose_b(n, k1 - k0, T);
     if (!decompose(n, k0, k1, p.b, p)) {
         snprintf(g_err, sizeof(g_err), "range decomposition exceeded %d segments", perm::kMaxSegments);
@@ -156,12 +162,12 @@ perm_status_t plan_walk(int n, uint64_t k0, uint64_t k1, WalkPlan& p) {
     if (max_grid_c > 0) {
         int best = -1;
         for (int s = 0; s < p.nseg; s++)
-            if (p.seg[s].e > 0 && (best < 0 || p.seg[s].count > p.seg[best].count)) best = s;
+            if (p.seg[s].e > perm::walk_inner_bits(n) && (best < 0 || p.seg[s].count > p.seg[best].count)) best = s;
         if (best >= 0) {
             p.use_const = 1;
             p.body = best;
             const uint64_t body = p.seg[best].count;
-            const uint64_t wc = perm::kWalkThreads;
+            const uint64_t wc = perm::walk_block_threads(n);
             uint64_t need = (body + wc - 1) / wc;
             p.grid = (int)(need < (uint64_t)max_grid_c ? need : (uint64_t)max_grid_c);
             if (p.grid < 1) p.grid = 1;
@@ -309,7 +315,7 @@ perm_status_t run_walk(const perm_c128_t* A, int n, uint64_t k0, uint64_t k1, in
         if (stats) {
             stats->terms = k1 - k0;
             stats->chunk_log2 = (uint32_t)p.b;
-            stats->threads = (uint32_t)((p.grid + p.grid_edge) * perm::kWalkThreads);
+            stats->threads = (uint32_t)((p.grid + p.grid_edge) * perm::walk_block_threads(n));
             stats->blocks = (uint32_t)(p.grid + p.grid_edge);
             stats->launches = launches;
         }
@@ -413,6 +419,21 @@ perm_status_t perm_c128_batched(const perm_c128_t* A_dev, int n, int64_t B, perm
     cudaError_t e = perm::batched_launch((const double2*)A_dev, n, B, (double2*)per_dev, abs2_dev,
                                          (cudaStream_t)stream, &launches);
     if (e != cudaSuccess) return cuda_fail(e, "batched kernel launch");
+    g_launches = (uint32_t)launches;
+    return PERM_OK;
+}
+
+perm_status_t perm_c128_weighted_batched(const perm_c128_t* C_dev, const int32_t* mult_dev, int n, int R,
+                                         int64_t B, perm_c128_t* per_dev, double* abs2_dev, void* stream) {
+    g_launches = 0;
+    if (B < 0 || R < 1 || R > perm::kMaxWeightedR) return PERM_E_ARG;
+    if (n < 1 || n > perm::kMaxBatchedN) return PERM_E_ORDER;
+    if (B == 0) return PERM_OK;
+    if (!C_dev || !mult_dev || (!per_dev && !abs2_dev)) return PERM_E_ARG;
+    int launches = 0;
+    cudaError_t e = perm::weighted_launch((const double2*)C_dev, mult_dev, n, R, B, (double2*)per_dev, abs2_dev,
+                                          (cudaStream_t)stream, &launches);
+    if (e != cudaSuccess) return cuda_fail(e, "weighted kernel launch");
     g_launches = (uint32_t)launches;
     return PERM_OK;
 }

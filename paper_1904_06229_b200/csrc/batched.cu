@@ -6,7 +6,7 @@
 // single-matrix kernel (walk.cuh: seeding, unrolled inner blocks, dd accumulation).  For n >= 12 a
 // whole warp walks one matrix, so every column read is a warp-uniform shared-memory broadcast; for
 // small n (few terms per matrix) several matrices share a warp.  Each warp stages its matrices
-// (coalesced global reads) column-major into its own shared-memory slice.  The group's dd partials
+// (coalesced global reads) column-major, with a negated copy, into its own shared-memory slice.  The group's dd partials
 // are combined with a fixed shuffle tree; lane 0 applies 2(-1)^n (App. A permanent step 4)
 // and writes per (rounded from dd) and |per|^2 = re^2 + im^2 of that rounded value.
 #include "walk.cuh"
@@ -21,7 +21,7 @@ struct BatCfg {
     static constexpr int E = N - 1 - LOG_L;       // log2 ranks per lane
     static constexpr int WARPS = 4;
     static constexpr int NT = 32 * WARPS;
-    static constexpr int MAT = N * N + N;         // double2 per matrix slot (columns + base)
+    static constexpr int MAT = 2 * N * N + N;     // double2 per matrix slot (columns, negated columns, base)
     static constexpr int SLOT = MAT + 1;          // +1 double2 pad: consecutive slots start in different banks
     static constexpr size_t smem_bytes = (size_t)WARPS * G * SLOT * sizeof(double2);
 };
@@ -43,7 +43,9 @@ __global__ void __launch_bounds__(BatCfg<N>::NT) batched_kernel(const double2* _
     for (int k = lane; k < gcount * N * N; k += 32) {
         const int g = k / (N * N), r = k - g * (N * N);
         const int i = r / N, j = r - i * N;
-        wbase[g * C::SLOT + j * N + i] = src[k];
+        const double2 a = src[k];
+        wbase[g * C::SLOT + j * N + i] = a;
+        wbase[g * C::SLOT + N * N + j * N + i] = make_double2(-a.x, -a.y);
     }
     __syncwarp();
     for (int k = lane; k < gcount * N; k += 32) {
@@ -54,7 +56,7 @@ __global__ void __launch_bounds__(BatCfg<N>::NT) batched_kernel(const double2* _
             sr += sc[j * N + i].x;
             si += sc[j * N + i].y;
         }
-        wbase[g * C::SLOT + N * N + i] =
+        wbase[g * C::SLOT + 2 * N * N + i] =
             make_double2(sc[(N - 1) * N + i].x - 0.5 * sr, sc[(N - 1) * N + i].y - 0.5 * si);
     }
     __syncwarp();
@@ -63,9 +65,9 @@ __global__ void __launch_bounds__(BatCfg<N>::NT) batched_kernel(const double2* _
     ddc acc;
     acc.re.hi = acc.re.lo = acc.im.hi = acc.im.lo = 0.0;
     if (g < gcount) {
-        using WC = WCfg<N, 1>;   // one lane per chunk; column stride N (no padding)
+        using WC = WCfg<N, 1>;   // one lane per chunk; column stride N (no padding); -A at WC::NEG
         const uint32_t sc = (uint32_t)__cvta_generic_to_shared(wbase + g * C::SLOT);
-        const uint32_t sbase = sc + (uint32_t)(N * N) * 16u;
+        const uint32_t sbase = sc + (uint32_t)(2 * N * N) * 16u;
         if constexpr (C::E == 0) {
             single_term<WC>(sc, sbase, 0u, (uint64_t)l, acc);
         } else {

@@ -36,6 +36,16 @@ constexpr int kWalkThreads = 64;
 __host__ __device__ constexpr int walk_lanes_per_chunk(int n) {
     return n >= PERM_WALK_S4_MIN ? 4 : (n >= PERM_WALK_S2_MIN ? 2 : 1);
 }
+// Threads per block of the shared-memory walk.  Each block stages A and -A column-major plus the base
+// vector, (2 n P + P) x 16 bytes (P = padded rows); at n = 44 that is 62.6 KB, so 64-thread blocks
+// (4 per SM at 255 registers) would not fit the 228 KB of shared memory per SM -- larger orders get
+// larger blocks instead of fewer warps.
+__host__ __device__ constexpr int walk_block_threads(int n) {
+    const int s = walk_lanes_per_chunk(n);
+    const int p = ((n + s - 1) / s) * s;
+    const long bytes = (2L * n * p + p) * 16L;
+    return bytes * 4 <= 200L * 1024 ? kWalkThreads : (bytes * 2 <= 220L * 1024 ? 2 * kWalkThreads : 4 * kWalkThreads);
+}
 // Plain-double partial sums are folded into the per-thread double-double accumulator every
 // 2^kWalkFoldBits terms (R7).
 #ifndef PERM_WALK_FOLD
@@ -99,6 +109,11 @@ cudaError_t fp64_probe_launch(int blocks, int threads, int iters, double* sink, 
 // batched.cu
 cudaError_t batched_launch(const double2* A, int n, int64_t B, double2* per, double* abs2, cudaStream_t s,
                            int* launches);
+
+// weighted.cu
+constexpr int kMaxWeightedR = 64;
+cudaError_t weighted_launch(const double2* C, const int32_t* mult, int n, int R, int64_t B, double2* per,
+                            double* abs2, cudaStream_t s, int* launches);
 
 // int01.cu
 size_t int01_workspace_bytes(int n, int64_t B);

@@ -40,13 +40,15 @@ struct WCfg {
     static constexpr int S = S_;                             // lanes per chunk
     static constexpr int R = (N + S - 1) / S;                // rows per lane
     static constexpr int P = R * S;                          // padded rows per column in shared memory
-    static constexpr int NT = kWalkThreads;
+    static constexpr int NT = walk_block_threads(N);
 #ifdef PERM_WALK_K
     static constexpr int K = R >= 16 ? PERM_WALK_K : (R >= 4 ? 2 : 1);
 #else
     static constexpr int K = R >= 4 ? 2 : 1;                 // independent product chains per lane
 #endif
-    static constexpr size_t smem_bytes = (size_t)(N * P + P) * sizeof(double2);
+    // columns a_{.j} (j < N), then their negations -a_{.j}, then the step-5 base vector
+    static constexpr uint32_t NEG = (uint32_t)(N * P) * 16u;   // byte offset of -a_{.j} from a_{.j}
+    static constexpr size_t smem_bytes = (size_t)(2 * N * P + P) * sizeof(double2);
     // Register budget per thread for S > 1: the 4R row-sum registers plus working set; it sets the
     // minimum resident blocks in __launch_bounds__ so ptxas does not trade occupancy for scheduling
     // freedom.  S = 1 is left uncapped (4n + ~30 registers).
@@ -96,13 +98,31 @@ __device__ __forceinline__ void cmul2(double& xr, double& xi, double yr, double 
     xr = nr;
 }
 
+// The same product with the roles of xr and xi swapped: the two DMULs read xr (the first result of
+// the previous cmul2), the DFMAs xi.  Alternating the two forms along a chain lets each multiply
+// start on the half of the previous result that is ready first.
+__device__ __forceinline__ void cmul2_alt(double& xr, double& xi, double yr, double yi) {
+    const double t = xr * yi;
+    const double u = xr * yr;
+    const double ni = fma(xi, yr, t);
+    xr = fma(-xi, yi, u);
+    xi = ni;
+}
+
 // Product of rows [B, E) into (pr, pi).
 template <int B, int E, int R>
 __device__ __forceinline__ void chain(const double (&wr)[R], const double (&wi)[R], double& pr, double& pi) {
     pr = wr[B];
     pi = wi[B];
 #pragma unroll
-    for (int i = B + 1; i < E; i++) cmul2(pr, pi, wr[i], wi[i]);
+    for (int i = B + 1; i < E; i++) {
+#ifdef PERM_CMUL_ALT
+        if ((i - B) & 1) cmul2(pr, pi, wr[i], wi[i]);
+        else             cmul2_alt(pr, pi, wr[i], wi[i]);
+#else
+        cmul2(pr, pi, wr[i], wi[i]);
+#endif
+    }
 }
 
 // Split prod_i w_i into two factors X * Y (K chains).
@@ -236,20 +256,34 @@ __device__ __forceinline__ void flip_static(uint32_t col, double (&wr)[R], doubl
     }
 }
 
+// w += column at shared address col (the address of a_{.j} or of -a_{.j} selects the sign): 2R DADD
+// with two vector operands each.  (fma(z, a, w) with a register sign z would read three vector register
+// pairs and issue at 2/3 of the FP64 pipe rate on sm_100a; tools/micro/fp64_reuse.cu.)
+template <int R>
+__device__ __forceinline__ void flip_add(uint32_t col, double (&wr)[R], double (&wi)[R]) {
+#pragma unroll
+    for (int i = 0; i < R; i++) {
+        const double2 a = lds_c(col + i * 16);
+        wr[i] += a.x;
+        wi[i] += a.y;
+    }
+}
+
 // Inner block: ranks t = 0 .. 2^U - 1 of the current block (t = 0 already seeded/flipped).
 // lc = this lane's address of row 0 of column 0 (columns are P rows apart).
 template <class C, int T>
 struct InnerStep {
     static constexpr int R = C::R;
-    static __device__ __forceinline__ void run(uint32_t lc, uint32_t h, double (&wr)[R], double (&wi)[R],
-                                               double zmid, double& ar, double& ai, double (&pr)[C::S],
+    static __device__ __forceinline__ void run(uint32_t lc, uint32_t lmid, uint32_t h, double (&wr)[R],
+                                               double (&wi)[R], double& ar, double& ai, double (&pr)[C::S],
                                                double (&pi)[C::S]) {
         constexpr int U = C::U;
         if constexpr (T > 0) {
             constexpr int J = ctz_c((unsigned)T);
             if constexpr (J == U - 1) {
-                // new bit = 1 ^ bit_U(rank): depends on the block (or chunk) parity -> signed by zmid
-                flip_dyn<R>(lc + (uint32_t)(J * C::P) * 16u, zmid, wr, wi);
+                // new bit = 1 ^ bit_U(rank): depends on the block (or chunk) parity; lmid is the address
+                // of +a_{.,U-1} or -a_{.,U-1} accordingly
+                flip_add<R>(lmid, wr, wi);
             } else {
                 constexpr bool PLUS = ((T >> (J + 1)) & 1) == 0;  // new bit = 1 ^ bit_{J+1}(t)
                 flip_static<R, PLUS>(lc + (uint32_t)(J * C::P) * 16u, wr, wi);
@@ -262,7 +296,7 @@ struct InnerStep {
             lane_product<R, C::K>(wr, wi, pr[T % C::S], pi[T % C::S]);
             if constexpr (T % C::S == C::S - 1) group_finish<C::S>(pr, pi, h, ar, ai);
         }
-        if constexpr (T + 1 < (1 << U)) InnerStep<C, T + 1>::run(lc, h, wr, wi, zmid, ar, ai, pr, pi);
+        if constexpr (T + 1 < (1 << U)) InnerStep<C, T + 1>::run(lc, lmid, h, wr, wi, ar, ai, pr, pi);
     }
 };
 
@@ -300,11 +334,11 @@ __device__ __forceinline__ void walk_chunk(uint32_t lc, uint32_t lb, uint32_t h,
             // block boundary: Gray bit j = U + ctz(q) flips to 1 ^ bit_{j+1}(rank)
             const int j = U + __ffsll((long long)q) - 1;
             const uint64_t nb = (j + 1 < e) ? ((q >> (j + 1 - U)) & 1ull) : cpar;
-            flip_dyn<R>(lc + (uint32_t)(j * C::P) * 16u, nb ? -1.0 : 1.0, wr, wi);
+            flip_add<R>(lc + (uint32_t)(j * C::P) * 16u + (nb ? C::NEG : 0u), wr, wi);
         }
         const uint64_t nbm = (U < e) ? (q & 1ull) : cpar;   // bit_U(rank) for the mid-block flip
-        const double zmid = nbm ? -1.0 : 1.0;
-        InnerStep<C, 0>::run(lc, h, wr, wi, zmid, ar, ai, pr, pi);
+        const uint32_t lmid = lc + (uint32_t)((U - 1) * C::P) * 16u + (nbm ? C::NEG : 0u);
+        InnerStep<C, 0>::run(lc, lmid, h, wr, wi, ar, ai, pr, pi);
         // fold the plain block sums into the dd accumulator every 2^kWalkFoldBits terms (and at the end)
         if (((q + 1) & kFoldMask) == 0 || q + 1 == nblk) {
             acc.re = dd_add_d(acc.re, ar);
@@ -352,7 +386,9 @@ __device__ __forceinline__ void stage_matrix(const double2* __restrict__ A, doub
     constexpr int N = C::N, P = C::P;
     for (int k = threadIdx.x; k < N * P; k += blockDim.x) {
         const int j = k / P, i = k - j * P;
-        sc[k] = (i < N) ? A[i * N + j] : make_double2(0.0, 0.0);
+        const double2 a = (i < N) ? A[i * N + j] : make_double2(0.0, 0.0);
+        sc[k] = a;
+        sc[N * P + k] = make_double2(-a.x, -a.y);   // negated copy (exact)
     }
     __syncthreads();
     for (int i = threadIdx.x; i < P; i += blockDim.x) {
@@ -374,11 +410,11 @@ template <int N>
 __global__ void __launch_bounds__(WalkCfg<N>::NT, WalkCfg<N>::MINB) walk_kernel(const __grid_constant__ WalkParams P) {
     using C = WalkCfg<N>;
     extern __shared__ double2 smem[];
-    stage_matrix<C>(P.A, smem, smem + N * C::P);
+    stage_matrix<C>(P.A, smem, smem + 2 * N * C::P);
     const uint32_t h = threadIdx.x % C::S;
     const uint32_t hoff = h * (uint32_t)C::R * 16u;
     const uint32_t lc = (uint32_t)__cvta_generic_to_shared(smem) + hoff;
-    const uint32_t lb = (uint32_t)__cvta_generic_to_shared(smem + N * C::P) + hoff;
+    const uint32_t lb = (uint32_t)__cvta_generic_to_shared(smem + 2 * N * C::P) + hoff;
 
     ddc acc;
     acc.re.hi = acc.re.lo = acc.im.hi = acc.im.lo = 0.0;
@@ -441,6 +477,8 @@ struct InnerStepC {
             constexpr int J = ctz_c((unsigned)T);
             const int jj = J + z * (T + 1);          // == J; distinct expression per use (no CSE/hoist)
             if constexpr (J == U - 1) {
+                // new bit = 1 ^ bit_U(rank): sign zmid = -+1 (the column is a uniform-register operand, so
+                // this DFMA reads only two vector registers)
 #pragma unroll
                 for (int i = 0; i < N; i++) {
                     const double2 a = P.col[jj][i];
@@ -480,7 +518,7 @@ __device__ __forceinline__ void walk_chunk_const(const WalkParamsC<C::N>& P, uin
         const double f = (double)((x >> j) & 1ull);
         flip_dyn<N>(lc + (uint32_t)(j * N) * 16u, f, wr, wi);
     }
-    const int nblk = 1 << (e - U);
+    const int nblk = 1 << (e - U);                        // >= 2: the planner sends only e > U here
     const uint64_t cpar = c & 1ull;
     constexpr int kFoldMask = (U >= kWalkFoldBits) ? 0 : ((1 << (kWalkFoldBits - U)) - 1);
     double ar = 0.0, ai = 0.0;
@@ -493,10 +531,9 @@ __device__ __forceinline__ void walk_chunk_const(const WalkParamsC<C::N>& P, uin
         if (q > 0) {
             const int j = U + __ffs(q) - 1;
             const uint64_t nb = (j + 1 < e) ? (uint64_t)((q >> (j + 1 - U)) & 1) : cpar;
-            flip_dyn<N>(lc + (uint32_t)(j * N) * 16u, nb ? -1.0 : 1.0, wr, wi);
+            flip_add<N>(lc + (uint32_t)(j * N) * 16u + (nb ? C::NEG : 0u), wr, wi);
         }
-        const uint64_t nbm = (U < e) ? (uint64_t)(q & 1) : cpar;
-        InnerStepC<C, 0>::run(P, z, wr, wi, nbm ? -1.0 : 1.0, ar, ai);
+        InnerStepC<C, 0>::run(P, z, wr, wi, (q & 1) ? -1.0 : 1.0, ar, ai);   // bit_U(rank) = q & 1 (e > U)
         if (((q + 1) & kFoldMask) == 0 || q + 1 == nblk) {
             acc.re = dd_add_d(acc.re, ar);
             acc.im = dd_add_d(acc.im, ai);
@@ -507,13 +544,16 @@ __device__ __forceinline__ void walk_chunk_const(const WalkParamsC<C::N>& P, uin
 }
 
 template <int N>
-__global__ void __launch_bounds__(kWalkThreads) walk_kernel_c(const __grid_constant__ WalkParamsC<N> P) {
+__global__ void __launch_bounds__(walk_block_threads(N)) walk_kernel_c(const __grid_constant__ WalkParamsC<N> P) {
     using C = WCfg<N, 1>;
-    __shared__ double2 scol[N * N];                          // scol[j*N + i] = a_ij (seeding, outer flips)
-    __shared__ double2 sbase[N];
+    extern __shared__ double2 smem[];
+    double2* scol = smem;                                    // scol[j*N + i] = a_ij, then -a_ij at + N*N
+    double2* sbase = smem + 2 * N * N;
     for (int k = threadIdx.x; k < N * N; k += blockDim.x) {
         const int i = k / N, j = k - i * N;
-        scol[j * N + i] = P.A[k];
+        const double2 a = P.A[k];
+        scol[j * N + i] = a;
+        scol[N * N + j * N + i] = make_double2(-a.x, -a.y);
     }
     __syncthreads();
     for (int i = threadIdx.x; i < N; i += blockDim.x) {     // App. A step 5, summed in column order
@@ -561,11 +601,11 @@ __global__ void seed_kernel(const double2* __restrict__ A, const uint64_t* __res
                             double2* __restrict__ out) {
     using C = WalkCfg<N>;
     extern __shared__ double2 smem[];
-    stage_matrix<C>(A, smem, smem + N * C::P);
+    stage_matrix<C>(A, smem, smem + 2 * N * C::P);
     const uint32_t h = threadIdx.x % C::S;
     const uint32_t hoff = h * (uint32_t)C::R * 16u;
     const uint32_t lc = (uint32_t)__cvta_generic_to_shared(smem) + hoff;
-    const uint32_t lb = (uint32_t)__cvta_generic_to_shared(smem + N * C::P) + hoff;
+    const uint32_t lb = (uint32_t)__cvta_generic_to_shared(smem + 2 * N * C::P) + hoff;
     const int groups = (int)(gridDim.x * (blockDim.x / C::S));
     for (int k = (int)(blockIdx.x * (blockDim.x / C::S) + threadIdx.x / C::S); k < count; k += groups) {
         const uint64_t r = ranks[k];
@@ -620,7 +660,7 @@ cudaError_t walk_launch(const WalkLaunch& L) {
             P.c0 = b.c0;
             P.count = b.count;
             P.eb = b.e;
-            walk_kernel_c<N><<<L.grid, kWalkThreads, 0, L.stream>>>(P);
+            walk_kernel_c<N><<<L.grid, walk_block_threads(N), WCfg<N, 1>::smem_bytes, L.stream>>>(P);
             cudaError_t err = cudaGetLastError();
             if (err != cudaSuccess || L.grid_edge == 0) return err;
             Segment rest[kMaxSegments];
@@ -637,8 +677,13 @@ cudaError_t walk_launch(const WalkLaunch& L) {
 template <int N>
 cudaError_t walk_occupancy_c(int* blocks_per_sm) {
     *blocks_per_sm = 0;
-    if constexpr (walk_const_path(N) && walk_lanes_per_chunk(N) == 1 && walk_inner_bits(N) >= 1)
-        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, walk_kernel_c<N>, kWalkThreads, 0);
+    if constexpr (walk_const_path(N) && walk_lanes_per_chunk(N) == 1 && walk_inner_bits(N) >= 1) {
+        cudaError_t err = cudaFuncSetAttribute(walk_kernel_c<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)WCfg<N, 1>::smem_bytes);
+        if (err != cudaSuccess) return err;
+        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, walk_kernel_c<N>, walk_block_threads(N),
+                                                             WCfg<N, 1>::smem_bytes);
+    }
     return cudaSuccess;
 }
 

@@ -106,3 +106,23 @@ def block_diag_scrambled(B1: np.ndarray, B2: np.ndarray, seed: int) -> tuple[np.
 
 def ones(n: int) -> np.ndarray:
     return np.ones((n, n), dtype=np.complex128)
+
+
+# ---------------------------------------------------------------- repeated columns (Eq. (4), NEXT-1)
+
+def collision_patterns(n: int, m: int, count: int, seed: int, R: int | None = None) -> tuple[np.ndarray, np.ndarray]:
+    """Boson-sampling output patterns WITH collisions: n photons enter the first n modes of an m-mode
+    Haar unitary U (seed); each pattern sends them to n output modes drawn uniformly WITH replacement
+    (sorted).  Returns C (count, n, R) complex128 -- the distinct output columns U[:n, mode] in
+    increasing mode order, zero-padded -- and mult (count, R) int32 -- their multiplicities, zero-padded;
+    R defaults to n.  Rows = input modes, columns = output modes."""
+    R = n if R is None else R
+    rng = np.random.default_rng(seed)
+    U = haar_unitary(m, rng)
+    C = np.zeros((count, n, R), dtype=np.complex128)
+    mult = np.zeros((count, R), dtype=np.int32)
+    for s in range(count):
+        modes, counts = np.unique(rng.integers(0, m, size=n), return_counts=True)
+        C[s, :, :len(modes)] = U[:n, modes]
+        mult[s, :len(modes)] = counts
+    return C, mult

@@ -24,12 +24,14 @@ def ev(fn, reps=3):
 
 
 tag = os.path.basename(os.environ.get("PERM_LIB", "libperm.so"))
-for n, span in ((20, None), (32, None), (44, 1 << 36)):
+ORDERS = os.environ.get("WALK_RATE_N", "20,32,44")
+for n, span in [(int(x), (1 << 36) if int(x) > 36 else None) for x in ORDERS.split(",") if x]:
     A = inputs.complex_gaussian((n, n), 44)
     ws = pb.make_workspace(n)
     terms = span or (1 << (n - 1))
     t = ev(lambda: pb.perm_c128_range(A, 0, terms, workspace=ws))
     print(f"{tag} n={n}: {terms / t:.4e} terms/s  {terms / t * 8 * n / 1e12:.2f} TF", flush=True)
-A = torch.from_numpy(inputs.cfg2(16, 100000)).cuda()
-t = ev(lambda: pb.perm_c128_batched(A))
-print(f"{tag} batched16: {1e5 / t:.4e} perms/s {1e5 * 2**15 * 128 / t / 1e12:.2f} TF", flush=True)
+if os.environ.get("WALK_RATE_BATCHED", "1") == "1":
+    A = torch.from_numpy(inputs.cfg2(16, 100000)).cuda()
+    t = ev(lambda: pb.perm_c128_batched(A))
+    print(f"{tag} batched16: {1e5 / t:.4e} perms/s {1e5 * 2**15 * 128 / t / 1e12:.2f} TF", flush=True)
