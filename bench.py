@@ -13,6 +13,8 @@ Workloads (BASELINE.json configs; synthetic inputs from paper_1904_06229_b200/in
   cfg1: one 16x16 complex Gaussian (latency-bound).
   cfg2: 10^5 submatrices of an n^2 x n^2 Haar unitary for each n in {8,12,16,20}; batched perms/s.
   cfg3: 64 Bernoulli 0-1 matrices of order 24; exact int128; perms/s.
+  cfgw: 10^4 Boson-sampling output patterns with collisions (20 photons, 20 modes), weighted Ryser
+        Eq. (4) (not a BASELINE config); perms/s.
 
 A step is one pass of the whole hot path over the config's input: walk + in-GPU reduction + (N > 1)
 the all-gather + ordered combine.  `value` is timed with CUDA events on the compute stream from the
@@ -231,6 +233,16 @@ def oracle_rate_cfg(cfg: str, seconds: float = 12.0) -> dict:
         dt = time.perf_counter() - t0
         return {"value": k / dt, "unit": "perms/s", "cores": cores, "kind": "oracle",
                 "sample": f"Eq. (3) int128 oracle on {k} of the 64 config-3 matrices, {dt:.1f} s"}
+    if cfg == "cfgw":
+        C, M = inputs.cfgw()
+        t0 = time.perf_counter()
+        k = 0
+        while time.perf_counter() - t0 < seconds and k < C.shape[0]:
+            oracle.ryser_weighted(C[k], M[k])
+            k += 1
+        dt = time.perf_counter() - t0
+        return {"value": k / dt, "unit": "perms/s", "cores": cores, "kind": "oracle",
+                "sample": f"Eq. (4) binary128 oracle on the first {k} of the 10^4 cfgw patterns, {dt:.1f} s"}
     raise ValueError(cfg)
 
 
@@ -392,6 +404,46 @@ def run_ours(args):
         config = {"workload": "64 Bernoulli(1/2) 0-1 matrices of order 24 (seed 24), exact int128 permanents",
                   "parallelism": f"batch x{world}", "l2": "input 37 KB; compute-bound"}
         scaling = "weak" if world > 1 else "strong"
+    elif cfg == "cfgw":
+        C_np, M_np = inputs.cfgw()
+        B, n, R = C_np.shape
+        b0, b1 = shard.rank_span(B, world, rank)
+        hostC = torch.from_numpy(np.ascontiguousarray(C_np[b0:b1])).pin_memory()
+        hostM = torch.from_numpy(np.ascontiguousarray(M_np[b0:b1])).pin_memory()
+        devC, devM = hostC.to(device), hostM.to(device)
+        per_d = torch.empty(b1 - b0, dtype=torch.complex128, device=device)
+        abs2_d = torch.empty(b1 - b0, dtype=torch.float64, device=device)
+        abs2_h = torch.empty(b1 - b0, dtype=torch.float64).pin_memory()
+        e0, e1 = ev(), ev()
+        h2d, d2h = hostC.numel() * 16 + hostM.numel() * 4, abs2_h.numel() * 8
+        terms_w = float(np.sum(np.prod(M_np[b0:b1].astype(np.float64) + 1.0, axis=1)))
+        walk_launches_per_step = 1
+
+        def step():
+            e0.record(stream)
+            pb.perm_c128_weighted_batched(devC, devM, per=per_d, abs2=abs2_d, stream=stream)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            es = torch.cuda.Event(enable_timing=True)
+            ee = torch.cuda.Event(enable_timing=True)
+            es.record(stream)
+            devC.copy_(hostC, non_blocking=True)
+            devM.copy_(hostM, non_blocking=True)
+            pb.perm_c128_weighted_batched(devC, devM, per=per_d, abs2=abs2_d, stream=stream)
+            abs2_h.copy_(abs2_d, non_blocking=True)
+            ee.record(stream)
+            torch.cuda.synchronize()
+            return {"dev": e0.elapsed_time(e1), "e2e": es.elapsed_time(ee), "walk": e0.elapsed_time(e1),
+                    "result": float(abs2_h[0])}
+
+        units_per_step = B
+        unit = "perms/s"
+        gpu_launches_per_step = 2
+        config = {"workload": "10^4 Boson-sampling output patterns with collisions: 20 photons in the 20 modes of a "
+                              "Haar unitary (seed 2424), weighted Ryser Eq. (4)", "batch": B, "n": n,
+                  "terms_per_step": terms_w * world, "parallelism": f"batch x{world}",
+                  "l2": "inputs 64 MB; compute-bound"}
+        scaling = "weak" if world > 1 else "strong"
     else:
         raise SystemExit(f"unknown config {cfg}")
 
@@ -453,7 +505,15 @@ def run_ours(args):
             out["fp64_peak_frac"] = achieved / nominal
     else:
         # batched / int: report the device time of the batch kernels against the FP64 (or INT) pipe
-        if cfg == "cfg2":
+        if cfg == "cfgw":
+            fl = terms_w * 8 * 20
+            achieved = fl / (dev_ms / K * 1e-3) / 1e12
+            out["roofline"] = {"bound": "alu", "achieved": achieved, "peak": nominal, "unit": "TFLOP/s",
+                               "frac": achieved / nominal, "traffic": ncu_traffic(cfg),
+                               "kernel": "weighted_kernel<20> (FP64 vector pipe)",
+                               "algorithmic": "8n flops per Eq. (4) term x prod_k (m_k+1) terms per pattern",
+                               "peak_measured_probe": peak_meas}
+        elif cfg == "cfg2":
             fl = sum(100000 / world * (1 << (n - 1)) * 8 * n for n in (8, 12, 16, 20))
             achieved = fl / (dev_ms / K * 1e-3) / 1e12
             out["roofline"] = {"bound": "alu", "achieved": achieved, "peak": nominal, "unit": "TFLOP/s",
@@ -489,7 +549,7 @@ def run_reference(args):
     if rank != 0:
         return          # the reference arm runs on rank 0 only
     cfg = args.config
-    unit = "perms/s" if cfg in ("cfg2", "cfg3") else "terms/s"
+    unit = "perms/s" if cfg in ("cfg2", "cfg3", "cfgw") else "terms/s"
     for _ in range(max(0, args.warmup)):
         oracle_rate_cfg(cfg, seconds=1.0)
     rates, samples = [], []
@@ -517,7 +577,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=1)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="cfg5", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
+    ap.add_argument("--config", default="cfg5", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "cfgw"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)

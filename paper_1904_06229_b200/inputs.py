@@ -18,7 +18,7 @@ from __future__ import annotations
 
 import numpy as np
 
-SEEDS = {"cfg1": 16, "cfg2_u": 2000, "cfg2_idx": 3000, "cfg3": 24, "cfg4": 1024, "cfg5": 44}
+SEEDS = {"cfg1": 16, "cfg2_u": 2000, "cfg2_idx": 3000, "cfg3": 24, "cfg4": 1024, "cfg5": 44, "cfgw": 2424}
 
 
 def complex_gaussian(shape, seed: int | np.random.Generator) -> np.ndarray:
@@ -126,3 +126,10 @@ def collision_patterns(n: int, m: int, count: int, seed: int, R: int | None = No
         C[s, :, :len(modes)] = U[:n, modes]
         mult[s, :len(modes)] = counts
     return C, mult
+
+
+def cfgw(count: int = 10_000) -> tuple[np.ndarray, np.ndarray]:
+    """Weighted-Ryser workload (not a BASELINE config): 20 photons into the 20 modes
+    of a Haar unitary, output modes drawn uniformly with replacement -- collision-rich patterns
+    (about 13 distinct modes each).  C (count, 20, 20), mult (count, 20)."""
+    return collision_patterns(20, 20, count, SEEDS["cfgw"])
