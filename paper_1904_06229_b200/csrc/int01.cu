@@ -24,12 +24,46 @@ template <int N>
 struct I01Cfg {
     static constexpr int U = walk_inner_bits(N);
     static constexpr int NT = 128;
+    static constexpr int NP = (N + 3) & ~3;          // column stride (ints): 16-byte aligned columns
 };
 
 __device__ __forceinline__ int lds_i(uint32_t addr) {
     int v;
     asm volatile("ld.volatile.shared.s32 %0, [%1];" : "=r"(v) : "r"(addr));
     return v;
+}
+
+// Four consecutive rows of a column in one 16-byte load (broadcast: every lane reads the same column).
+__device__ __forceinline__ int4 lds_i4(uint32_t addr) {
+    int4 v;
+    asm volatile("ld.volatile.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+    return v;
+}
+
+// g += z * column (z = +-1, or 0/1 when seeding); col = address of row 0 of the column.
+template <int N>
+__device__ __forceinline__ void int_flip(uint32_t col, int z, int (&g)[N]) {
+#pragma unroll
+    for (int i = 0; i < N; i += 4) {
+        const int4 a = lds_i4(col + 4u * (uint32_t)i);
+        g[i] += z * a.x;
+        if (i + 1 < N) g[i + 1] += z * a.y;
+        if (i + 2 < N) g[i + 2] += z * a.z;
+        if (i + 3 < N) g[i + 3] += z * a.w;
+    }
+}
+
+// g += column (PLUS) or g -= column, compile-time sign.
+template <int N, bool PLUS>
+__device__ __forceinline__ void int_flip_static(uint32_t col, int (&g)[N]) {
+#pragma unroll
+    for (int i = 0; i < N; i += 4) {
+        const int4 a = lds_i4(col + 4u * (uint32_t)i);
+        const int v[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+        for (int k = 0; k < 4; k++)
+            if (i + k < N) g[i + k] = PLUS ? g[i + k] + v[k] : g[i + k] - v[k];
+    }
 }
 
 // prod_i g_i mod 2^128.
@@ -54,9 +88,11 @@ __device__ __forceinline__ u128 int_product(const int (&g)[N]) {
         if constexpr (NQ == 1) {
             return (u128)(__int128)q[0];
         } else {
-            // signed 64 x 64 -> 128
-            unsigned long long lo = (unsigned long long)q[0] * (unsigned long long)q[1];
-            unsigned long long hi = (unsigned long long)__mul64hi(q[0], q[1]);
+            // signed 64 x 64 -> 128: unsigned high part minus the two-complement corrections
+            const unsigned long long a = (unsigned long long)q[0], b = (unsigned long long)q[1];
+            unsigned long long lo = a * b;
+            unsigned long long hi = __umul64hi(a, b) - ((unsigned long long)(q[0] >> 63) & b) -
+                                    ((unsigned long long)(q[1] >> 63) & a);
 #pragma unroll
             for (int k = 2; k < NQ; k++) {
                 const unsigned long long yl = (unsigned long long)q[k];
@@ -77,26 +113,17 @@ __device__ __forceinline__ void int_term(const int (&g)[N], u128& acc) {
     if (SIGN > 0) acc += p; else acc -= p;
 }
 
-template <int N>
-__device__ __forceinline__ void int_flip_dyn(uint32_t col, int z, int (&g)[N]) {
-#pragma unroll
-    for (int i = 0; i < N; i++) g[i] += z * lds_i(col + 4 * i);
-}
-
 template <int N, int U, int T>
 struct IntInner {
     static __device__ __forceinline__ void run(uint32_t sc, int (&g)[N], int zmid, u128& acc) {
         if constexpr (T > 0) {
             constexpr int J = ctz_c((unsigned)T);
+            constexpr int NP = I01Cfg<N>::NP;
             if constexpr (J == U - 1) {
-                int_flip_dyn<N>(sc + 4u * (uint32_t)(J * N), zmid, g);
+                int_flip<N>(sc + 4u * (uint32_t)(J * NP), zmid, g);
             } else {
                 constexpr bool PLUS = ((T >> (J + 1)) & 1) == 0;
-#pragma unroll
-                for (int i = 0; i < N; i++) {
-                    const int a = lds_i(sc + 4u * (uint32_t)(J * N + i));
-                    if (PLUS) g[i] += a; else g[i] -= a;
-                }
+                int_flip_static<N, PLUS>(sc + 4u * (uint32_t)(J * NP), g);
             }
         }
         if constexpr (T & 1) int_term<N, +1>(g, acc);
@@ -111,7 +138,7 @@ __device__ __forceinline__ void int_seed(uint32_t sc, uint32_t sbase, uint64_t x
     for (int i = 0; i < N; i++) g[i] = lds_i(sbase + 4 * i);
     for (int j = j0; j < N - 1; j++) {
         const int f = (int)((x >> j) & 1ull);
-        int_flip_dyn<N>(sc + 4u * (uint32_t)(j * N), f, g);
+        int_flip<N>(sc + 4u * (uint32_t)(j * I01Cfg<N>::NP), f, g);
     }
 }
 
@@ -133,7 +160,7 @@ __device__ __forceinline__ void int_chunk(uint32_t sc, uint32_t sbase, uint64_t 
             if (q > 0) {
                 const int j = U + __ffsll((long long)q) - 1;
                 const uint64_t nb = (j + 1 < e) ? ((q >> (j + 1 - U)) & 1ull) : cpar;
-                int_flip_dyn<N>(sc + 4u * (uint32_t)(j * N), nb ? -1 : 1, g);
+                int_flip<N>(sc + 4u * (uint32_t)(j * I01Cfg<N>::NP), nb ? -1 : 1, g);
             }
             const uint64_t nbm = (U < e) ? (q & 1ull) : cpar;
             IntInner<N, U, 0>::run(sc, g, nbm ? -1 : 1, acc);
@@ -146,21 +173,24 @@ template <int N>
 __global__ void __launch_bounds__(I01Cfg<N>::NT) int01_kernel(const uint8_t* __restrict__ A, int e,
                                                               uint64_t chunks, u128* __restrict__ partials,
                                                               int* __restrict__ flag) {
-    __shared__ int s_col[N * N];   // s_col[j*N + i] = 2 a_ij
-    __shared__ int s_base[N];      // a_{i,n} - sum_{j<n} a_ij
+    constexpr int NP = I01Cfg<N>::NP;
+    __shared__ __align__(16) int s_col[N * NP];   // s_col[j*NP + i] = 2 a_ij (rows N..NP-1 zero)
+    __shared__ int s_base[N];                     // a_{i,n} - sum_{j<n} a_ij
     const int64_t m = blockIdx.y;
     const uint8_t* a = A + m * (N * N);
+    for (int k = threadIdx.x; k < N * NP; k += blockDim.x) s_col[k] = 0;
+    __syncthreads();
     for (int k = threadIdx.x; k < N * N; k += blockDim.x) {
         const int v = a[k];
         if (v > 1) atomicOr(flag, 1);
         const int i = k / N, j = k - i * N;
-        s_col[j * N + i] = 2 * (v & 1);
+        s_col[j * NP + i] = 2 * (v & 1);
     }
     __syncthreads();
     for (int i = threadIdx.x; i < N; i += blockDim.x) {
         int s = 0;
-        for (int j = 0; j < N - 1; j++) s += s_col[j * N + i];
-        s_base[i] = s_col[(N - 1) * N + i] / 2 - s / 2;
+        for (int j = 0; j < N - 1; j++) s += s_col[j * NP + i];
+        s_base[i] = s_col[(N - 1) * NP + i] / 2 - s / 2;
     }
     __syncthreads();
     const uint32_t sc = (uint32_t)__cvta_generic_to_shared(s_col);
