@@ -47,6 +47,15 @@ def test_validation_without_gpu():
     assert L.perm_int01(None, 24, 0, None, None, 0, None) == 0                           # B == 0: no-op
     b = ctypes.c_size_t()
     assert L.perm_int01_workspace_bytes(24, 64, ctypes.byref(b)) == 0 and b.value > 16
+    # weighted Ryser (Eq. (4)): order, R and batch validation happen before any device work
+    W = L.perm_c128_weighted_batched
+    assert W(None, None, 33, 4, 1, None, None, None) == 2                                # n > 32
+    assert W(None, None, 0, 4, 1, None, None, None) == 2                                 # n < 1
+    assert W(None, None, 8, 0, 1, None, None, None) == 1                                 # R < 1
+    assert W(None, None, 8, 65, 1, None, None, None) == 1                                # R > 64
+    assert W(None, None, 8, 4, -1, None, None, None) == 1                                # B < 0
+    assert W(None, None, 8, 4, 0, None, None, None) == 0                                 # B == 0: no-op
+    assert W(None, None, 8, 4, 3, None, None, None) == 1                                 # null inputs
 
 
 def test_finalize_ordered_dd():

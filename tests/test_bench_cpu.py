@@ -21,3 +21,19 @@ def test_reference_arm_json():
     assert d["unit"] == "terms/s" and d["value"] > 0
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+
+
+def test_collision_patterns_are_valid_multisets():
+    # host-side input generator for Eq. (4): multiplicities sum to n, columns are U[:n, mode]
+    import numpy as np
+    from paper_1904_06229_b200 import inputs
+    C, M = inputs.collision_patterns(8, 8, 50, 3)
+    assert C.shape == (50, 8, 8) and M.shape == (50, 8)
+    assert np.all(M.sum(axis=1) == 8) and np.all(M >= 0)
+    U = inputs.haar_unitary(8, np.random.default_rng(3))
+    for b in range(50):
+        k = int(np.count_nonzero(M[b]))
+        assert np.all(M[b, :k] > 0) and np.all(M[b, k:] == 0) and np.all(C[b, :, k:] == 0)
+        # each stored column is a column of U's first n rows (unit-norm rows of a unitary restricted)
+        for j in range(k):
+            assert np.min(np.abs(U[:8, :] - C[b, :, j:j + 1]).sum(axis=0)) < 1e-12
