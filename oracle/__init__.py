@@ -61,6 +61,7 @@ def _L():
             "oracle_distribute": [u64, u64, u64, P, P],
             "oracle_gray": [u64],
             "oracle_ryser_weighted_c128": [P, P, i32, i32, P, P],
+            "oracle_ryser_i8": [P, i32, i32, P],
             "oracle_num_threads": [],
         }
         for name, args in sig.items():
@@ -233,3 +234,15 @@ def ryser_weighted(C, mult) -> tuple[QC, float]:
     if _L().oracle_ryser_weighted_c128(_ptr(C), _ptr(m), n, R, _ptr(out), _ptr(a)) != 0:
         raise ValueError("oracle_ryser_weighted_c128 failed")
     return QC(out), float(a[0] + a[1])
+
+
+def ryser_i8(A, parts: int | None = None) -> int:
+    """Eq. (3) in exact integers (mod 2^128, exact for n <= 33) for a matrix with entries in {-1, 0, 1}
+    (the Bernoulli +-1 ensemble of Sec. V)."""
+    A = np.ascontiguousarray(np.asarray(A, dtype=np.int8))
+    if parts is None:
+        parts = max(1, 4 * num_threads())
+    out = np.zeros(2, dtype=np.uint64)
+    if _L().oracle_ryser_i8(_ptr(A), A.shape[0], parts, _ptr(out)) != 0:
+        raise ValueError("oracle_ryser_i8 failed (order or entry outside {-1, 0, 1})")
+    return _u128_to_int(out[0], out[1])

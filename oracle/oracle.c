@@ -25,6 +25,7 @@
  *   oracle_seed_c128      App. A steps 2,5-8: w(r)
  *   oracle_naive_i01 / oracle_ryser_i01   Eq. (1) / Eq. (3) in exact integers
  *   oracle_distribute, oracle_gray        App. A distribute P:1077-1095, Gray unrank P:1097-1106
+ *   oracle_ryser_i8       Eq. (3) in exact integers for entries in {-1,0,1} (Sec. V Bernoulli +-1)
  *   oracle_ryser_weighted_c128  Eq. (4), P:137-158 (repeated columns); pinned against Eq. (3) on the
  *                                expanded matrix, R = 1 (n! prod c_i) and the Boson-sampling
  *                                normalisation with collisions
@@ -208,6 +209,56 @@ int oracle_ryser_i01(const uint8_t* A, int n, int m, uint64_t* out2) {
         uint64_t k0, len;
         oracle_distribute(total, (uint64_t)m, (uint64_t)k, &k0, &len);
         part[k] = ryser_i01_part(A, n, k0, len);
+    }
+    u128 S = 0;
+    for (int k = 0; k < m; k++) S += part[k];
+    free(part);
+    if (n & 1) S = (u128)0 - S;
+    out2[0] = (uint64_t)S;
+    out2[1] = (uint64_t)(S >> 64);
+    return 0;
+}
+
+/* Eq. (3) in exact integers for matrices with entries in {-1, 0, 1} (the Bernoulli +-1 ensemble of
+ * Sec. V, P:846-860, and 0-1 matrices): row sums are small signed integers, products and the signed
+ * sum are taken mod 2^128 -- exact while |per| < 2^127, i.e. n <= 33 since |per| <= n!. */
+static u128 ryser_i8_part(const int8_t* A, int n, uint64_t k0, uint64_t len) {
+    int64_t rs[64];
+    u128 S = 0;
+    uint64_t x = oracle_gray(k0);
+    for (int i = 0; i < n; i++) {
+        rs[i] = 0;
+        for (int j = 0; j < n; j++)
+            if ((x >> j) & 1) rs[i] += A[(size_t)i * n + j];
+    }
+    for (uint64_t r = k0; r < k0 + len; r++) {
+        if (r != k0) {
+            uint64_t xn = oracle_gray(r);
+            int j = __builtin_ctzll(xn ^ x);
+            for (int i = 0; i < n; i++)
+                rs[i] += ((xn >> j) & 1) ? A[(size_t)i * n + j] : -(int64_t)A[(size_t)i * n + j];
+            x = xn;
+        }
+        u128 p = 1;
+        for (int i = 0; i < n; i++) p *= (u128)(int64_t)rs[i];      /* sign-extended, mod 2^128 */
+        if (__builtin_popcountll(x) & 1) S -= p; else S += p;
+    }
+    return S;
+}
+
+int oracle_ryser_i8(const int8_t* A, int n, int m, uint64_t* out2) {
+    if (n < 1 || n > 33) return 1;
+    for (size_t k = 0; k < (size_t)n * n; k++)
+        if (A[k] < -1 || A[k] > 1) return 2;
+    if (m < 1) m = 1;
+    uint64_t total = (uint64_t)1 << n;
+    if ((uint64_t)m > total) m = (int)total;
+    u128* part = (u128*)calloc((size_t)m, sizeof(u128));
+    #pragma omp parallel for schedule(dynamic, 1)
+    for (int k = 0; k < m; k++) {
+        uint64_t k0, len;
+        oracle_distribute(total, (uint64_t)m, (uint64_t)k, &k0, &len);
+        part[k] = ryser_i8_part(A, n, k0, len);
     }
     u128 S = 0;
     for (int k = 0; k < m; k++) S += part[k];

@@ -371,3 +371,38 @@ def test_weighted_boson_sampling_normalization_with_collisions():
             val, _ = oracle.ryser_weighted(U[np.ix_(S, modes)], counts)
             tot += abs(val.value) ** 2 / math.prod(math.factorial(int(c)) for c in counts)
         assert abs(tot - 1.0) < 1e-13
+
+
+# ------------------------------------------------------------------ entries in {-1, 0, 1} (NEXT-2, Sec. V)
+
+def test_i8_brute_force_python():
+    rng = np.random.default_rng(31)
+    for n in range(1, 8):
+        A = rng.integers(-1, 2, size=(n, n)).astype(np.int8)
+        ref = sum(math.prod(int(A[i, p[i]]) for i in range(n)) for p in itertools.permutations(range(n)))
+        assert oracle.ryser_i8(A) == ref
+
+
+def test_i8_against_binary128_complex_oracle():
+    # an independent evaluation: Eq. (3) in binary128 complex arithmetic (exact for these magnitudes)
+    rng = np.random.default_rng(32)
+    for n in (8, 12, 16):
+        A = (2 * rng.integers(0, 2, size=(n, n)) - 1).astype(np.int8)
+        q = oracle.ryser(A.astype(np.complex128))
+        assert oracle.ryser_i8(A) == int(q.re_hi) + int(q.re_lo) and q.im_hi == 0.0
+
+
+def test_i8_sign_identities_and_01_agreement():
+    rng = np.random.default_rng(33)
+    n = 14
+    A = (2 * rng.integers(0, 2, size=(n, n)) - 1).astype(np.int8)
+    p = oracle.ryser_i8(A)
+    assert oracle.ryser_i8(-A) == (-1) ** n * p                        # per(-A) = (-1)^n per(A)
+    B = A.copy()
+    B[3] *= -1
+    assert oracle.ryser_i8(B) == -p                                     # one row negated
+    assert oracle.ryser_i8(np.ones((n, n), np.int8)) == math.factorial(n)
+    Z = rng.integers(0, 2, size=(n, n)).astype(np.uint8)                # 0-1 special case
+    assert oracle.ryser_i8(Z.astype(np.int8)) == oracle.ryser_i01(Z)
+    with pytest.raises(ValueError):
+        oracle.ryser_i8(np.full((3, 3), 2, np.int8))
