@@ -13,6 +13,7 @@ Workloads (BASELINE.json configs; synthetic inputs from paper_1904_06229_b200/in
   cfg1: one 16x16 complex Gaussian (latency-bound).
   cfg2: 10^5 submatrices of an n^2 x n^2 Haar unitary for each n in {8,12,16,20}; batched perms/s.
   cfg3: 64 Bernoulli 0-1 matrices of order 24; exact int128; perms/s.
+  cfgpm: 1024 Bernoulli +-1 matrices of order 24 (Sec. V ensemble); exact; perms/s.
   cfgw: 10^4 Boson-sampling output patterns with collisions (20 photons, 20 modes), weighted Ryser
         Eq. (4) (not a BASELINE config); perms/s.
 
@@ -233,6 +234,16 @@ def oracle_rate_cfg(cfg: str, seconds: float = 12.0) -> dict:
         dt = time.perf_counter() - t0
         return {"value": k / dt, "unit": "perms/s", "cores": cores, "kind": "oracle",
                 "sample": f"Eq. (3) int128 oracle on {k} of the 64 config-3 matrices, {dt:.1f} s"}
+    if cfg == "cfgpm":
+        A = inputs.bernoulli_pm1((1024, 24, 24), inputs.SEEDS["cfgpm"])
+        t0 = time.perf_counter()
+        k = 0
+        while time.perf_counter() - t0 < seconds and k < A.shape[0]:
+            oracle.ryser_i8(A[k])
+            k += 1
+        dt = time.perf_counter() - t0
+        return {"value": k / dt, "unit": "perms/s", "cores": cores, "kind": "oracle",
+                "sample": f"Eq. (3) int128 oracle on the first {k} of the 1024 cfgpm matrices, {dt:.1f} s"}
     if cfg == "cfgw":
         C, M = inputs.cfgw()
         t0 = time.perf_counter()
@@ -369,8 +380,9 @@ def run_ours(args):
         scaling = "weak" if world > 1 else "strong"
         if world > 1:
             units_per_step = count * len(ns)   # every rank does its share of the same global batch
-    elif cfg == "cfg3":
-        A_np = inputs.cfg3()
+    elif cfg in ("cfg3", "cfgpm"):
+        pm1 = cfg == "cfgpm"
+        A_np = inputs.bernoulli_pm1((1024, 24, 24), inputs.SEEDS["cfgpm"]) if pm1 else inputs.cfg3()
         B, n = A_np.shape[0], A_np.shape[1]
         b0, b1 = shard.rank_span(B, world, rank)
         host = torch.from_numpy(np.ascontiguousarray(A_np[b0:b1])).pin_memory()
@@ -381,17 +393,18 @@ def run_ours(args):
         e0, e1 = ev(), ev()
         h2d, d2h = host.numel(), out_host.numel() * 8
         walk_launches_per_step = 1
+        fn = pb.perm_pm1 if pm1 else pb.perm_int01
 
         def step():
             e0.record(stream)
-            pb.perm_int01(dev_in, workspace=ws, out=out, stream=stream, as_int=False)
+            fn(dev_in, workspace=ws, out=out, stream=stream, as_int=False)
             e1.record(stream)
             torch.cuda.synchronize()
             es = torch.cuda.Event(enable_timing=True)
             ee = torch.cuda.Event(enable_timing=True)
             es.record(stream)
             dev_in.copy_(host, non_blocking=True)
-            pb.perm_int01(dev_in, workspace=ws, out=out, stream=stream, as_int=False)
+            fn(dev_in, workspace=ws, out=out, stream=stream, as_int=False)
             out_host.copy_(out, non_blocking=True)
             ee.record(stream)
             torch.cuda.synchronize()
@@ -401,8 +414,10 @@ def run_ours(args):
         units_per_step = B
         unit = "perms/s"
         gpu_launches_per_step = 2 * 2
-        config = {"workload": "64 Bernoulli(1/2) 0-1 matrices of order 24 (seed 24), exact int128 permanents",
-                  "parallelism": f"batch x{world}", "l2": "input 37 KB; compute-bound"}
+        config = {"workload": ("1024 Bernoulli +-1 matrices of order 24 (Sec. V ensemble, seed 2425), exact int128 "
+                               "permanents" if pm1 else
+                               "64 Bernoulli(1/2) 0-1 matrices of order 24 (seed 24), exact int128 permanents"),
+                  "parallelism": f"batch x{world}", "l2": "input 0.6 MB; compute-bound" if pm1 else "input 37 KB; compute-bound"}
         scaling = "weak" if world > 1 else "strong"
     elif cfg == "cfgw":
         C_np, M_np = inputs.cfgw()
@@ -489,7 +504,8 @@ def run_ours(args):
     e2e_val = units_per_step * K / (e2e_ms * 1e-3)
     out = {"metric": METRIC, "value": value, "unit": unit, "n_gpus": world, "steps": K, "warmup": args.warmup,
            "ms_per_step": dev_ms / K, "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
-           "dtype": "f64", "data": "synthetic (seeded generators, paper_1904_06229_b200/inputs.py)",
+           "dtype": "int128" if cfg in ("cfg3", "cfgpm") else "f64",
+           "data": "synthetic (seeded generators, paper_1904_06229_b200/inputs.py)",
            "config": config}
     nominal = fp64_nominal_tflops()
     if roofline_units is not None:
@@ -525,12 +541,13 @@ def run_ours(args):
             # algorithmic integer ops per Gray term: n row-sum adds + (n-1) multiplies + 1 signed add
             n3 = 24
             ops = units_per_step / world * (1 << (n3 - 1)) * 2 * n3
+            kname = "int01_kernel<24, pm1> (INT fma + alu pipes)" if cfg == "cfgpm" else "int01_kernel<24> (INT fma + alu pipes)"
             achieved = ops / (dev_ms / K * 1e-3) / 1e12
             ipeak = int_nominal_tops()
             out["roofline"] = {"bound": "alu", "achieved": achieved, "peak": ipeak, "unit": "Tops/s",
                                "frac": achieved / ipeak, "traffic": ncu_traffic(cfg),
-                               "kernel": "int01_kernel<24> (INT fma + alu pipes)",
-                               "algorithmic": "2n integer ops per Gray term x 2^(n-1) terms x 64 matrices",
+                               "kernel": kname,
+                               "algorithmic": "2n integer ops per Gray term x 2^(n-1) terms x matrices",
                                "peak_note": "derived: 148 SMs x 128 int lanes/clk (issue-bound) x 1965 MHz"}
     out["e2e"] = {"value": e2e_val, "unit": unit, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
     out["gpu_launches"] = gpu_launches_per_step * K
@@ -549,7 +566,7 @@ def run_reference(args):
     if rank != 0:
         return          # the reference arm runs on rank 0 only
     cfg = args.config
-    unit = "perms/s" if cfg in ("cfg2", "cfg3", "cfgw") else "terms/s"
+    unit = "perms/s" if cfg in ("cfg2", "cfg3", "cfgw", "cfgpm") else "terms/s"
     for _ in range(max(0, args.warmup)):
         oracle_rate_cfg(cfg, seconds=1.0)
     rates, samples = [], []
@@ -577,7 +594,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=1)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="cfg5", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "cfgw"])
+    ap.add_argument("--config", default="cfg5", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "cfgw", "cfgpm"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)

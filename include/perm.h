@@ -153,6 +153,14 @@ perm_status_t perm_int01_workspace_bytes(int n, int64_t B, size_t* bytes);
 perm_status_t perm_int01(const uint8_t* A_dev, int n, int64_t B, perm_i128_t* out_dev,
                          void* workspace, size_t workspace_bytes, void* stream);
 
+/* Exact per(A) of B matrices with entries in {-1, 0, 1} -- the Bernoulli +-1 ensemble of Sec. V
+ * -- by the same integer Glynn walk as perm_int01 (|g_i| <= n, so the
+ * same n <= 28 exactness bound).  Same workspace (perm_int01_workspace_bytes), outputs and errors as
+ * perm_int01; PERM_E_NOT01 here means an entry outside {-1, 0, 1}.
+ *   A_dev     device, B*n*n signed bytes, row-major. */
+perm_status_t perm_pm1(const int8_t* A_dev, int n, int64_t B, perm_i128_t* out_dev,
+                       void* workspace, size_t workspace_bytes, void* stream);
+
 /* ------------------------------------------------------------------------------------------
  * Diagnostics.
  * ------------------------------------------------------------------------------------------ */

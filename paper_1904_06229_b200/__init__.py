@@ -13,6 +13,7 @@ Names follow the C ABI:
 * :func:`perm_c128_batched`  -- per and |per|^2 of a batch of small matrices
 * :func:`perm_c128_weighted_batched` -- repeated columns, weighted Ryser Eq. (4)
 * :func:`perm_int01`         -- exact int128 permanents of 0-1 matrices
+* :func:`perm_pm1`           -- exact int128 permanents of matrices with entries in {-1, 0, 1} (Sec. V)
 """
 from __future__ import annotations
 
@@ -109,6 +110,7 @@ def lib() -> ctypes.CDLL:
         "perm_c128_weighted_batched": [P, P, i32, i32, i64, P, P, P],
         "perm_int01_workspace_bytes": [i32, i64, ctypes.POINTER(sz)],
         "perm_int01": [P, i32, i64, P, P, sz, P],
+        "perm_pm1": [P, i32, i64, P, P, sz, P],
         "perm_c128_seed": [P, i32, P, i32, P, P],
         "perm_fp64_probe": [i32, i32, i32, P, P],
     }
@@ -349,6 +351,27 @@ def perm_int01(A, *, workspace=None, out=None, stream=None, as_int: bool = True)
     return vals
 
 
+def perm_pm1(A, *, workspace=None, out=None, stream=None, as_int: bool = True):
+    """Exact per of a (B, n, n) int8 CUDA tensor with entries in {-1, 0, 1} (Bernoulli +-1 ensemble,
+    Sec. V), n <= 28.  Synchronizes.  Returns Python ints (as_int) or the raw (B, 2) int64 {lo, hi}."""
+    torch = _torch()
+    if not (_is_torch(A) and A.is_cuda and A.dtype == torch.int8):
+        raise ValueError("perm_pm1 expects a CUDA int8 tensor (B, n, n)")
+    A = A.contiguous()
+    B, n, n2 = A.shape
+    if n != n2:
+        raise ValueError("matrices must be square")
+    if out is None:
+        out = torch.empty((B, 2), dtype=torch.int64, device=A.device)
+    ws, wsb = _ws_args(workspace)
+    _check(lib().perm_pm1(ctypes.c_void_p(A.data_ptr()), n, B, ctypes.c_void_p(out.data_ptr()), ws, wsb,
+                          _stream_ptr(stream)))
+    if not as_int:
+        return out
+    raw = out.cpu().numpy()
+    return [(int(hi) << 64) + (int(lo) & ((1 << 64) - 1)) for lo, hi in raw]
+
+
 def perm_c128_seed(A, ranks) -> np.ndarray:
     """w(r) (App. A steps 2, 5-8) computed by the device seeding code, for each rank r -> (count, n)."""
     ptr, n, keep = _matrix_ptr(A)
@@ -366,6 +389,6 @@ def perm_fp64_probe(blocks: int, threads: int, iters: int, sink, stream=None):
 
 
 __all__ = ["perm_c128", "perm_c128_range", "perm_c128_finalize", "perm_c128_batched", "perm_c128_weighted_batched",
-           "perm_int01",
+           "perm_int01", "perm_pm1",
            "perm_c128_seed", "perm_fp64_probe", "workspace_bytes", "make_workspace", "int01_workspace_bytes",
            "PermError", "DD", "lib", "header_functions", "last_launches"]

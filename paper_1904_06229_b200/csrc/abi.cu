@@ -446,8 +446,8 @@ perm_status_t perm_int01_workspace_bytes(int n, int64_t B, size_t* bytes) {
     return PERM_OK;
 }
 
-perm_status_t perm_int01(const uint8_t* A_dev, int n, int64_t B, perm_i128_t* out_dev, void* workspace,
-                         size_t workspace_bytes, void* stream) {
+static perm_status_t run_int(const uint8_t* A_dev, bool pm1, int n, int64_t B, perm_i128_t* out_dev, void* workspace,
+                             size_t workspace_bytes, void* stream) {
     g_launches = 0;
     if (B < 0) return PERM_E_ARG;
     if (n < 1 || n > perm::kMaxInt01N) return PERM_E_ORDER;
@@ -469,7 +469,7 @@ perm_status_t perm_int01(const uint8_t* A_dev, int n, int64_t B, perm_i128_t* ou
     for (int64_t b0 = 0; b0 < B && result == PERM_OK; b0 += step) {
         const int64_t nb = (B - b0) < step ? (B - b0) : step;
         int flag = 0, l = 0;
-        cudaError_t e = perm::int01_launch(A_dev + b0 * n * n, n, nb, out_dev + b0, ws, need, s, &flag, &l);
+        cudaError_t e = perm::int01_launch(A_dev + b0 * n * n, n, nb, pm1, out_dev + b0, ws, need, s, &flag, &l);
         launches += (uint32_t)l;
         if (e != cudaSuccess) result = cuda_fail(e, "int01 kernel");
         else if (flag & 1) result = PERM_E_NOT01;
@@ -478,6 +478,16 @@ perm_status_t perm_int01(const uint8_t* A_dev, int n, int64_t B, perm_i128_t* ou
     if (own) cudaFreeAsync(ws, s);
     if (result == PERM_OK) g_launches = launches;
     return result;
+}
+
+perm_status_t perm_int01(const uint8_t* A_dev, int n, int64_t B, perm_i128_t* out_dev, void* workspace,
+                         size_t workspace_bytes, void* stream) {
+    return run_int(A_dev, false, n, B, out_dev, workspace, workspace_bytes, stream);
+}
+
+perm_status_t perm_pm1(const int8_t* A_dev, int n, int64_t B, perm_i128_t* out_dev, void* workspace,
+                       size_t workspace_bytes, void* stream) {
+    return run_int((const uint8_t*)A_dev, true, n, B, out_dev, workspace, workspace_bytes, stream);
 }
 
 perm_status_t perm_c128_seed(const perm_c128_t* A, int n, const uint64_t* ranks, int count, perm_c128_t* w_out,

@@ -169,7 +169,9 @@ __device__ __forceinline__ void int_chunk(uint32_t sc, uint32_t sbase, uint64_t 
 }
 
 // ws layout: [int flag][pad to 16][u128 partials[B][nblk]]
-template <int N>
+// PM1 = false: entries are bytes 0/1 (perm_int01); PM1 = true: signed bytes in {-1, 0, 1} (perm_pm1, the
+// Bernoulli +-1 ensemble of Sec. V).  Either way |g_i| <= n, so the product and exactness bounds hold.
+template <int N, bool PM1>
 __global__ void __launch_bounds__(I01Cfg<N>::NT) int01_kernel(const uint8_t* __restrict__ A, int e,
                                                               uint64_t chunks, u128* __restrict__ partials,
                                                               int* __restrict__ flag) {
@@ -181,10 +183,10 @@ __global__ void __launch_bounds__(I01Cfg<N>::NT) int01_kernel(const uint8_t* __r
     for (int k = threadIdx.x; k < N * NP; k += blockDim.x) s_col[k] = 0;
     __syncthreads();
     for (int k = threadIdx.x; k < N * N; k += blockDim.x) {
-        const int v = a[k];
-        if (v > 1) atomicOr(flag, 1);
+        const int v = PM1 ? (int)(int8_t)a[k] : (int)a[k];
+        if (PM1 ? (v < -1 || v > 1) : (v > 1)) atomicOr(flag, 1);
         const int i = k / N, j = k - i * N;
-        s_col[j * NP + i] = 2 * (v & 1);
+        s_col[j * NP + i] = PM1 ? 2 * (v < -1 ? -1 : (v > 1 ? 1 : v)) : 2 * (v & 1);
     }
     __syncthreads();
     for (int i = threadIdx.x; i < N; i += blockDim.x) {
@@ -265,16 +267,17 @@ size_t int01_workspace_bytes(int n, int64_t B) {
 }
 
 template <int N>
-cudaError_t int01_launch_t(const uint8_t* A, int64_t B, const I01Plan& p, u128* partials, int* flag,
+cudaError_t int01_launch_t(const uint8_t* A, int64_t B, const I01Plan& p, u128* partials, int* flag, bool pm1,
                            cudaStream_t s) {
     dim3 grid((unsigned)p.nblk, (unsigned)B);
-    int01_kernel<N><<<grid, I01Cfg<N>::NT, 0, s>>>(A, p.e, p.chunks, partials, flag);
+    if (pm1) int01_kernel<N, true><<<grid, I01Cfg<N>::NT, 0, s>>>(A, p.e, p.chunks, partials, flag);
+    else     int01_kernel<N, false><<<grid, I01Cfg<N>::NT, 0, s>>>(A, p.e, p.chunks, partials, flag);
     return cudaGetLastError();
 }
 
 #define PERM_R8(M, b) M(b + 1) M(b + 2) M(b + 3) M(b + 4) M(b + 5) M(b + 6) M(b + 7) M(b + 8)
 
-cudaError_t int01_launch(const uint8_t* A, int n, int64_t B, void* out, void* ws, size_t ws_bytes,
+cudaError_t int01_launch(const uint8_t* A, int n, int64_t B, bool pm1, void* out, void* ws, size_t ws_bytes,
                          cudaStream_t s, int* flag_host_status, int* launches) {
     *launches = 0;
     *flag_host_status = 0;
@@ -286,7 +289,7 @@ cudaError_t int01_launch(const uint8_t* A, int n, int64_t B, void* out, void* ws
     cudaError_t err = cudaMemsetAsync(flag, 0, sizeof(int), s);
     if (err != cudaSuccess) return err;
     switch (n) {
-#define PERM_CASE(N) case N: err = int01_launch_t<N>(A, B, p, partials, flag, s); break;
+#define PERM_CASE(N) case N: err = int01_launch_t<N>(A, B, p, partials, flag, pm1, s); break;
         PERM_R8(PERM_CASE, 0) PERM_R8(PERM_CASE, 8) PERM_R8(PERM_CASE, 16)
         PERM_CASE(25) PERM_CASE(26) PERM_CASE(27) PERM_CASE(28)
 #undef PERM_CASE

@@ -117,7 +117,7 @@ cudaError_t weighted_launch(const double2* C, const int32_t* mult, int n, int R,
 
 // int01.cu
 size_t int01_workspace_bytes(int n, int64_t B);
-cudaError_t int01_launch(const uint8_t* A, int n, int64_t B, void* out, void* ws, size_t ws_bytes,
+cudaError_t int01_launch(const uint8_t* A, int n, int64_t B, bool pm1, void* out, void* ws, size_t ws_bytes,
                          cudaStream_t s, int* flag_host_status, int* launches);
 
 }  // namespace perm

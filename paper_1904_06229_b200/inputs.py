@@ -18,7 +18,7 @@ from __future__ import annotations
 
 import numpy as np
 
-SEEDS = {"cfg1": 16, "cfg2_u": 2000, "cfg2_idx": 3000, "cfg3": 24, "cfg4": 1024, "cfg5": 44, "cfgw": 2424}
+SEEDS = {"cfg1": 16, "cfg2_u": 2000, "cfg2_idx": 3000, "cfg3": 24, "cfg4": 1024, "cfg5": 44, "cfgw": 2424, "cfgpm": 2425}
 
 
 def complex_gaussian(shape, seed: int | np.random.Generator) -> np.ndarray:
@@ -133,3 +133,25 @@ def cfgw(count: int = 10_000) -> tuple[np.ndarray, np.ndarray]:
     of a Haar unitary, output modes drawn uniformly with replacement -- collision-rich patterns
     (about 13 distinct modes each).  C (count, 20, 20), mult (count, 20)."""
     return collision_patterns(20, 20, count, SEEDS["cfgw"])
+
+
+# ---------------------------------------------------------------- ensembles of Secs. III-VI (NEXT-2)
+
+def bernoulli_pm1(shape, seed: int) -> np.ndarray:
+    """Bernoulli +-1 entries, Pr(+1) = Pr(-1) = 1/2 (Sec. V), as int8."""
+    rng = np.random.default_rng(seed)
+    return np.ascontiguousarray((2 * rng.integers(0, 2, size=shape) - 1).astype(np.int8))
+
+
+def haar_minors(n: int, a: float, count: int, seed: int) -> np.ndarray:
+    """(count, n, n) submatrices with distinct sorted rows and columns of an m x m Haar unitary,
+    m = round(n^a) (the minors S(n^a, n) of Sec. VI; a = 2 is config 2)."""
+    m = int(round(n ** a))
+    rng = np.random.default_rng(seed)
+    U = haar_unitary(m, rng)
+    rows = np.empty((count, n), dtype=np.int64)
+    cols = np.empty((count, n), dtype=np.int64)
+    for s in range(count):
+        rows[s] = np.sort(rng.choice(m, n, replace=False))
+        cols[s] = np.sort(rng.choice(m, n, replace=False))
+    return gather_submatrices(U, rows, cols)
