@@ -62,6 +62,8 @@ def _L():
             "oracle_gray": [u64],
             "oracle_ryser_weighted_c128": [P, P, i32, i32, P, P],
             "oracle_ryser_i8": [P, i32, i32, P],
+            "oracle_sparse_partition": [P, i32, P, P],
+            "oracle_sparse_c128": [P, i32, P, P],
             "oracle_num_threads": [],
         }
         for name, args in sig.items():
@@ -246,3 +248,25 @@ def ryser_i8(A, parts: int | None = None) -> int:
     if _L().oracle_ryser_i8(_ptr(A), A.shape[0], parts, _ptr(out)) != 0:
         raise ValueError("oracle_ryser_i8 failed (order or entry outside {-1, 0, 1})")
     return _u128_to_int(out[0], out[1])
+
+
+def sparse_partition(A) -> tuple[list[int], int]:
+    """App. B greedypartition: column bit masks S_1..S_d and T."""
+    A = _c128(A)
+    n = A.shape[0]
+    masks = np.zeros(64, dtype=np.uint64)
+    t = np.zeros(1, dtype=np.uint64)
+    d = _L().oracle_sparse_partition(_ptr(A), n, _ptr(masks), _ptr(t))
+    if d < 0:
+        raise ValueError("oracle_sparse_partition failed")
+    return [int(m) for m in masks[:d]], int(t[0])
+
+
+def sparse(A) -> tuple[QC, int]:
+    """App. B sparsepermanent with greedypartition: (per, number of sets enumerated)."""
+    A = _c128(A)
+    out = np.zeros(4, dtype=np.float64)
+    c = np.zeros(2, dtype=np.float64)
+    if _L().oracle_sparse_c128(_ptr(A), A.shape[0], _ptr(out), _ptr(c)) != 0:
+        raise ValueError("oracle_sparse_c128 failed")
+    return QC(out), int(c[0]) + int(c[1])

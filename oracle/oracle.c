@@ -26,6 +26,8 @@
  *   oracle_naive_i01 / oracle_ryser_i01   Eq. (1) / Eq. (3) in exact integers
  *   oracle_distribute, oracle_gray        App. A distribute P:1077-1095, Gray unrank P:1097-1106
  *   oracle_ryser_i8       Eq. (3) in exact integers for entries in {-1,0,1} (Sec. V Bernoulli +-1)
+ *   oracle_sparse_partition / oracle_sparse_c128  App. B greedypartition + sparsepermanent
+ *                                (P:1254-1293), pinned against Eq. (3) and by the enumeration count
  *   oracle_ryser_weighted_c128  Eq. (4), P:137-158 (repeated columns); pinned against Eq. (3) on the
  *                                expanded matrix, R = 1 (n! prod c_i) and the Boson-sampling
  *                                normalisation with collisions
@@ -508,6 +510,107 @@ int oracle_ryser_weighted_c128(const double* C, const int* mult, int n, int R, d
     if (n & 1) S = qc_scale(S, -1);
     put_qc(out4, S);
     if (out2) put_q(out2, Sa);
+    return 0;
+}
+
+/* ---------------- App. B: sparse restricted enumeration ----------------
+ * greedypartition(A, D), literally: b_ij = [a_ij != 0]; delta_i = out-degree of row i;
+ * V = all rows; while V is not empty: k = argmin_{i in V} delta_i (lowest index on ties), S_d = N_k =
+ * {l : b_kl = 1}, V -= {k}, V -= {l in V : N_k and N_l intersect}; T = columns in no S.  Returns d and
+ * fills masks[0..d-1] = S_1..S_d (column bit masks) and *tmask = T.  n <= 64. */
+int oracle_sparse_partition(const double* A, int n, uint64_t* masks, uint64_t* tmask) {
+    if (n < 1 || n > 64) return -1;
+    uint64_t N[64];
+    int deg[64];
+    for (int i = 0; i < n; i++) {
+        N[i] = 0;
+        deg[i] = 0;
+        for (int j = 0; j < n; j++) {
+            const double re = A[2 * ((size_t)i * n + j)], im = A[2 * ((size_t)i * n + j) + 1];
+            if (re != 0.0 || im != 0.0) { N[i] |= (uint64_t)1 << j; deg[i]++; }
+        }
+    }
+    uint64_t V = (n == 64) ? ~(uint64_t)0 : (((uint64_t)1 << n) - 1);
+    uint64_t used = 0;
+    int d = 0;
+    while (V) {
+        int k = -1;
+        for (int i = 0; i < n; i++)
+            if (((V >> i) & 1) && (k < 0 || deg[i] < deg[k])) k = i;
+        masks[d++] = N[k];
+        used |= N[k];
+        V &= ~((uint64_t)1 << k);
+        for (int l = 0; l < n; l++)
+            if (((V >> l) & 1) && (N[k] & N[l])) V &= ~((uint64_t)1 << l);
+    }
+    *tmask = ((n == 64) ? ~(uint64_t)0 : (((uint64_t)1 << n) - 1)) & ~used;
+    return d;
+}
+
+/* sparsepermanent(A, D, p), literally: for every choice of non-empty s_l subset of S_l
+ * (l = 1..d) and every t subset of T, J = s_1 u ... u s_d u t and p += (-1)^{|J|} prod_i sum_{j in J} a_ij;
+ * p *= (-1)^n.  Row sums from the definition for every J, binary128.  The outermost enumeration (the
+ * subsets of T, in index order) is split over OpenMP threads and summed in index order.
+ * out2 = number of sets J enumerated (as a double pair hi, lo). */
+int oracle_sparse_c128(const double* A, int n, double* out4, double* out_count) {
+    if (n < 1 || n > 40) return 1;
+    uint64_t S[64], T;
+    const int d = oracle_sparse_partition(A, n, S, &T);
+    for (int i = 0; i < n; i++) {                    /* a zero row makes every product zero */
+        int nz = 0;
+        for (int j = 0; j < n; j++) nz |= A[2 * ((size_t)i * n + j)] != 0.0 || A[2 * ((size_t)i * n + j) + 1] != 0.0;
+        if (!nz) { qc z = { 0, 0 }; put_qc(out4, z); if (out_count) put_q(out_count, 0); return 0; }
+    }
+    int tcols[64], nt = 0;
+    for (int j = 0; j < n; j++) if ((T >> j) & 1) tcols[nt++] = j;
+    const uint64_t ntsub = (uint64_t)1 << nt;
+    const int parts = 256;
+    qc* part = (qc*)calloc(parts, sizeof(qc));
+    quad* cnt = (quad*)calloc(parts, sizeof(quad));
+    #pragma omp parallel for schedule(dynamic, 1)
+    for (int pi = 0; pi < parts; pi++) {
+        uint64_t t0, tl;
+        oracle_distribute(ntsub, parts, (uint64_t)pi, &t0, &tl);
+        qc acc = { 0, 0 };
+        quad c = 0;
+        for (uint64_t tb = t0; tb < t0 + tl; tb++) {
+            uint64_t tsel = 0;
+            for (int q = 0; q < nt; q++) if ((tb >> q) & 1) tsel |= (uint64_t)1 << tcols[q];
+            /* odometer over the non-empty subsets s_l of S_l: s_l runs through the sub-masks of S_l */
+            uint64_t s[64];
+            for (int l = 0; l < d; l++) s[l] = S[l] & (~S[l] + 1);   /* lowest non-empty sub-mask */
+            if (d == 0) s[0] = 0;
+            for (;;) {
+                uint64_t J = tsel;
+                for (int l = 0; l < d; l++) J |= s[l];
+                qc p = { 1, 0 };
+                for (int i = 0; i < n; i++) {
+                    qc rs = { 0, 0 };
+                    for (int j = 0; j < n; j++) if ((J >> j) & 1) rs = qc_add(rs, entry(A, n, i, j));
+                    p = qc_mul(p, rs);
+                }
+                if (__builtin_popcountll(J) & 1) acc = qc_sub(acc, p); else acc = qc_add(acc, p);
+                c += 1;
+                int l = 0;                         /* next combination: sub-mask successor, carry */
+                for (; l < d; l++) {
+                    s[l] = (s[l] - S[l]) & S[l];   /* next sub-mask of S[l] in increasing order */
+                    if (s[l] != 0) break;
+                    s[l] = S[l] & (~S[l] + 1);
+                }
+                if (l == d) break;
+            }
+        }
+        part[pi] = acc;
+        cnt[pi] = c;
+    }
+    qc P = { 0, 0 };
+    quad C = 0;
+    for (int pi = 0; pi < parts; pi++) { P = qc_add(P, part[pi]); C += cnt[pi]; }
+    free(part);
+    free(cnt);
+    if (n & 1) P = qc_scale(P, -1);
+    put_qc(out4, P);
+    if (out_count) put_q(out_count, C);
     return 0;
 }
 

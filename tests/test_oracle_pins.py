@@ -406,3 +406,58 @@ def test_i8_sign_identities_and_01_agreement():
     assert oracle.ryser_i8(Z.astype(np.int8)) == oracle.ryser_i01(Z)
     with pytest.raises(ValueError):
         oracle.ryser_i8(np.full((3, 3), 2, np.int8))
+
+
+# ------------------------------------------------------------------ App. B sparse enumeration (NEXT-3)
+
+def _sparse_matrix(n, density, seed, complex_=True):
+    rng = np.random.default_rng(seed)
+    M = (rng.random((n, n)) < density).astype(float)
+    M[np.arange(n), rng.permutation(n)] = 1.0                   # no zero rows / columns, per != 0 generically
+    if complex_:
+        M = M * (rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n)))
+    return M
+
+
+def _partition_ok(A, S, T):
+    n = A.shape[0]
+    supp = [sum(1 << j for j in range(n) if A[i, j] != 0) for i in range(n)]
+    used = 0
+    for s in S:
+        assert s in supp and (used & s) == 0                        # a row's support, pairwise disjoint
+        used |= s
+    assert T == ((1 << n) - 1) & ~used
+
+
+@pytest.mark.parametrize("n,density,seed", [(6, 0.3, 1), (10, 0.2, 2), (14, 0.15, 3), (16, 0.1, 4), (12, 0.5, 5)])
+def test_sparse_matches_eq3_and_counts(n, density, seed):
+    # App. B restricts Eq. (3) to sets J meeting every S_l; every skipped J leaves some row sum exactly 0,
+    # so the restricted sum equals Eq. (3)/(1).  The enumeration count is 2^|T| prod (2^|S_l| - 1).
+    A = _sparse_matrix(n, density, seed)
+    S, T = oracle.sparse_partition(A)
+    _partition_ok(A, S, T)
+    val, cnt = oracle.sparse(A)
+    ref = oracle.naive(A).value if n <= 9 else oracle.ryser(A).value
+    scale = max(abs(ref), 1e-30)
+    assert abs(val.value - ref) <= 1e-25 * max(scale, float(np.prod(np.abs(A).sum(axis=1))))
+    assert cnt == 2 ** bin(T).count("1") * math.prod(2 ** bin(s).count("1") - 1 for s in S)
+    assert cnt <= 2 ** n
+
+
+def test_sparse_structured_closed_forms():
+    # permutation matrix -> 1; tridiagonal all-ones -> Fibonacci F_{n+1}; zero row -> 0;
+    # diagonal -> product of the diagonal; block diagonal -> product of the blocks
+    n = 12
+    P = np.eye(n)[np.random.default_rng(7).permutation(n)]
+    assert oracle.sparse(P)[0].value == 1.0
+    assert oracle.sparse(pins.tridiagonal_ones(n).astype(float))[0].value == pins.fibonacci(n + 1)
+    Z = _sparse_matrix(8, 0.3, 9)
+    Z[3] = 0
+    assert oracle.sparse(Z)[0].value == 0.0
+    d = np.arange(1, n + 1) * (0.5 + 0.25j)
+    assert abs(oracle.sparse(np.diag(d))[0].value - np.prod(d)) <= 1e-14 * abs(np.prod(d))
+    B1, B2 = _sparse_matrix(5, 0.5, 10), _sparse_matrix(6, 0.4, 11)
+    M = np.zeros((11, 11), complex)
+    M[:5, :5], M[5:, 5:] = B1, B2
+    ref = oracle.naive(B1).value * oracle.naive(B2).value
+    assert abs(oracle.sparse(M)[0].value - ref) <= 1e-13 * abs(ref)
