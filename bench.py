@@ -13,6 +13,7 @@ Workloads (BASELINE.json configs; synthetic inputs from paper_1904_06229_b200/in
   cfg1: one 16x16 complex Gaussian (latency-bound).
   cfg2: 10^5 submatrices of an n^2 x n^2 Haar unitary for each n in {8,12,16,20}; batched perms/s.
   cfg3: 64 Bernoulli 0-1 matrices of order 24; exact int128; perms/s.
+  cfgsp: one sparse 48x48 complex matrix (4% + a matching), App. B restricted enumeration (NEXT-3); sets/s.
   cfgpm: 1024 Bernoulli +-1 matrices of order 24 (Sec. V ensemble); exact; perms/s.
   cfgw: 10^4 Boson-sampling output patterns with collisions (20 photons, 20 modes), weighted Ryser
         Eq. (4) (not a BASELINE config); perms/s.
@@ -234,6 +235,15 @@ def oracle_rate_cfg(cfg: str, seconds: float = 12.0) -> dict:
         dt = time.perf_counter() - t0
         return {"value": k / dt, "unit": "perms/s", "cores": cores, "kind": "oracle",
                 "sample": f"Eq. (3) int128 oracle on {k} of the 64 config-3 matrices, {dt:.1f} s"}
+    if cfg == "cfgsp":
+        A = inputs.cfgsp()
+        A20 = inputs.sparse_gaussian(24, 0.04 * 48 / 24, inputs.SEEDS["cfgsp"])
+        t0 = time.perf_counter()
+        _, cnt = oracle.sparse(A20)
+        dt = time.perf_counter() - t0
+        return {"value": cnt / dt, "unit": "terms/s", "cores": cores, "kind": "oracle",
+                "sample": f"App. B binary128 oracle (sparsepermanent) on a 24x24 matrix of the same recipe "
+                          f"({cnt} restricted sets in {dt:.1f} s; the 48x48 instance is out of its reach)"}
     if cfg == "cfgpm":
         A = inputs.bernoulli_pm1((1024, 24, 24), inputs.SEEDS["cfgpm"])
         t0 = time.perf_counter()
@@ -419,6 +429,38 @@ def run_ours(args):
                                "64 Bernoulli(1/2) 0-1 matrices of order 24 (seed 24), exact int128 permanents"),
                   "parallelism": f"batch x{world}", "l2": "input 0.6 MB; compute-bound" if pm1 else "input 37 KB; compute-bound"}
         scaling = "weak" if world > 1 else "strong"
+    elif cfg == "cfgsp":
+        A_np = inputs.cfgsp()
+        n = A_np.shape[0]
+        plan = pb.perm_sparse_plan(A_np)
+        A_pin = torch.from_numpy(A_np).pin_memory()
+        A_dev = A_pin.to(device)
+        h2d, d2h = A_np.nbytes, 16
+        walk_launches_per_step = 1
+        sets = plan["sets"]
+
+        def step():
+            es, ee = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            es.record(stream)
+            val = pb.perm_c128_sparse(A_dev, stream=stream)      # synchronizes
+            ee.record(stream)
+            torch.cuda.synchronize()
+            e2s, e2e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e2s.record(stream)
+            val = pb.perm_c128_sparse(A_pin, stream=stream)      # host input: H2D inside the call
+            e2e.record(stream)
+            torch.cuda.synchronize()
+            return {"dev": es.elapsed_time(ee), "e2e": e2s.elapsed_time(e2e), "walk": es.elapsed_time(ee),
+                    "result": val}
+
+        units_per_step = sets
+        unit = "terms/s"
+        gpu_launches_per_step = 2 * 2
+        config = {"workload": "one sparse 48x48 complex matrix (density 4% + a perfect matching, seed 4848): per(A) "
+                              "by App. B restricted enumeration", "n": n, "terms_per_step": sets,
+                  "dense_terms": float(2 ** (n - 1)), "partition": {"d": len(plan["S"]), "T": plan["nt"]},
+                  "parallelism": "sets x1", "l2": "input 37 KB; compute-bound"}
+        scaling = "strong"
     elif cfg == "cfgw":
         C_np, M_np = inputs.cfgw()
         B, n, R = C_np.shape
@@ -521,7 +563,15 @@ def run_ours(args):
             out["fp64_peak_frac"] = achieved / nominal
     else:
         # batched / int: report the device time of the batch kernels against the FP64 (or INT) pipe
-        if cfg == "cfgw":
+        if cfg == "cfgsp":
+            fl = sets * 8 * n
+            achieved = fl / (dev_ms / K * 1e-3) / 1e12
+            out["roofline"] = {"bound": "alu", "achieved": achieved, "peak": nominal, "unit": "TFLOP/s",
+                               "frac": achieved / nominal, "traffic": ncu_traffic(cfg),
+                               "kernel": "sparse_kernel<48> (FP64 vector pipe)",
+                               "algorithmic": "8n flops per restricted set J x 2^|T| prod (2^|S_l| - 1) sets",
+                               "peak_measured_probe": peak_meas}
+        elif cfg == "cfgw":
             fl = terms_w * 8 * 20
             achieved = fl / (dev_ms / K * 1e-3) / 1e12
             out["roofline"] = {"bound": "alu", "achieved": achieved, "peak": nominal, "unit": "TFLOP/s",
@@ -594,7 +644,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=1)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="cfg5", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "cfgw", "cfgpm"])
+    ap.add_argument("--config", default="cfg5", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "cfgw", "cfgpm", "cfgsp"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)

@@ -116,6 +116,35 @@ perm_status_t perm_c128_batched(const perm_c128_t* A_dev, int n, int64_t B, perm
                                 double* abs2_dev, void* stream);
 
 /* ------------------------------------------------------------------------------------------
+ * Sparse matrices: restricted enumeration (App. B; Sec. II-D; NEXT-3).
+ * ------------------------------------------------------------------------------------------ */
+
+/* The column partition D = {S_1, ..., S_d, T} of greedypartition (repeatedly take the
+ * remaining row k of least out-degree, the lowest index on ties; S = the columns where row k is
+ * nonzero; drop the remaining rows whose supports meet S), and the enumeration size
+ * sets = 2^{|T|} prod_l (2^{|S_l|} - 1). */
+typedef struct {
+    uint32_t d;          /* number of S sets */
+    uint32_t nt;         /* |T| */
+    uint64_t tmask;      /* columns of T (bit j = column j) */
+    uint64_t smask[64];  /* columns of S_1 .. S_d */
+    double sets;         /* sets J enumerated (0 when a zero row or column makes per = 0) */
+    int32_t chunk_log2;  /* T-walk chunk length used by perm_c128_sparse (-1: not launched) */
+} perm_sparse_info_t;
+
+/* Host only: the partition and enumeration size for A (host, row-major n x n, 1 <= n <= 64).
+ * Errors: PERM_E_ARG (NULL), PERM_E_ORDER, PERM_E_NONFINITE. */
+perm_status_t perm_sparse_plan(const perm_c128_t* A_host, int n, perm_sparse_info_t* info);
+
+/* per(A) by sparsepermanent over the partition of perm_sparse_plan: every set J that
+ * meets each S_l, t-part walked in Gray order on the GPU, signed sum in double-double, (-1)^n applied.
+ * Exactly Eq. (3) (every skipped J has a zero row sum).  A is host or device (row-major), 1 <= n <= 48;
+ * out_host host; info optional; scratch is allocated stream-ordered.  Synchronizes `stream`.
+ * Errors: PERM_E_ARG, PERM_E_ORDER, PERM_E_NONFINITE, PERM_E_CUDA. */
+perm_status_t perm_c128_sparse(const perm_c128_t* A, int n, perm_c128_t* out_host, perm_sparse_info_t* info,
+                               void* stream);
+
+/* ------------------------------------------------------------------------------------------
  * Repeated columns: the weighted Ryser formula, Eq. (4).
  * ------------------------------------------------------------------------------------------ */
 

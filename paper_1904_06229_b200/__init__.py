@@ -14,6 +14,7 @@ Names follow the C ABI:
 * :func:`perm_c128_weighted_batched` -- repeated columns, weighted Ryser Eq. (4)
 * :func:`perm_int01`         -- exact int128 permanents of 0-1 matrices
 * :func:`perm_pm1`           -- exact int128 permanents of matrices with entries in {-1, 0, 1} (Sec. V)
+* :func:`perm_c128_sparse`   -- sparse matrices, App. B restricted enumeration
 """
 from __future__ import annotations
 
@@ -56,6 +57,16 @@ class stats_t(ctypes.Structure):
     _fields_ = [("terms", ctypes.c_uint64), ("chunk_log2", ctypes.c_uint32), ("threads", ctypes.c_uint32),
                 ("blocks", ctypes.c_uint32), ("launches", ctypes.c_uint32),
                 ("ev_walk_begin", ctypes.c_void_p), ("ev_walk_end", ctypes.c_void_p)]
+
+
+class sparse_info_t(ctypes.Structure):
+    _fields_ = [("d", ctypes.c_uint32), ("nt", ctypes.c_uint32), ("tmask", ctypes.c_uint64),
+                ("smask", ctypes.c_uint64 * 64), ("sets", ctypes.c_double), ("chunk_log2", ctypes.c_int32)]
+
+
+def _sparse_info(info: sparse_info_t) -> dict:
+    return {"S": [int(info.smask[l]) for l in range(info.d)], "T": int(info.tmask), "nt": int(info.nt),
+            "sets": float(info.sets), "chunk_log2": int(info.chunk_log2)}
 
 
 def _make_stats(events):
@@ -108,6 +119,8 @@ def lib() -> ctypes.CDLL:
         "perm_c128_finalize": [P, i32, i32, P, P],
         "perm_c128_batched": [P, i32, i64, P, P, P],
         "perm_c128_weighted_batched": [P, P, i32, i32, i64, P, P, P],
+        "perm_sparse_plan": [P, i32, P],
+        "perm_c128_sparse": [P, i32, P, P, P],
         "perm_int01_workspace_bytes": [i32, i64, ctypes.POINTER(sz)],
         "perm_int01": [P, i32, i64, P, P, sz, P],
         "perm_pm1": [P, i32, i64, P, P, sz, P],
@@ -230,6 +243,26 @@ def perm_c128(A, *, workspace=None, stream=None, out=None, return_dd: bool = Fal
         extra.append({"terms": st.terms, "chunk_log2": st.chunk_log2, "threads": st.threads,
                       "blocks": st.blocks, "launches": st.launches})
     return (val, *extra) if extra else val
+
+
+def perm_sparse_plan(A) -> dict:
+    """App. B greedypartition of a host matrix: {"S": column masks, "T": mask, "sets": ...}."""
+    A = np.ascontiguousarray(np.asarray(A, dtype=np.complex128))
+    info = sparse_info_t()
+    _check(lib().perm_sparse_plan(A.ctypes.data_as(ctypes.c_void_p), int(A.shape[0]), ctypes.byref(info)))
+    return _sparse_info(info)
+
+
+def perm_c128_sparse(A, *, stream=None, info: bool = False):
+    """per(A) by App. B sparsepermanent on the GPU, 1 <= n <= 48.  Synchronizes.
+    Returns a complex (and the partition / enumeration info if asked)."""
+    ptr, n, keep = _matrix_ptr(A)
+    res = c128()
+    inf = sparse_info_t()
+    _check(lib().perm_c128_sparse(ptr, n, ctypes.byref(res), ctypes.byref(inf), _stream_ptr(stream)))
+    del keep
+    val = complex(res.re, res.im)
+    return (val, _sparse_info(inf)) if info else val
 
 
 def perm_c128_range(A, k_begin: int, k_end: int, *, workspace=None, stream=None, out=None, stats: bool = False,
@@ -389,6 +422,6 @@ def perm_fp64_probe(blocks: int, threads: int, iters: int, sink, stream=None):
 
 
 __all__ = ["perm_c128", "perm_c128_range", "perm_c128_finalize", "perm_c128_batched", "perm_c128_weighted_batched",
-           "perm_int01", "perm_pm1",
+           "perm_int01", "perm_pm1", "perm_c128_sparse", "perm_sparse_plan",
            "perm_c128_seed", "perm_fp64_probe", "workspace_bytes", "make_workspace", "int01_workspace_bytes",
            "PermError", "DD", "lib", "header_functions", "last_launches"]

@@ -29,7 +29,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
                 f"-I{CSRC}", f"-I{os.path.join(ROOT, 'include')}", "-Xptxas", "-v"]
 
-HEADERS = ["common.cuh", "internal.h", "walk.cuh"]
+HEADERS = ["common.cuh", "internal.h", "walk.cuh", "sparse.cuh"]
 
 
 def units():
@@ -38,6 +38,8 @@ def units():
          ("weighted.o", "weighted.cu", [])]
     for p in range(8):
         u.append((f"walk_inst_{p}.o", "walk_inst.cu", [f"-DPERM_PART={p}"]))
+    for p in range(6):
+        u.append((f"sparse_inst_{p}.o", "sparse_inst.cu", [f"-DPERM_PART={p}"]))
     return u
 
 

@@ -423,6 +423,151 @@ perm_status_t perm_c128_batched(const perm_c128_t* A_dev, int n, int64_t B, perm
     return PERM_OK;
 }
 
+// greedypartition (App. B) on the host.  Returns false if A has a zero row or column.
+static bool sparse_partition(const perm_c128_t* A, int n, perm_sparse_info_t& I) {
+    uint64_t N[64];
+    int deg[64];
+    uint64_t colany = 0;
+    bool zero_row = false;
+    for (int i = 0; i < n; i++) {
+        N[i] = 0;
+        deg[i] = 0;
+        for (int j = 0; j < n; j++) {
+            const perm_c128_t a = A[(size_t)i * n + j];
+            if (a.re != 0.0 || a.im != 0.0) { N[i] |= 1ull << j; deg[i]++; }
+        }
+        colany |= N[i];
+        zero_row |= N[i] == 0;
+    }
+    const uint64_t all = n == 64 ? ~0ull : ((1ull << n) - 1ull);
+    uint64_t V = all, used = 0;
+    I.d = 0;
+    while (V) {
+        int k = -1;
+        for (int i = 0; i < n; i++)
+            if (((V >> i) & 1ull) && (k < 0 || deg[i] < deg[k])) k = i;
+        I.smask[I.d++] = N[k];
+        used |= N[k];
+        V &= ~(1ull << k);
+        for (int l = 0; l < n; l++)
+            if (((V >> l) & 1ull) && (N[k] & N[l])) V &= ~(1ull << l);
+    }
+    I.tmask = all & ~used;
+    I.nt = (uint32_t)__builtin_popcountll(I.tmask);
+    double sets = std::ldexp(1.0, (int)I.nt);
+    for (uint32_t l = 0; l < I.d; l++) sets *= std::ldexp(1.0, __builtin_popcountll(I.smask[l])) - 1.0;
+    const bool zero = zero_row || colany != all;
+    I.sets = zero ? 0.0 : sets;
+    I.chunk_log2 = -1;
+    return !zero;
+}
+
+perm_status_t perm_sparse_plan(const perm_c128_t* A_host, int n, perm_sparse_info_t* info) {
+    if (!A_host || !info) return PERM_E_ARG;
+    if (n < 1 || n > 64) return PERM_E_ORDER;
+    for (size_t k = 0; k < (size_t)n * n; k++)
+        if (!std::isfinite(A_host[k].re) || !std::isfinite(A_host[k].im)) return PERM_E_NONFINITE;
+    memset(info, 0, sizeof(*info));
+    sparse_partition(A_host, n, *info);
+    return PERM_OK;
+}
+
+perm_status_t perm_c128_sparse(const perm_c128_t* A, int n, perm_c128_t* out_host, perm_sparse_info_t* info,
+                               void* stream) {
+    g_launches = 0;
+    if (!A || !out_host) return PERM_E_ARG;
+    if (n < 1 || n > perm::kMaxSparseN) return PERM_E_ORDER;
+    cudaStream_t s = (cudaStream_t)stream;
+    const bool a_dev = is_device_ptr(A);
+    std::vector<perm_c128_t> host;
+    perm_status_t st = load_and_check(A, n, a_dev, s, host);
+    if (st != PERM_OK) return st;
+    const perm_c128_t* Ah = a_dev ? host.data() : A;
+    perm_sparse_info_t I;
+    memset(&I, 0, sizeof(I));
+    if (!sparse_partition(Ah, n, I)) {                    // a zero row or column: per = 0
+        out_host->re = 0.0;
+        out_host->im = 0.0;
+        if (info) *info = I;
+        return PERM_OK;
+    }
+    perm::SparseLaunch L;
+    memset(&L, 0, sizeof(L));
+    L.n = n;
+    L.d = (int)I.d;
+    L.nt = (int)I.nt;
+    int slot = 0;
+    for (int j = 0; j < n; j++)
+        if ((I.tmask >> j) & 1ull) L.col[slot++] = j;
+    uint64_t outer = 1;
+    for (int l = 0; l < L.d; l++) {
+        L.soff[l] = slot;
+        L.ssz[l] = __builtin_popcountll(I.smask[l]);
+        for (int j = 0; j < n; j++)
+            if ((I.smask[l] >> j) & 1ull) L.col[slot++] = j;
+        outer *= (1ull << L.ssz[l]) - 1ull;
+    }
+    L.outer = outer;
+    int dev = 0, sms = 0, bps = 0;
+    PERM_CUDA(cudaGetDevice(&dev), "cudaGetDevice");
+    PERM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "cudaDeviceGetAttribute");
+    PERM_CUDA(perm::sparse_occupancy(n, &bps), "sparse occupancy");
+    if (bps < 1) bps = 1;
+    const uint64_t threads = (uint64_t)sms * bps * perm::walk_block_threads(n);
+    // T-walk chunk length: at least ~128 items per thread, at least the unrolled block, at most |T|
+    const int U = perm::walk_inner_bits(n);
+    int e = 0;
+    if (L.nt >= U && U >= 1) {
+        const double per_thread = I.sets / ((double)threads * 128.0);
+        e = per_thread >= 2.0 ? (int)std::floor(std::log2(per_thread)) : 0;
+        if (e > L.nt) e = L.nt;
+        if (e > 30) e = 30;
+        if (e < U) e = U;
+    }
+    L.e = e;
+    L.chunks = 1ull << (L.nt - e);
+    const uint64_t items = L.outer * L.chunks;
+    const uint64_t bthreads = (uint64_t)perm::walk_block_threads(n);
+    uint64_t grid = (items + bthreads - 1) / bthreads;
+    if (grid > (uint64_t)sms * bps) grid = (uint64_t)sms * bps;
+    L.grid = (int)grid;
+    L.stream = s;
+    I.chunk_log2 = e;
+    char* ws = nullptr;
+    const size_t part_bytes = (size_t)L.grid * sizeof(ddc);
+    const size_t total = part_bytes + sizeof(ddc) + (a_dev ? 0 : (size_t)n * n * sizeof(double2));
+    PERM_CUDA(cudaMallocAsync((void**)&ws, total, s), "cudaMallocAsync(sparse workspace)");
+    perm_status_t result = PERM_OK;
+    do {
+        const double2* A_dev = (const double2*)A;
+        if (!a_dev) {
+            A_dev = (const double2*)(ws + part_bytes + sizeof(ddc));
+            cudaError_t e2 = cudaMemcpyAsync((void*)A_dev, A, (size_t)n * n * sizeof(double2), cudaMemcpyHostToDevice, s);
+            if (e2 != cudaSuccess) { result = cuda_fail(e2, "cudaMemcpyAsync(A H2D)"); break; }
+        }
+        L.A_dev = A_dev;
+        L.partials = (ddc*)ws;
+        cudaError_t e2 = perm::sparse_launch(L);
+        if (e2 != cudaSuccess) { result = cuda_fail(e2, "sparse kernel launch"); break; }
+        ddc* res = (ddc*)(ws + part_bytes);
+        e2 = perm::reduce_launch(L.partials, L.grid, 0, res, nullptr, s);
+        if (e2 != cudaSuccess) { result = cuda_fail(e2, "reduce kernel launch"); break; }
+        ddc r;
+        e2 = cudaMemcpyAsync(&r, res, sizeof(ddc), cudaMemcpyDeviceToHost, s);
+        if (e2 == cudaSuccess) e2 = cudaFreeAsync(ws, s);
+        ws = nullptr;
+        if (e2 == cudaSuccess) e2 = cudaStreamSynchronize(s);
+        if (e2 != cudaSuccess) { result = cuda_fail(e2, "sparse result"); break; }
+        const double f = (n & 1) ? -1.0 : 1.0;             // (-1)^n
+        out_host->re = (r.re.hi + r.re.lo) * f;
+        out_host->im = (r.im.hi + r.im.lo) * f;
+        g_launches = 2;
+    } while (0);
+    if (ws) cudaFreeAsync(ws, s);
+    if (info) *info = I;
+    return result;
+}
+
 perm_status_t perm_c128_weighted_batched(const perm_c128_t* C_dev, const int32_t* mult_dev, int n, int R,
                                          int64_t B, perm_c128_t* per_dev, double* abs2_dev, void* stream) {
     g_launches = 0;

@@ -110,6 +110,25 @@ cudaError_t fp64_probe_launch(int blocks, int threads, int iters, double* sink, 
 cudaError_t batched_launch(const double2* A, int n, int64_t B, double2* per, double* abs2, cudaStream_t s,
                            int* launches);
 
+// sparse.cuh / sparse_inst.cu (App. B restricted enumeration), n <= kMaxSparseN
+constexpr int kMaxSparseN = 48;
+constexpr int kSparseMaxD = 64;
+struct SparseLaunch {
+    const double2* A_dev;   // device, row-major n x n
+    ddc* partials;          // device, grid entries
+    uint64_t outer;         // prod_l (2^{|S_l|} - 1)
+    uint64_t chunks;        // T-walk chunks per outer combination
+    int e, nt, d, n, grid;
+    int col[64];            // permuted column order: T columns, then S_1, S_2, ...
+    int soff[kSparseMaxD];  // first slot of S_l
+    int ssz[kSparseMaxD];   // |S_l|
+    cudaStream_t stream;
+};
+template <int N> cudaError_t sparse_launch_t(const SparseLaunch& L);
+template <int N> cudaError_t sparse_occupancy_t(int* blocks_per_sm);
+cudaError_t sparse_launch(const SparseLaunch& L);
+cudaError_t sparse_occupancy(int n, int* blocks_per_sm);
+
 // weighted.cu
 constexpr int kMaxWeightedR = 64;
 cudaError_t weighted_launch(const double2* C, const int32_t* mult, int n, int R, int64_t B, double2* per,

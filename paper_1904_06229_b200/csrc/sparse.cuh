@@ -1,0 +1,141 @@
+// sparse.cuh -- restricted enumeration for sparse matrices (App. B,
+// sparsepermanent P:1254-1266 with greedypartition P:1275-1293, Sec. II-D).
+//
+// With the column partition D = {S_1, ..., S_d, T} (S_l = the column support of a row, pairwise disjoint),
+// every set J of Eq. (3) that misses some S_l leaves that row's sum exactly 0, so
+//     per(A) = (-1)^n sum_{s_l subset S_l, s_l != {}} sum_{t subset T} (-1)^{|J|} prod_i sum_{j in J} a_ij,
+//     J = s_1 u ... u s_d u t,
+// over 2^|T| prod_l (2^|S_l| - 1) sets instead of 2^n.  Here the t-part is walked in Gray order with the
+// machinery of walk.cuh: an item is (outer combination o, aligned chunk c of 2^e ranks of the T walk);
+// the lanes of a warp take consecutive items, so they share o and walk aligned chunks of the same T
+// columns in lock-step (warp-uniform column operands).  Each item seeds its row sums explicitly:
+//     w = sum_l sum_{j in s_l(o)} a_{.j} + sum_{q in gray(c 2^e)} a_{.,T_q},
+// and the walk accumulates sum_r (-1)^{r+1} prod w (walk_seeded); with |J| = |s| + |gray r| and
+// |gray r| = r (mod 2) the item's contribution is -(-1)^{|s|} times that.  Partials: dd per thread ->
+// warp -> block -> fixed-order reduction (reduce.cu) with the final factor (-1)^n.
+#pragma once
+#include "walk.cuh"
+
+namespace perm {
+
+struct SparseParams {   // kernel-parameter copy of SparseLaunch
+    const double2* A;             // device, row-major n x n
+    ddc* partials;                // [gridDim.x]
+    uint64_t outer;               // prod_l (2^{|S_l|} - 1)
+    uint64_t chunks;              // 2^{nt - e} T-walk chunks per outer combination
+    int32_t e;                    // log2 chunk length (0: single terms)
+    int32_t nt;                   // |T|
+    int32_t d;                    // number of S sets
+    int32_t col[64];              // permuted column order: T columns, then S_1, S_2, ...
+    int32_t soff[kSparseMaxD];    // slot of S_l's first column (in the permuted order)
+    int32_t ssz[kSparseMaxD];     // |S_l|
+};
+
+template <int N>
+__global__ void __launch_bounds__(walk_block_threads(N)) sparse_kernel(const __grid_constant__ SparseParams P) {
+    using C = WCfg<N, 1>;
+    extern __shared__ double2 smem[];
+    // stage the permuted columns (slot k = column P.col[k]) and their negations, walk layout
+    for (int k = threadIdx.x; k < N * C::P; k += blockDim.x) {
+        const int slot = k / C::P, i = k - slot * C::P;
+        const double2 a = (i < N) ? P.A[i * N + P.col[slot]] : make_double2(0.0, 0.0);
+        smem[k] = a;
+        smem[N * C::P + k] = make_double2(-a.x, -a.y);
+    }
+    __syncthreads();
+    const uint32_t lc = (uint32_t)__cvta_generic_to_shared(smem);
+    ddc acc;
+    acc.re.hi = acc.re.lo = acc.im.hi = acc.im.lo = 0.0;
+    const uint64_t total = P.outer * P.chunks;
+    const uint64_t W = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < total; g += W) {
+        uint64_t o = g / P.chunks;
+        const uint64_t c = g - o * P.chunks;
+        double wr[N], wi[N];
+#pragma unroll
+        for (int i = 0; i < N; i++) { wr[i] = 0.0; wi[i] = 0.0; }
+        // outer combination o -> non-empty s_l: mixed radix 2^{|S_l|} - 1, digit v -> sub-mask v + 1
+        int ssum = 0;
+        for (int l = 0; l < P.d; l++) {
+            const uint64_t r = (1ull << P.ssz[l]) - 1ull;
+            const uint64_t m = o % r + 1ull;
+            o /= r;
+            for (int q = 0; q < P.ssz[l]; q++) {
+                const double f = (double)((m >> q) & 1ull);
+                flip_dyn<N>(lc + (uint32_t)((P.soff[l] + q) * C::P) * 16u, f, wr, wi);
+            }
+            ssum += __popcll(m);
+        }
+        ddc part;
+        part.re.hi = part.re.lo = part.im.hi = part.im.lo = 0.0;
+        if (P.e == 0) {
+            // a single rank r = c of the T walk (|T| < U, or no T at all)
+            const uint64_t x = c ^ (c >> 1);
+            for (int q = 0; q < P.nt; q++)
+                flip_dyn<N>(lc + (uint32_t)(q * C::P) * 16u, (double)((x >> q) & 1ull), wr, wi);
+            double ar = 0.0, ai = 0.0;
+            if (c & 1ull) term_acc<N, C::K, +1>(wr, wi, ar, ai);
+            else          term_acc<N, C::K, -1>(wr, wi, ar, ai);
+            part.re = dd_add_d(part.re, ar);
+            part.im = dd_add_d(part.im, ai);
+        } else {
+            const int e = P.e;
+            const uint64_t x = ((c ^ (c >> 1)) << e) | ((c & 1ull) << (e - 1));
+            for (int q = e - 1; q < P.nt; q++)
+                flip_dyn<N>(lc + (uint32_t)(q * C::P) * 16u, (double)((x >> q) & 1ull), wr, wi);
+            walk_seeded<C>(lc, 0u, c, e, wr, wi, part);
+        }
+        // contribution -(-1)^{|s|} * part
+        if ((ssum & 1) == 0) {
+            part.re.hi = -part.re.hi; part.re.lo = -part.re.lo;
+            part.im.hi = -part.im.hi; part.im.lo = -part.im.lo;
+        }
+        acc = ddc_add(acc, part);
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) acc = ddc_add(acc, shfl_down_ddc(acc, off));
+    __shared__ ddc swarp[32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) swarp[warp] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        ddc b = swarp[0];
+        for (int w = 1; w < (int)(blockDim.x >> 5); w++) b = ddc_add(b, swarp[w]);
+        P.partials[blockIdx.x] = b;
+    }
+}
+
+template <int N>
+cudaError_t sparse_launch_t(const SparseLaunch& L) {
+    using C = WCfg<N, 1>;
+    SparseParams P;
+    P.A = L.A_dev;
+    P.partials = L.partials;
+    P.outer = L.outer;
+    P.chunks = L.chunks;
+    P.e = L.e;
+    P.nt = L.nt;
+    P.d = L.d;
+    for (int k = 0; k < 64; k++) P.col[k] = k < N ? L.col[k] : 0;
+    for (int l = 0; l < kSparseMaxD; l++) {
+        P.soff[l] = l < L.d ? L.soff[l] : 0;
+        P.ssz[l] = l < L.d ? L.ssz[l] : 0;
+    }
+    cudaError_t err = cudaFuncSetAttribute(sparse_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)C::smem_bytes);
+    if (err != cudaSuccess) return err;
+    sparse_kernel<N><<<L.grid, walk_block_threads(N), C::smem_bytes, L.stream>>>(P);
+    return cudaGetLastError();
+}
+
+template <int N>
+cudaError_t sparse_occupancy_t(int* blocks_per_sm) {
+    using C = WCfg<N, 1>;
+    cudaError_t err = cudaFuncSetAttribute(sparse_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)C::smem_bytes);
+    if (err != cudaSuccess) return err;
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, sparse_kernel<N>, walk_block_threads(N),
+                                                         C::smem_bytes);
+}
+
+}  // namespace perm

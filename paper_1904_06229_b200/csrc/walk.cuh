@@ -327,13 +327,26 @@ __device__ __forceinline__ void seed_rows(uint32_t lc, uint32_t lb, uint64_t x, 
     }
 }
 
+template <class C>
+__device__ __forceinline__ void walk_seeded(uint32_t lc, uint32_t h, uint64_t c, int e, double (&wr)[C::R],
+                                            double (&wi)[C::R], ddc& acc);
+
 // One aligned chunk of 2^e ranks (e >= U >= 1), walked by the S lanes of a group (h = lane in group).
 template <class C>
 __device__ __forceinline__ void walk_chunk(uint32_t lc, uint32_t lb, uint32_t h, uint64_t c, int e, ddc& acc) {
-    constexpr int U = C::U, R = C::R;
+    constexpr int R = C::R;
     double wr[R], wi[R];
     const uint64_t x = ((c ^ (c >> 1)) << e) | ((c & 1ull) << (e - 1));
     seed_rows<C>(lc, lb, x, e - 1, wr, wi);
+    walk_seeded<C>(lc, h, c, e, wr, wi, acc);
+}
+
+// The walk of chunk c (2^e ranks, e >= U) from row sums already seeded at its first rank c 2^e:
+// acc += sum_{r in chunk} (-1)^{r+1} prod_i w_i(gray r).
+template <class C>
+__device__ __forceinline__ void walk_seeded(uint32_t lc, uint32_t h, uint64_t c, int e, double (&wr)[C::R],
+                                            double (&wi)[C::R], ddc& acc) {
+    constexpr int U = C::U, R = C::R;
     const uint64_t nblk = 1ull << (e - U);
     const uint64_t cpar = c & 1ull;
     constexpr uint64_t kFoldMask = (U >= kWalkFoldBits) ? 0ull : ((1ull << (kWalkFoldBits - U)) - 1ull);

@@ -32,4 +32,18 @@ cudaError_t walk_seed_launch_n(int n, const double2* A_dev, const uint64_t* rank
 #undef PERM_CASE
 }
 
+#define PERM_R48(M) PERM_R8(M, 0) PERM_R8(M, 8) PERM_R8(M, 16) PERM_R8(M, 24) PERM_R8(M, 32) PERM_R8(M, 40)
+
+cudaError_t sparse_launch(const SparseLaunch& L) {
+#define PERM_CASE(N) case N: return sparse_launch_t<N>(L);
+    switch (L.n) { PERM_R48(PERM_CASE) default: return cudaErrorInvalidValue; }
+#undef PERM_CASE
+}
+
+cudaError_t sparse_occupancy(int n, int* blocks_per_sm) {
+#define PERM_CASE(N) case N: return sparse_occupancy_t<N>(blocks_per_sm);
+    switch (n) { PERM_R48(PERM_CASE) default: return cudaErrorInvalidValue; }
+#undef PERM_CASE
+}
+
 }  // namespace perm

@@ -18,7 +18,7 @@ from __future__ import annotations
 
 import numpy as np
 
-SEEDS = {"cfg1": 16, "cfg2_u": 2000, "cfg2_idx": 3000, "cfg3": 24, "cfg4": 1024, "cfg5": 44, "cfgw": 2424, "cfgpm": 2425}
+SEEDS = {"cfg1": 16, "cfg2_u": 2000, "cfg2_idx": 3000, "cfg3": 24, "cfg4": 1024, "cfg5": 44, "cfgw": 2424, "cfgpm": 2425, "cfgsp": 4848}
 
 
 def complex_gaussian(shape, seed: int | np.random.Generator) -> np.ndarray:
@@ -155,3 +155,23 @@ def haar_minors(n: int, a: float, count: int, seed: int) -> np.ndarray:
         rows[s] = np.sort(rng.choice(m, n, replace=False))
         cols[s] = np.sort(rng.choice(m, n, replace=False))
     return gather_submatrices(U, rows, cols)
+
+
+# ---------------------------------------------------------------- sparse matrices (App. B, NEXT-3)
+
+def sparse_gaussian(n: int, density: float, seed: int) -> np.ndarray:
+    """Sparse complex Gaussian matrix: each entry nonzero with probability `density`, plus a random
+    perfect matching (so no row or column is empty and per != 0 generically) -- the low-depth
+    Boson-sampling shape of Sec. II-D.  Nonzero entries (g1 + i g2)/sqrt(2)."""
+    rng = np.random.default_rng(seed)
+    mask = rng.random((n, n)) < density
+    M = mask * (rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))) / np.sqrt(2.0)
+    M[np.arange(n), rng.permutation(n)] += (rng.standard_normal(n) + 1j * rng.standard_normal(n)) / np.sqrt(2.0)
+    return np.ascontiguousarray(M)
+
+
+def cfgsp() -> np.ndarray:
+    """Sparse workload (not a BASELINE config): n = 48, density 4% + a matching
+    (about 2.8 nonzeros per row; the paper's sparse code stops gaining above ~5%):
+    1.8e11 restricted sets instead of 2^47 = 1.4e14 Gray terms."""
+    return sparse_gaussian(48, 0.04, SEEDS["cfgsp"])

@@ -76,3 +76,24 @@ def test_finalize_errors():
         pb.perm_c128_finalize([(1, 0, 0, 0)], 0)
     with pytest.raises(pb.PermError):
         pb.perm_c128_finalize([(1, 0, 0, 0)], 65)
+
+
+def test_sparse_plan_host_logic_matches_oracle_partition():
+    # perm_sparse_plan is host-only C++ (App. B greedypartition); the oracle implements the same
+    # procedure independently -- identical partitions and enumeration sizes
+    import oracle
+    rng = np.random.default_rng(12)
+    for n, dens in ((10, 0.2), (16, 0.12), (24, 0.08), (40, 0.05)):
+        M = (rng.random((n, n)) < dens) * (rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n)))
+        M[np.arange(n), rng.permutation(n)] += 1.0
+        p = pb.perm_sparse_plan(M)
+        S, T = oracle.sparse_partition(M)
+        assert p["S"] == S and p["T"] == T
+        assert p["sets"] == 2.0 ** bin(T).count("1") * math.prod(2.0 ** bin(s).count("1") - 1 for s in S)
+    with pytest.raises(pb.PermError):
+        pb.perm_sparse_plan(np.full((3, 3), np.nan))
+    L = pb.lib()
+    assert L.perm_c128_sparse(None, 4, None, None, None) == 1
+    out = pb.c128()
+    A = np.eye(3, dtype=np.complex128)
+    assert L.perm_c128_sparse(A.ctypes.data_as(ctypes.c_void_p), 49, ctypes.byref(out), None, None) == 2

@@ -1,0 +1,74 @@
+"""GPU parity of perm_c128_sparse (App. B sparsepermanent + greedypartition; SURVEY 8(f)
+NEXT-3) against the CPU oracle (Eq. (3) / App. B written out) and the dense GPU walk."""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_1904_06229_b200 as pb
+from tests import pins
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-9
+
+
+def _sparse(n, density, seed):
+    rng = np.random.default_rng(seed)
+    M = (rng.random((n, n)) < density) * (rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))) / np.sqrt(2)
+    M[np.arange(n), rng.permutation(n)] += (rng.standard_normal(n) + 1j * rng.standard_normal(n)) / np.sqrt(2)
+    return M
+
+
+@pytest.mark.parametrize("n,density,seed", [(1, 1.0, 1), (3, 0.5, 2), (6, 0.3, 3), (10, 0.2, 4), (14, 0.15, 5),
+                                            (16, 0.1, 6), (20, 0.1, 7), (24, 0.08, 8)])
+def test_sparse_vs_oracle(n, density, seed):
+    A = _sparse(n, density, seed)
+    got, info = pb.perm_c128_sparse(A, info=True)
+    ref = oracle.ryser(A).value
+    assert pins.scaled_error(got, ref, A) <= TOL, (got, ref)
+    S, T = oracle.sparse_partition(A)
+    assert info["S"] == S and info["T"] == T
+    assert info["sets"] == 2.0 ** bin(T).count("1") * math.prod(2.0 ** bin(s).count("1") - 1 for s in S)
+
+
+def test_sparse_vs_oracle_app_b_count():
+    A = _sparse(18, 0.12, 21)
+    got, info = pb.perm_c128_sparse(A, info=True)
+    ref, cnt = oracle.sparse(A)
+    assert pins.scaled_error(got, ref.value, A) <= TOL and info["sets"] == cnt
+
+
+def test_sparse_structured():
+    n = 30
+    assert pb.perm_c128_sparse(pins.tridiagonal_ones(n).astype(complex)) == pins.fibonacci(n + 1)
+    P = np.eye(40)[np.random.default_rng(3).permutation(40)]
+    assert pb.perm_c128_sparse(P) == 1.0
+    d = (np.arange(1, 21) % 7 + 1) * (0.5 - 0.25j)
+    ref = np.prod(d)
+    assert abs(pb.perm_c128_sparse(np.diag(d)) - ref) <= 1e-13 * abs(ref)
+    Z = _sparse(12, 0.3, 9)
+    Z[:, 4] = 0
+    v, info = pb.perm_c128_sparse(Z, info=True)
+    assert v == 0 and info["sets"] == 0.0
+
+
+def test_sparse_device_input_and_dense_walk_agree():
+    import torch
+    n = 34
+    A = _sparse(n, 0.07, 34)
+    got = pb.perm_c128_sparse(torch.from_numpy(A).cuda())
+    dense = pb.perm_c128(A)                       # Glynn walk over 2^33 terms
+    assert pins.scaled_error(got, dense, A) <= TOL, (got, dense)
+
+
+def test_sparse_block_diagonal_closed_form():
+    B1, B2 = _sparse(14, 0.2, 41), _sparse(16, 0.15, 42)
+    M = np.zeros((30, 30), complex)
+    M[:14, :14], M[14:, 14:] = B1, B2
+    rng = np.random.default_rng(43)
+    M = M[rng.permutation(30)][:, rng.permutation(30)]
+    ref = oracle.ryser(B1).value * oracle.ryser(B2).value
+    assert pins.scaled_error(pb.perm_c128_sparse(M), ref, M) <= TOL
