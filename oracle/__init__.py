@@ -64,6 +64,7 @@ def _L():
             "oracle_ryser_i8": [P, i32, i32, P],
             "oracle_sparse_partition": [P, i32, P, P],
             "oracle_sparse_c128": [P, i32, P, P],
+            "oracle_band_c128": [P, i32, i32, P],
             "oracle_num_threads": [],
         }
         for name, args in sig.items():
@@ -270,3 +271,10 @@ def sparse(A) -> tuple[QC, int]:
     if _L().oracle_sparse_c128(_ptr(A), A.shape[0], _ptr(out), _ptr(c)) != 0:
         raise ValueError("oracle_sparse_c128 failed")
     return QC(out), int(c[0]) + int(c[1])
+
+
+def band(A, k: int) -> QC:
+    """App. C bandpermanent of an n x n matrix of bandwidth k (entries with |i-j| > k
+    are not read)."""
+    A = _c128(A)
+    return _call_c(_L().oracle_band_c128, _ptr(A), A.shape[0], k)

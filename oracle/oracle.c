@@ -28,6 +28,8 @@
  *   oracle_ryser_i8       Eq. (3) in exact integers for entries in {-1,0,1} (Sec. V Bernoulli +-1)
  *   oracle_sparse_partition / oracle_sparse_c128  App. B greedypartition + sparsepermanent
  *                                (P:1254-1293), pinned against Eq. (3) and by the enumeration count
+ *   oracle_band_c128      App. C bandpermanent, literal polynomial steps; pinned against
+ *                         Eq. (3)/(1) on banded matrices, Fibonacci (tridiagonal), diagonal, k >= n-1
  *   oracle_ryser_weighted_c128  Eq. (4), P:137-158 (repeated columns); pinned against Eq. (3) on the
  *                                expanded matrix, R = 1 (n! prod c_i) and the Boson-sampling
  *                                normalisation with collisions
@@ -611,6 +613,47 @@ int oracle_sparse_c128(const double* A, int n, double* out4, double* out_count) 
     if (n & 1) P = qc_scale(P, -1);
     put_qc(out4, P);
     if (out_count) put_q(out_count, C);
+    return 0;
+}
+
+/* ---------------- App. C: matrices of limited bandwidth ----------------
+ * bandpermanent(A, k, p) literally: C_i = sum_j a_ij x_j (the band |i-j| <= k of row i); p := 1; for
+ * i = 1..n: p := p * C_i, then in p set x_{i-k-1} = 1 and x_j^2 = 0; finally set every x_i = 1.
+ * p is stored as dense binary128 coefficients over the monomials of its live variables: after row i
+ * (1-based) only x_{i-k} .. x_{i+k} can be live, so before multiplying by C_i the live window is
+ * x_{i-k-1} .. x_{i+k-1} (2k+1 bits) and after it x_{i-k-1} .. x_{i+k} (2k+2 bits); "set x_{i-k-1} = 1"
+ * merges each monomial with and without that variable (a shift of the window).  x_j^2 = 0 discards any
+ * product that would repeat a live variable.  A is n x n row-major; entries outside the band are not
+ * read.  k <= 10. */
+int oracle_band_c128(const double* A, int n, int k, double* out4) {
+    if (n < 1 || k < 0 || k > 10) return 1;
+    if (k > n - 1) k = n - 1;
+    const int W = 2 * k + 1;                             /* live window before a row */
+    const size_t SW = (size_t)1 << W, SQ = (size_t)1 << (W + 1);
+    qc* p = (qc*)calloc(SW, sizeof(qc));
+    qc* q = (qc*)calloc(SQ, sizeof(qc));
+    p[0].re = 1;                                         /* p := 1 */
+    for (int i = 0; i < n; i++) {                        /* 0-based row i; window base b = i - k - 1 */
+        const int b = i - k - 1;
+        for (size_t m = 0; m < SQ; m++) { q[m].re = 0; q[m].im = 0; }
+        for (size_t m = 0; m < SW; m++) {
+            if (p[m].re == 0 && p[m].im == 0) continue;
+            for (int j = i - k; j <= i + k; j++) {       /* p * C_i */
+                if (j < 0 || j >= n) continue;
+                const int bit = j - b;                   /* 1 .. 2k+1 */
+                if ((m >> bit) & 1) continue;            /* x_j^2 = 0 */
+                q[m | ((size_t)1 << bit)] = qc_add(q[m | ((size_t)1 << bit)], qc_mul(p[m], entry(A, n, i, j)));
+            }
+        }
+        for (size_t m = 0; m < SW; m++) { p[m].re = 0; p[m].im = 0; }
+        for (size_t m = 0; m < SQ; m++)                  /* set x_{b} = 1: drop bit 0, shift the window */
+            p[m >> 1] = qc_add(p[m >> 1], q[m]);
+    }
+    qc S = { 0, 0 };
+    for (size_t m = 0; m < SW; m++) S = qc_add(S, p[m]); /* set every x = 1 */
+    free(p);
+    free(q);
+    put_qc(out4, S);
     return 0;
 }
 

@@ -461,3 +461,38 @@ def test_sparse_structured_closed_forms():
     M[:5, :5], M[5:, 5:] = B1, B2
     ref = oracle.naive(B1).value * oracle.naive(B2).value
     assert abs(oracle.sparse(M)[0].value - ref) <= 1e-13 * abs(ref)
+
+
+# ------------------------------------------------------------------ App. C band-limited (NEXT-4)
+
+def _banded(n, k, seed):
+    rng = np.random.default_rng(seed)
+    A = (rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))) / np.sqrt(2)
+    i, j = np.indices((n, n))
+    A[np.abs(i - j) > k] = 0
+    return A
+
+
+@pytest.mark.parametrize("n,k", [(1, 0), (2, 1), (5, 1), (7, 2), (9, 3), (12, 2), (14, 4), (16, 5), (18, 7)])
+def test_band_matches_eq3(n, k):
+    # App. C's transfer polynomial against Eq. (3)/(1) on matrices that vanish outside the band
+    A = _banded(n, k, 100 * n + k)
+    ref = oracle.naive(A).value if n <= 9 else oracle.ryser(A).value
+    got = oracle.band(A, k).value
+    scale = oracle.band(np.abs(A).astype(complex), k).value.real        # per(|A|): sum of |path products|
+    assert abs(got - ref) <= 1e-25 * scale
+
+
+def test_band_closed_forms():
+    for n in (1, 2, 10, 40, 90):
+        q = oracle.band(pins.tridiagonal_ones(n).astype(complex), 1)       # binary128: exact to 2^113
+        assert int(q.re_hi) + int(q.re_lo) == pins.fibonacci(n + 1) and q.im_hi == 0.0
+    d = np.arange(1, 13) * (1 - 0.5j)
+    assert abs(oracle.band(np.diag(d), 0).value - np.prod(d)) <= 1e-14 * abs(np.prod(d))
+    A = inputs.complex_gaussian((8, 8), 88)
+    assert abs(oracle.band(A, 7).value - oracle.naive(A).value) <= 1e-25 * float(np.prod(np.abs(A).sum(1)))
+    assert abs(oracle.band(A, 20).value - oracle.naive(A).value) <= 1e-25 * float(np.prod(np.abs(A).sum(1)))
+    # entries outside the band are never read
+    B = _banded(10, 2, 5)
+    C = B + np.triu(np.ones((10, 10)), 3) * 7.0
+    assert oracle.band(C, 2).value == oracle.band(B, 2).value
