@@ -626,8 +626,9 @@ int oracle_sparse_c128(const double* A, int n, double* out4, double* out_count) 
  * product that would repeat a live variable.  A is n x n row-major; entries outside the band are not
  * read.  k <= 10. */
 int oracle_band_c128(const double* A, int n, int k, double* out4) {
-    if (n < 1 || k < 0 || k > 10) return 1;
+    if (n < 1 || k < 0) return 1;
     if (k > n - 1) k = n - 1;
+    if (k > 10) return 1;
     const int W = 2 * k + 1;                             /* live window before a row */
     const size_t SW = (size_t)1 << W, SQ = (size_t)1 << (W + 1);
     qc* p = (qc*)calloc(SW, sizeof(qc));
