@@ -13,6 +13,7 @@ Workloads (BASELINE.json configs; synthetic inputs from paper_1904_06229_b200/in
   cfg1: one 16x16 complex Gaussian (latency-bound).
   cfg2: 10^5 submatrices of an n^2 x n^2 Haar unitary for each n in {8,12,16,20}; batched perms/s.
   cfg3: 64 Bernoulli 0-1 matrices of order 24; exact int128; perms/s.
+  cfgbd: 10^4 band matrices, n = 100, k = 5, App. C transfer method (NEXT-4); perms/s.
   cfgsp: one sparse 48x48 complex matrix (4% + a matching), App. B restricted enumeration (NEXT-3); sets/s.
   cfgpm: 1024 Bernoulli +-1 matrices of order 24 (Sec. V ensemble); exact; perms/s.
   cfgw: 10^4 Boson-sampling output patterns with collisions (20 photons, 20 modes), weighted Ryser
@@ -235,6 +236,16 @@ def oracle_rate_cfg(cfg: str, seconds: float = 12.0) -> dict:
         dt = time.perf_counter() - t0
         return {"value": k / dt, "unit": "perms/s", "cores": cores, "kind": "oracle",
                 "sample": f"Eq. (3) int128 oracle on {k} of the 64 config-3 matrices, {dt:.1f} s"}
+    if cfg == "cfgbd":
+        A = inputs.cfgbd(64)
+        t0 = time.perf_counter()
+        k = 0
+        while time.perf_counter() - t0 < seconds and k < A.shape[0]:
+            oracle.band(A[k], 5)
+            k += 1
+        dt = time.perf_counter() - t0
+        return {"value": k / dt, "unit": "perms/s", "cores": 1, "kind": "oracle",
+                "sample": f"App. C binary128 oracle (literal polynomial, single-threaded) on {k} cfgbd matrices, {dt:.1f} s"}
     if cfg == "cfgsp":
         A = inputs.cfgsp()
         A20 = inputs.sparse_gaussian(24, 0.04 * 48 / 24, inputs.SEEDS["cfgsp"])
@@ -429,6 +440,48 @@ def run_ours(args):
                                "64 Bernoulli(1/2) 0-1 matrices of order 24 (seed 24), exact int128 permanents"),
                   "parallelism": f"batch x{world}", "l2": "input 0.6 MB; compute-bound" if pm1 else "input 37 KB; compute-bound"}
         scaling = "weak" if world > 1 else "strong"
+    elif cfg == "cfgbd":
+        kb = 5
+        A_np = inputs.cfgbd()
+        Bn, n = A_np.shape[0], A_np.shape[1]
+        b0, b1 = shard.rank_span(Bn, world, rank)
+        host = torch.from_numpy(np.ascontiguousarray(pb.band_storage(A_np[b0:b1], kb))).pin_memory()
+        dev_in = host.to(device)
+        per_d = torch.empty(b1 - b0, dtype=torch.complex128, device=device)
+        abs2_d = torch.empty(b1 - b0, dtype=torch.float64, device=device)
+        abs2_h = torch.empty(b1 - b0, dtype=torch.float64).pin_memory()
+        e0, e1 = ev(), ev()
+        h2d, d2h = host.numel() * 16, abs2_h.numel() * 8
+        walk_launches_per_step = 1
+        # transitions per row of the App. C transfer matrix: every new state has k+1 predecessors unless
+        # the window's top column is the one just used (then 1)
+        trans = sum((1 if (t >> (2 * kb - 1)) & 1 else kb + 1) for t in range(1 << (2 * kb))
+                    if bin(t).count("1") == kb)
+        band_flops = (b1 - b0) * n * trans * 8.0
+
+        def step():
+            e0.record(stream)
+            pb.perm_c128_band_batched(dev_in, kb, per=per_d, abs2=abs2_d, stream=stream)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            es = torch.cuda.Event(enable_timing=True)
+            ee = torch.cuda.Event(enable_timing=True)
+            es.record(stream)
+            dev_in.copy_(host, non_blocking=True)
+            pb.perm_c128_band_batched(dev_in, kb, per=per_d, abs2=abs2_d, stream=stream)
+            abs2_h.copy_(abs2_d, non_blocking=True)
+            ee.record(stream)
+            torch.cuda.synchronize()
+            return {"dev": e0.elapsed_time(e1), "e2e": es.elapsed_time(ee), "walk": e0.elapsed_time(e1),
+                    "result": float(abs2_h[0])}
+
+        units_per_step = Bn
+        unit = "perms/s"
+        gpu_launches_per_step = 2
+        config = {"workload": "10^4 complex Gaussian matrices of order 100 and bandwidth 5 (seed 1005), App. C "
+                              "transfer method", "batch": Bn, "n": n, "k": kb, "parallelism": f"batch x{world}",
+                  "l2": "inputs 176 MB > L2"}
+        scaling = "weak" if world > 1 else "strong"
     elif cfg == "cfgsp":
         A_np = inputs.cfgsp()
         n = A_np.shape[0]
@@ -563,7 +616,14 @@ def run_ours(args):
             out["fp64_peak_frac"] = achieved / nominal
     else:
         # batched / int: report the device time of the batch kernels against the FP64 (or INT) pipe
-        if cfg == "cfgsp":
+        if cfg == "cfgbd":
+            achieved = band_flops / (dev_ms / K * 1e-3) / 1e12
+            out["roofline"] = {"bound": "alu", "achieved": achieved, "peak": nominal, "unit": "TFLOP/s",
+                               "frac": achieved / nominal, "traffic": ncu_traffic(cfg),
+                               "kernel": "band_kernel (FP64 complex MACs from shared memory)",
+                               "algorithmic": "8 flops per transfer-matrix transition x transitions per row x n rows",
+                               "peak_measured_probe": peak_meas}
+        elif cfg == "cfgsp":
             fl = sets * 8 * n
             achieved = fl / (dev_ms / K * 1e-3) / 1e12
             out["roofline"] = {"bound": "alu", "achieved": achieved, "peak": nominal, "unit": "TFLOP/s",
@@ -616,7 +676,7 @@ def run_reference(args):
     if rank != 0:
         return          # the reference arm runs on rank 0 only
     cfg = args.config
-    unit = "perms/s" if cfg in ("cfg2", "cfg3", "cfgw", "cfgpm") else "terms/s"
+    unit = "perms/s" if cfg in ("cfg2", "cfg3", "cfgw", "cfgpm", "cfgbd") else "terms/s"
     for _ in range(max(0, args.warmup)):
         oracle_rate_cfg(cfg, seconds=1.0)
     rates, samples = [], []
@@ -644,7 +704,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=1)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="cfg5", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "cfgw", "cfgpm", "cfgsp"])
+    ap.add_argument("--config", default="cfg5", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "cfgw", "cfgpm", "cfgsp", "cfgbd"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)

@@ -145,6 +145,21 @@ perm_status_t perm_c128_sparse(const perm_c128_t* A, int n, perm_c128_t* out_hos
                                void* stream);
 
 /* ------------------------------------------------------------------------------------------
+ * Matrices of limited bandwidth: App. C transfer method (NEXT-4).
+ * ------------------------------------------------------------------------------------------ */
+
+/* per and |per|^2 of B matrices of bandwidth k (a_ij = 0 for |i - j| > k) in O(n C(2k,k) (k+1)) work
+ * each: App. C's polynomial bookkeeping (x_j^2 = 0, x_j := 1 once column j leaves the band) as a
+ * transfer matrix over the used columns of the sliding window.
+ *   A_dev      device, band storage B*n*(2k+1) perm_c128_t: A_dev[(b*n + i)*(2k+1) + d] = a_{i, i-k+d};
+ *              entries whose column i-k+d lies outside 0..n-1 are not read.
+ *   per_dev    device, B perm_c128_t, or NULL.       abs2_dev   device, B doubles, or NULL.
+ * 1 <= n <= 2^20, 0 <= k <= min(6, n-1).  Stream-ordered; B == 0 is a no-op.
+ * Errors: PERM_E_ARG (NULL input, B < 0, k out of range, both outputs NULL), PERM_E_ORDER, PERM_E_CUDA. */
+perm_status_t perm_c128_band_batched(const perm_c128_t* A_dev, int n, int k, int64_t B, perm_c128_t* per_dev,
+                                     double* abs2_dev, void* stream);
+
+/* ------------------------------------------------------------------------------------------
  * Repeated columns: the weighted Ryser formula, Eq. (4).
  * ------------------------------------------------------------------------------------------ */
 

@@ -15,6 +15,7 @@ Names follow the C ABI:
 * :func:`perm_int01`         -- exact int128 permanents of 0-1 matrices
 * :func:`perm_pm1`           -- exact int128 permanents of matrices with entries in {-1, 0, 1} (Sec. V)
 * :func:`perm_c128_sparse`   -- sparse matrices, App. B restricted enumeration
+* :func:`perm_c128_band_batched` -- bandwidth-limited matrices, App. C transfer method
 """
 from __future__ import annotations
 
@@ -120,6 +121,7 @@ def lib() -> ctypes.CDLL:
         "perm_c128_batched": [P, i32, i64, P, P, P],
         "perm_c128_weighted_batched": [P, P, i32, i32, i64, P, P, P],
         "perm_sparse_plan": [P, i32, P],
+        "perm_c128_band_batched": [P, i32, i32, i64, P, P, P],
         "perm_c128_sparse": [P, i32, P, P, P],
         "perm_int01_workspace_bytes": [i32, i64, ctypes.POINTER(sz)],
         "perm_int01": [P, i32, i64, P, P, sz, P],
@@ -243,6 +245,41 @@ def perm_c128(A, *, workspace=None, stream=None, out=None, return_dd: bool = Fal
         extra.append({"terms": st.terms, "chunk_log2": st.chunk_log2, "threads": st.threads,
                       "blocks": st.blocks, "launches": st.launches})
     return (val, *extra) if extra else val
+
+
+def band_storage(A, k: int) -> np.ndarray:
+    """(..., n, n) dense -> (..., n, 2k+1) band storage S[..., i, d] = a_{i, i-k+d} (0 outside the matrix)."""
+    A = np.asarray(A, dtype=np.complex128)
+    n = A.shape[-1]
+    out = np.zeros(A.shape[:-1] + (2 * k + 1,), dtype=np.complex128)
+    for d in range(2 * k + 1):
+        for i in range(n):
+            j = i - k + d
+            if 0 <= j < n:
+                out[..., i, d] = A[..., i, j]
+    return out
+
+
+def perm_c128_band_batched(Ab, k: int, *, per=None, abs2=None, want_per: bool = True, want_abs2: bool = True,
+                           stream=None):
+    """per and |per|^2 of B band matrices (App. C) given in band storage: a (B, n, 2k+1)
+    complex128 CUDA tensor (see band_storage).  Stream-ordered.  Returns (per, abs2) CUDA tensors."""
+    torch = _torch()
+    if not (_is_torch(Ab) and Ab.is_cuda and Ab.dtype == torch.complex128):
+        raise ValueError("perm_c128_band_batched expects a CUDA complex128 tensor (B, n, 2k+1)")
+    Ab = Ab.contiguous()
+    B, n, w = Ab.shape
+    if w != 2 * k + 1:
+        raise ValueError("band storage width must be 2k+1")
+    if per is None and want_per:
+        per = torch.empty(B, dtype=torch.complex128, device=Ab.device)
+    if abs2 is None and want_abs2:
+        abs2 = torch.empty(B, dtype=torch.float64, device=Ab.device)
+    _check(lib().perm_c128_band_batched(ctypes.c_void_p(Ab.data_ptr()), n, k, B,
+                                        ctypes.c_void_p(per.data_ptr() if per is not None else 0),
+                                        ctypes.c_void_p(abs2.data_ptr() if abs2 is not None else 0),
+                                        _stream_ptr(stream)))
+    return per, abs2
 
 
 def perm_sparse_plan(A) -> dict:
@@ -423,5 +460,6 @@ def perm_fp64_probe(blocks: int, threads: int, iters: int, sink, stream=None):
 
 __all__ = ["perm_c128", "perm_c128_range", "perm_c128_finalize", "perm_c128_batched", "perm_c128_weighted_batched",
            "perm_int01", "perm_pm1", "perm_c128_sparse", "perm_sparse_plan",
+           "perm_c128_band_batched", "band_storage",
            "perm_c128_seed", "perm_fp64_probe", "workspace_bytes", "make_workspace", "int01_workspace_bytes",
            "PermError", "DD", "lib", "header_functions", "last_launches"]

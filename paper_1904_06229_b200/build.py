@@ -35,7 +35,7 @@ HEADERS = ["common.cuh", "internal.h", "walk.cuh", "sparse.cuh"]
 def units():
     u = [("abi.o", "abi.cu", []), ("reduce.o", "reduce.cu", []), ("batched.o", "batched.cu", []),
          ("int01.o", "int01.cu", []), ("walk_dispatch.o", "walk_dispatch.cu", []),
-         ("weighted.o", "weighted.cu", [])]
+         ("weighted.o", "weighted.cu", []), ("band.o", "band.cu", [])]
     for p in range(8):
         u.append((f"walk_inst_{p}.o", "walk_inst.cu", [f"-DPERM_PART={p}"]))
     for p in range(6):

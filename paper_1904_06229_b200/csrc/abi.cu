@@ -568,6 +568,21 @@ perm_status_t perm_c128_sparse(const perm_c128_t* A, int n, perm_c128_t* out_hos
     return result;
 }
 
+perm_status_t perm_c128_band_batched(const perm_c128_t* A_dev, int n, int k, int64_t B, perm_c128_t* per_dev,
+                                     double* abs2_dev, void* stream) {
+    g_launches = 0;
+    if (B < 0 || k < 0 || k > perm::kMaxBandK || (n >= 1 && k > n - 1)) return PERM_E_ARG;
+    if (n < 1 || n > (1 << 20)) return PERM_E_ORDER;
+    if (B == 0) return PERM_OK;
+    if (!A_dev || (!per_dev && !abs2_dev)) return PERM_E_ARG;
+    int launches = 0;
+    cudaError_t e = perm::band_launch((const double2*)A_dev, n, k, B, (double2*)per_dev, abs2_dev,
+                                      (cudaStream_t)stream, &launches);
+    if (e != cudaSuccess) return cuda_fail(e, "band kernel launch");
+    g_launches = (uint32_t)launches;
+    return PERM_OK;
+}
+
 perm_status_t perm_c128_weighted_batched(const perm_c128_t* C_dev, const int32_t* mult_dev, int n, int R,
                                          int64_t B, perm_c128_t* per_dev, double* abs2_dev, void* stream) {
     g_launches = 0;

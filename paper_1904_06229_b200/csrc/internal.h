@@ -129,6 +129,11 @@ template <int N> cudaError_t sparse_occupancy_t(int* blocks_per_sm);
 cudaError_t sparse_launch(const SparseLaunch& L);
 cudaError_t sparse_occupancy(int n, int* blocks_per_sm);
 
+// band.cu (App. C bandwidth-limited matrices)
+constexpr int kMaxBandK = 6;
+cudaError_t band_launch(const double2* A, int n, int k, int64_t B, double2* per, double* abs2, cudaStream_t s,
+                        int* launches);
+
 // weighted.cu
 constexpr int kMaxWeightedR = 64;
 cudaError_t weighted_launch(const double2* C, const int32_t* mult, int n, int R, int64_t B, double2* per,

@@ -18,7 +18,7 @@ from __future__ import annotations
 
 import numpy as np
 
-SEEDS = {"cfg1": 16, "cfg2_u": 2000, "cfg2_idx": 3000, "cfg3": 24, "cfg4": 1024, "cfg5": 44, "cfgw": 2424, "cfgpm": 2425, "cfgsp": 4848}
+SEEDS = {"cfg1": 16, "cfg2_u": 2000, "cfg2_idx": 3000, "cfg3": 24, "cfg4": 1024, "cfg5": 44, "cfgw": 2424, "cfgpm": 2425, "cfgsp": 4848, "cfgbd": 1005}
 
 
 def complex_gaussian(shape, seed: int | np.random.Generator) -> np.ndarray:
@@ -175,3 +175,21 @@ def cfgsp() -> np.ndarray:
     (about 2.8 nonzeros per row; the paper's sparse code stops gaining above ~5%):
     1.8e11 restricted sets instead of 2^47 = 1.4e14 Gray terms."""
     return sparse_gaussian(48, 0.04, SEEDS["cfgsp"])
+
+
+# ---------------------------------------------------------------- bandwidth-limited matrices (App. C, NEXT-4)
+
+def band_gaussian(shape, k: int, seed: int) -> np.ndarray:
+    """(B, n) -> (B, n, n) complex Gaussian matrices of bandwidth k (a_ij = 0 for |i - j| > k), the
+    band-limited Boson-sampling shape of Sec. II-D."""
+    B, n = shape
+    A = complex_gaussian((B, n, n), seed)
+    i, j = np.indices((n, n))
+    A[:, np.abs(i - j) > k] = 0
+    return np.ascontiguousarray(A)
+
+
+def cfgbd(count: int = 10_000) -> np.ndarray:
+    """Band-limited workload (not a BASELINE config): count complex Gaussian matrices of
+    order 100 and bandwidth 5 (the largest case of the paper's App. C timing figure)."""
+    return band_gaussian((count, 100), 5, SEEDS["cfgbd"])
