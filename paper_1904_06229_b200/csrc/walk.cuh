@@ -234,15 +234,6 @@ __device__ __forceinline__ void group_finish(double (&vr)[S], double (&vi)[S], u
     }
 }
 
-#ifdef PERM_EXP_NOLDS
-// timing experiment only (wrong results): the column operand comes from a register, not shared memory
-__device__ __forceinline__ double2 lds_x(uint32_t addr) {
-    return make_double2(__longlong_as_double((long long)addr), __longlong_as_double((long long)(addr + 8)));
-}
-#else
-#define lds_x lds_c
-#endif
-
 // w += z * column (lane's slice at shared address col), z = +-1 (or 0/1 when seeding).
 template <int R>
 __device__ __forceinline__ void flip_dyn(uint32_t col, double z, double (&wr)[R], double (&wi)[R]) {
@@ -259,7 +250,7 @@ template <int R, bool PLUS>
 __device__ __forceinline__ void flip_static(uint32_t col, double (&wr)[R], double (&wi)[R]) {
 #pragma unroll
     for (int i = 0; i < R; i++) {
-        const double2 a = lds_x(col + i * 16);
+        const double2 a = lds_c(col + i * 16);
         if (PLUS) { wr[i] += a.x; wi[i] += a.y; }
         else      { wr[i] -= a.x; wi[i] -= a.y; }
     }
@@ -272,7 +263,7 @@ template <int R>
 __device__ __forceinline__ void flip_add(uint32_t col, double (&wr)[R], double (&wi)[R]) {
 #pragma unroll
     for (int i = 0; i < R; i++) {
-        const double2 a = lds_x(col + i * 16);
+        const double2 a = lds_c(col + i * 16);
         wr[i] += a.x;
         wi[i] += a.y;
     }
