@@ -10,13 +10,14 @@
 // signed-sum step as the Gray walk of walk.cuh, with the weight prod_k C(m_k, f_k) as an extra real
 // factor (an exact integer < 2^n, exact in binary64 for n <= 32).
 //
-// Mapping: one warp per problem, persistent (problems round-robin over the resident warps).  The digit with the largest multiplicity, s, is the fastest digit:
+// Mapping: one warp per problem, persistent (each warp takes the next problem from an atomic counter).  The digit with the largest multiplicity, s, is the fastest digit:
 // every "sweep" runs f_s through 0..m_s (even sweeps) or m_s..0 (odd sweeps) while the other digits,
 // numbered in input order, follow the reflected Gray code of the sweep index q.  Lane l takes the
 // contiguous sweeps [distribute(NS, 32, l)) (App. A distribute) and seeds its row sums,
 // digits and weight explicitly from q (the "chunk seeding" of the walk), so all lanes step f_s in
 // lock-step and read the same column (+cbar_s or -cbar_s: both are staged in shared memory, the
-// address picks the sign).  Between sweeps each lane changes one outer digit (lane-dependent column).
+// address picks the sign).  Between sweeps each lane changes one outer digit (lane-dependent column,
+// fma with the direction).
 // Each lane sums its terms in double per sweep and folds them into a double-double; the 32 lane
 // partials are combined by a fixed shuffle tree; lane 0 applies (-1)^n and writes per and |per|^2.
 #include "walk.cuh"
@@ -40,21 +41,22 @@ __device__ __forceinline__ double binom_d(int m, int f) {
 
 // Shared-memory slot (bytes) of one warp for R distinct columns of order N.
 __host__ __device__ constexpr size_t wgt_slot_bytes(int N, int R) {
-    // +cbar and -cbar (2 R N double2), binomial row of each digit (R (N+1) doubles), the sweep table
-    // (N+1 doubles), radices / multiplicities / digit order (3 R ints), the lanes' outer digits and
-    // directions (2 R x 32 bytes)
-    return ((size_t)2 * R * N * 16 + (size_t)(R + 1) * (N + 1) * 8 + (size_t)3 * R * 4 + (size_t)2 * R * 32 + 15) &
+    // cbar (R N double2) and -cbar_s of the sweep digit (N double2), binomial row of each digit
+    // (R (N+1) doubles), the sweep table (N+1 doubles), radices / multiplicities / digit order (3 R ints),
+    // the lanes' outer digits and directions (2 R x 32 bytes)
+    return ((size_t)(R + 1) * N * 16 + (size_t)(R + 1) * (N + 1) * 8 + (size_t)3 * R * 4 + (size_t)2 * R * 32 + 15) &
            ~(size_t)15;
 }
 
 template <int N>
 __global__ void __launch_bounds__(WgtCfg<N>::NT, WgtCfg<N>::MINB)
     weighted_kernel(const double2* __restrict__ C, const int32_t* __restrict__ mult, int R, int64_t B,
-                    double2* __restrict__ per, double* __restrict__ abs2) {
+                    double2* __restrict__ per, double* __restrict__ abs2, unsigned long long* __restrict__ next) {
     extern __shared__ __align__(16) unsigned char wsm[];
     const int lane = threadIdx.x & 31;
     double2* col = (double2*)wsm;                                         // col[k*N + i] = cbar_i(k)
-    double* bin = (double*)(wsm + (size_t)2 * R * N * 16);                // bin[k*(N+1) + f] = C(m_k, f)
+    double2* negs = col + (size_t)R * N;                                  // -cbar_s (sweep digit)
+    double* bin = (double*)(wsm + (size_t)(R + 1) * N * 16);              // bin[k*(N+1) + f] = C(m_k, f)
     double* tsw = bin + (size_t)R * (N + 1);                              // tsw[j] = (-1)^j C(m_s, j)
     int* order = (int*)(tsw + (N + 1));                                   // order[0] = s, then the outer digits
     int* rad = order + R;                                                 // rad[p] = m_{order[p]} + 1
@@ -62,18 +64,14 @@ __global__ void __launch_bounds__(WgtCfg<N>::NT, WgtCfg<N>::MINB)
     unsigned char* gdig = (unsigned char*)(mlt + R);                      // gdig[p*32 + lane]: outer digit p
     signed char* gdir = (signed char*)(gdig + R * 32);                    // its direction (+-1)
     const uint32_t base = (uint32_t)__cvta_generic_to_shared(col);
-    const uint32_t NEG = (uint32_t)(R * N) * 16u;
+    const uint32_t nbase = (uint32_t)__cvta_generic_to_shared(negs);
 
-    for (int64_t b = blockIdx.x; b < B; b += gridDim.x) {                 // persistent: problems round-robin
+    for (;;) {                                                            // persistent: a shared work queue
         __syncwarp();
-        // stage the columns (and their negations) and the multiplicities
-        const double2* src = C + b * (int64_t)N * R;
-        for (int k = lane; k < N * R; k += 32) {
-            const int i = k / R, j = k - i * R;
-            const double2 a = src[k];
-            col[j * N + i] = a;
-            col[R * N + j * N + i] = make_double2(-a.x, -a.y);
-        }
+        unsigned long long bq = 0;
+        if (lane == 0) bq = atomicAdd(next, 1ull);
+        const int64_t b = (int64_t)__shfl_sync(0xffffffffu, bq, 0);
+        if (b >= B) break;
         const int32_t* mb = mult + b * (int64_t)R;
         int msum = 0, mbad = 0, s = 0, ms = -1;
         for (int k = 0; k < R; k++) {                                     // warp-uniform scan
@@ -81,6 +79,14 @@ __global__ void __launch_bounds__(WgtCfg<N>::NT, WgtCfg<N>::MINB)
             msum += m;
             mbad |= (m < 0) | (m > N);
             if (m > ms) { ms = m; s = k; }
+        }
+        // stage the columns, column-major, and the negated sweep column
+        const double2* src = C + b * (int64_t)N * R;
+        for (int k = lane; k < N * R; k += 32) {
+            const int i = k / R, j = k - i * R;
+            const double2 a = src[k];
+            col[j * N + i] = a;
+            if (j == s) negs[i] = make_double2(-a.x, -a.y);
         }
         if (msum != N || mbad) {                                          // not a valid multiplicity vector
             if (lane == 0) {
@@ -147,7 +153,7 @@ __global__ void __launch_bounds__(WgtCfg<N>::NT, WgtCfg<N>::MINB)
             double scale = (fsum & 1) ? -wout : wout;
             const double flip_after = (ms & 1) ? 1.0 : -1.0;              // (-1)^{m_s + 1}
             for (uint32_t q = q0;; q++) {
-                const uint32_t step = cs + ((q & 1u) ? NEG : 0u);
+                const uint32_t step = (q & 1u) ? nbase : cs;
                 double ar = 0.0, ai = 0.0;
                 for (int j = 0; j <= ms; j++) {
                     const double wt = scale * tsw[j];                     // exact: +-integer < 2^n
@@ -176,7 +182,7 @@ __global__ void __launch_bounds__(WgtCfg<N>::NT, WgtCfg<N>::MINB)
                 gdig[(p - 1) * 32 + lane] = (unsigned char)(g + d);
                 const double* bk = bin + order[p] * (N + 1);
                 wout = __dmul_rn(__ddiv_rn(wout, bk[g]), bk[g + d]);      // exact: integer quotient
-                flip_add<N>(base + (uint32_t)(order[p] * N) * 16u + (d > 0 ? 0u : NEG), wr, wi);
+                flip_dyn<N>(base + (uint32_t)(order[p] * N) * 16u, (double)d, wr, wi);   // once per sweep
                 const double sg = scale < 0.0 ? -1.0 : 1.0;
                 scale = sg * flip_after * wout;
             }
@@ -207,8 +213,16 @@ cudaError_t weighted_launch_t(const double2* C, const int32_t* mult, int R, int6
     if (bps < 1) return cudaErrorInvalidConfiguration;       // R too large for shared memory
     const int64_t cap = (int64_t)sms * bps;
     const int64_t grid = B < cap ? B : cap;
-    weighted_kernel<N><<<(unsigned)grid, WgtCfg<N>::NT, smem, st>>>(C, mult, R, B, per, abs2);
-    return cudaGetLastError();
+    unsigned long long* next = nullptr;                     // the work-queue counter, stream-ordered
+    err = cudaMallocAsync((void**)&next, sizeof(unsigned long long), st);
+    if (err != cudaSuccess) return err;
+    err = cudaMemsetAsync(next, 0, sizeof(unsigned long long), st);
+    if (err == cudaSuccess) {
+        weighted_kernel<N><<<(unsigned)grid, WgtCfg<N>::NT, smem, st>>>(C, mult, R, B, per, abs2, next);
+        err = cudaGetLastError();
+    }
+    const cudaError_t e2 = cudaFreeAsync(next, st);
+    return err != cudaSuccess ? err : e2;
 }
 
 #define PERM_R8(M, b) M(b + 1) M(b + 2) M(b + 3) M(b + 4) M(b + 5) M(b + 6) M(b + 7) M(b + 8)
