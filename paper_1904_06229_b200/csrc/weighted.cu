@@ -27,7 +27,10 @@ namespace perm {
 template <int N>
 struct WgtCfg {
     static constexpr int NT = 32;                    // one warp (one problem at a time) per block
-    static constexpr int REGS = ((4 * N + 64 + 7) / 8) * 8;
+#ifndef PERM_WGT_REG_EXTRA
+#define PERM_WGT_REG_EXTRA 64
+#endif
+    static constexpr int REGS = ((4 * N + PERM_WGT_REG_EXTRA + 7) / 8) * 8;
     static constexpr int MINB_RAW = 65536 / (NT * (REGS < 255 ? REGS : 255));
     static constexpr int MINB = MINB_RAW > 32 ? 32 : (MINB_RAW < 1 ? 1 : MINB_RAW);
 };
