@@ -58,7 +58,7 @@ typedef struct {
 typedef enum {
     PERM_OK = 0,
     PERM_E_ARG = 1,        /* null required pointer, negative count, k_begin > k_end, bad workspace size */
-    PERM_E_ORDER = 2,      /* n < 1, n > 64 (complex), n > 28 (int01), k_end > 2^{n-1}                  */
+    PERM_E_ORDER = 2,      /* n < 1, n > 64 (complex), n > 33 (int01, pm1), k_end > 2^{n-1}           */
     PERM_E_NONFINITE = 3,  /* a NaN/Inf matrix entry (perm_c128 / perm_c128_range)                       */
     PERM_E_NOT01 = 4,      /* a byte other than 0 or 1 (perm_int01)                                      */
     PERM_E_CUDA = 5,       /* a CUDA runtime call failed; see perm_last_error()                         */
@@ -186,9 +186,10 @@ perm_status_t perm_c128_weighted_batched(const perm_c128_t* C_dev, const int32_t
 /* Scratch bytes needed by perm_int01 for B matrices of order n. */
 perm_status_t perm_int01_workspace_bytes(int n, int64_t B, size_t* bytes);
 
-/* Exact per(A) of B 0-1 matrices, 1 <= n <= 28, as int128.  Integer Glynn sums g_i = 2 w_i are walked
- * in Gray order; products and the signed sum are exact mod 2^128, per = (-1)^n Sum / 2^{n-1} is exact
- * for n <= 28 (n! 2^{n-1} < 2^127), and the low n-1 bits of Sum are checked to be zero.
+/* Exact per(A) of B 0-1 matrices, 1 <= n <= 33, as int128.  n <= 28: integer Glynn sums g_i = 2 w_i are
+ * walked in Gray order; products and the signed sum are exact mod 2^128, per = (-1)^n Sum / 2^{n-1} is
+ * exact (n! 2^{n-1} < 2^127), and the low n-1 bits of Sum are checked to be zero.  29 <= n <= 33: the
+ * same walk over all 2^n subsets of Eq. (3), Sum = (-1)^{n+1} per, exact while n! < 2^127.
  *   A_dev     device, B*n*n bytes, each 0 or 1, row-major.
  *   out_dev   device, B perm_i128_t.
  * Synchronizes `stream` (to report PERM_E_NOT01 / PERM_E_CHECK).
@@ -198,8 +199,8 @@ perm_status_t perm_int01(const uint8_t* A_dev, int n, int64_t B, perm_i128_t* ou
                          void* workspace, size_t workspace_bytes, void* stream);
 
 /* Exact per(A) of B matrices with entries in {-1, 0, 1} -- the Bernoulli +-1 ensemble of Sec. V
- * -- by the same integer Glynn walk as perm_int01 (|g_i| <= n, so the
- * same n <= 28 exactness bound).  Same workspace (perm_int01_workspace_bytes), outputs and errors as
+ * -- by the same integer walks as perm_int01 (|g_i| <= n, so the
+ * same n <= 33 range).  Same workspace (perm_int01_workspace_bytes), outputs and errors as
  * perm_int01; PERM_E_NOT01 here means an entry outside {-1, 0, 1}.
  *   A_dev     device, B*n*n signed bytes, row-major. */
 perm_status_t perm_pm1(const int8_t* A_dev, int n, int64_t B, perm_i128_t* out_dev,

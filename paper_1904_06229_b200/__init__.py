@@ -398,7 +398,7 @@ def int01_workspace_bytes(n: int, B: int) -> int:
 
 
 def perm_int01(A, *, workspace=None, out=None, stream=None, as_int: bool = True):
-    """Exact per of a (B, n, n) uint8 0-1 CUDA tensor, n <= 28.  Synchronizes.  Returns a list of Python
+    """Exact per of a (B, n, n) uint8 0-1 CUDA tensor, n <= 33.  Synchronizes.  Returns a list of Python
     ints (as_int) or the raw (B, 2) int64 CUDA tensor {lo, hi} of two's-complement int128."""
     torch = _torch()
     if not (_is_torch(A) and A.is_cuda and A.dtype == torch.uint8):
@@ -423,7 +423,7 @@ def perm_int01(A, *, workspace=None, out=None, stream=None, as_int: bool = True)
 
 def perm_pm1(A, *, workspace=None, out=None, stream=None, as_int: bool = True):
     """Exact per of a (B, n, n) int8 CUDA tensor with entries in {-1, 0, 1} (Bernoulli +-1 ensemble,
-    Sec. V), n <= 28.  Synchronizes.  Returns Python ints (as_int) or the raw (B, 2) int64 {lo, hi}."""
+    Sec. V), n <= 33.  Synchronizes.  Returns Python ints (as_int) or the raw (B, 2) int64 {lo, hi}."""
     torch = _torch()
     if not (_is_torch(A) and A.is_cuda and A.dtype == torch.int8):
         raise ValueError("perm_pm1 expects a CUDA int8 tensor (B, n, n)")

@@ -7,7 +7,9 @@
 // Products: rows in groups of 6 in int32 (n^6 < 2^31 for n <= 28), pairs of groups in int64,
 // then 64x64 -> 128 (and a further 128x64 for n > 24) modulo 2^128; the signed sum is kept mod 2^128
 // in unsigned __int128.  The result is exact when |Sum| = 2^{n-1} per <= 2^{n-1} n! < 2^127, i.e.
-// n <= 28 (R10); the low n-1 bits of Sum must be zero (self-check, PERM_E_CHECK).
+// n <= 28 (R10); the low n-1 bits of Sum must be zero (self-check, PERM_E_CHECK).  For
+// 29 <= n <= 33 the same walk runs over all 2^n subsets of Eq. (3) (row sums a_ij, no pinned column),
+// whose signed sum is -(-1)^n per itself -- exact in int128 while n! < 2^127.
 //
 // Mapping: grid (blocks_per_matrix, B); each block stages its matrix (validating 0/1 bytes) in shared
 // memory as int32 column increments 2 a_ij; each thread walks aligned chunks of 2^E ranks with the
@@ -25,6 +27,10 @@ struct I01Cfg {
     static constexpr int U = walk_inner_bits(N);
     static constexpr int NT = 128;
     static constexpr int NP = (N + 3) & ~3;          // column stride (ints): 16-byte aligned columns
+    // n <= 28: the half-range Glynn walk (2^{n-1} terms, Sum = 2^{n-1} per must stay below 2^127);
+    // 29 <= n <= 33: the full-range Ryser walk of Eq. (3) (2^n terms, Sum = -(-1)^n per, |per| <= n! < 2^127)
+    static constexpr bool FULL = N > kMaxGlynnInt01N;
+    static constexpr int NB = FULL ? N : N - 1;      // Gray bits (columns walked)
 };
 
 __device__ __forceinline__ int lds_i(uint32_t addr) {
@@ -136,7 +142,7 @@ template <int N>
 __device__ __forceinline__ void int_seed(uint32_t sc, uint32_t sbase, uint64_t x, int j0, int (&g)[N]) {
 #pragma unroll
     for (int i = 0; i < N; i++) g[i] = lds_i(sbase + 4 * i);
-    for (int j = j0; j < N - 1; j++) {
+    for (int j = j0; j < I01Cfg<N>::NB; j++) {
         const int f = (int)((x >> j) & 1ull);
         int_flip<N>(sc + 4u * (uint32_t)(j * I01Cfg<N>::NP), f, g);
     }
@@ -176,8 +182,10 @@ __global__ void __launch_bounds__(I01Cfg<N>::NT) int01_kernel(const uint8_t* __r
                                                               uint64_t chunks, u128* __restrict__ partials,
                                                               int* __restrict__ flag) {
     constexpr int NP = I01Cfg<N>::NP;
-    __shared__ __align__(16) int s_col[N * NP];   // s_col[j*NP + i] = 2 a_ij (rows N..NP-1 zero)
-    __shared__ int s_base[N];                     // a_{i,n} - sum_{j<n} a_ij
+    constexpr bool FULL = I01Cfg<N>::FULL;
+    constexpr int CM = FULL ? 1 : 2;               // column increment: 2 a_ij (Glynn) or a_ij (Ryser)
+    __shared__ __align__(16) int s_col[N * NP];   // s_col[j*NP + i] = CM a_ij (rows N..NP-1 zero)
+    __shared__ int s_base[N];                     // Glynn: a_{i,n} - sum_{j<n} a_ij; Ryser: 0
     const int64_t m = blockIdx.y;
     const uint8_t* a = A + m * (N * N);
     for (int k = threadIdx.x; k < N * NP; k += blockDim.x) s_col[k] = 0;
@@ -186,13 +194,13 @@ __global__ void __launch_bounds__(I01Cfg<N>::NT) int01_kernel(const uint8_t* __r
         const int v = PM1 ? (int)(int8_t)a[k] : (int)a[k];
         if (PM1 ? (v < -1 || v > 1) : (v > 1)) atomicOr(flag, 1);
         const int i = k / N, j = k - i * N;
-        s_col[j * NP + i] = PM1 ? 2 * (v < -1 ? -1 : (v > 1 ? 1 : v)) : 2 * (v & 1);
+        s_col[j * NP + i] = PM1 ? CM * (v < -1 ? -1 : (v > 1 ? 1 : v)) : CM * (v & 1);
     }
     __syncthreads();
     for (int i = threadIdx.x; i < N; i += blockDim.x) {
         int s = 0;
         for (int j = 0; j < N - 1; j++) s += s_col[j * NP + i];
-        s_base[i] = s_col[(N - 1) * NP + i] / 2 - s / 2;
+        s_base[i] = FULL ? 0 : s_col[(N - 1) * NP + i] / 2 - s / 2;
     }
     __syncthreads();
     const uint32_t sc = (uint32_t)__cvta_generic_to_shared(s_col);
@@ -227,10 +235,16 @@ __global__ void int01_final_kernel(const u128* __restrict__ partials, int nblk, 
     if (m >= B) return;
     u128 s = 0;
     for (int k = 0; k < nblk; k++) s += partials[m * nblk + k];
-    const u128 mask = (((u128)1) << (n - 1)) - 1;
-    if (s & mask) atomicOr(flag, 2);
-    __int128 v = (__int128)s >> (n - 1);          // arithmetic shift: Sum / 2^{n-1}
-    if (n & 1) v = -v;                            // per = (-1)^n Sum / 2^{n-1}
+    __int128 v;
+    if (n > kMaxGlynnInt01N) {                    // full-range Ryser: per = (-1)^{n+1} Sum
+        v = (__int128)s;
+        if (!(n & 1)) v = -v;
+    } else {
+        const u128 mask = (((u128)1) << (n - 1)) - 1;
+        if (s & mask) atomicOr(flag, 2);
+        v = (__int128)s >> (n - 1);               // arithmetic shift: Sum / 2^{n-1}
+        if (n & 1) v = -v;                        // per = (-1)^n Sum / 2^{n-1}
+    }
     out[2 * m] = (unsigned long long)v;
     out[2 * m + 1] = (unsigned long long)((u128)v >> 64);
 }
@@ -244,10 +258,11 @@ struct I01Plan {
 static I01Plan int01_plan(int n, int64_t B) {
     // threads per matrix ~ max(128, 148*16*128 / B) (a few waves of the whole chip), chunk >= 2^U
     const int U = walk_inner_bits(n);
-    const uint64_t total = 1ull << (n - 1);
+    const int nb = n > kMaxGlynnInt01N ? n : n - 1;           // Gray bits
+    const uint64_t total = 1ull << nb;
     int64_t want_threads = (int64_t)148 * 16 * 128 / (B > 0 ? B : 1);
     if (want_threads < 128) want_threads = 128;
-    int e = n - 1;
+    int e = nb;
     while (e > U && (total >> e) < (uint64_t)want_threads * 4) e--;
     if (n == 1) e = 0;
     I01Plan p;
@@ -290,8 +305,8 @@ cudaError_t int01_launch(const uint8_t* A, int n, int64_t B, bool pm1, void* out
     if (err != cudaSuccess) return err;
     switch (n) {
 #define PERM_CASE(N) case N: err = int01_launch_t<N>(A, B, p, partials, flag, pm1, s); break;
-        PERM_R8(PERM_CASE, 0) PERM_R8(PERM_CASE, 8) PERM_R8(PERM_CASE, 16)
-        PERM_CASE(25) PERM_CASE(26) PERM_CASE(27) PERM_CASE(28)
+        PERM_R8(PERM_CASE, 0) PERM_R8(PERM_CASE, 8) PERM_R8(PERM_CASE, 16) PERM_R8(PERM_CASE, 24)
+        PERM_CASE(33)
 #undef PERM_CASE
         default: return cudaErrorInvalidValue;
     }

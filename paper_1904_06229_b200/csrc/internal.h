@@ -10,7 +10,8 @@ namespace perm {
 
 constexpr int kMaxN = 64;          // ranks are 64-bit words
 constexpr int kMaxBatchedN = 32;   // perm_c128_batched
-constexpr int kMaxInt01N = 28;     // exactness bound of the int128 Glynn sum (R10)
+constexpr int kMaxGlynnInt01N = 28;   // exactness bound of the int128 Glynn sum (R10)
+constexpr int kMaxInt01N = 33;        // full-range Ryser in int128 beyond it: |per| <= n! < 2^127
 constexpr int kMaxSegments = 96;
 
 // Inner unrolled Gray bits U(N) of the single-matrix walk: a block of 2^U consecutive ranks is

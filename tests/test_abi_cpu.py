@@ -43,7 +43,7 @@ def test_validation_without_gpu():
     assert L.perm_c128_batched(None, 33, 1, None, None, None) == 2                       # n > 32
     assert L.perm_c128_batched(None, 8, -1, None, None, None) == 1                       # B < 0
     assert L.perm_c128_batched(None, 8, 0, None, None, None) == 0                        # B == 0: no-op
-    assert L.perm_int01(None, 29, 1, None, None, 0, None) == 2                           # n > 28
+    assert L.perm_int01(None, 34, 1, None, None, 0, None) == 2                           # n > 33
     assert L.perm_int01(None, 24, 0, None, None, 0, None) == 0                           # B == 0: no-op
     b = ctypes.c_size_t()
     assert L.perm_int01_workspace_bytes(24, 64, ctypes.byref(b)) == 0 and b.value > 16

@@ -40,8 +40,9 @@ def test_dense_and_sparse(torch):
         assert _run(torch, A) == oracle.ryser_i01_batch(A)
 
 
-@pytest.mark.parametrize("n", [20, 24, 26, 28])
+@pytest.mark.parametrize("n", [20, 24, 26, 28, 29, 31, 33])
 def test_closed_forms(torch, n):
+    # n >= 29 runs the full-range Ryser walk (2^n subsets): the same closed forms, exact in int128
     mats = [np.ones((n, n), np.uint8), np.eye(n, dtype=np.uint8), pins.j_minus_i(n), pins.tridiagonal_ones(n),
             pins.hessenberg_ones(n), pins.identity_plus_shift(n), pins.menage_matrix(n),
             np.zeros((n, n), np.uint8)]
@@ -65,4 +66,12 @@ def test_not01_and_empty(torch):
     assert e.value.name == "PERM_E_NOT01"
     assert pb.perm_int01(torch.zeros((0, 5, 5), dtype=torch.uint8, device="cuda")) == []
     with pytest.raises(pb.PermError):
-        _run(torch, np.ones((1, 29, 29), np.uint8))
+        _run(torch, np.ones((1, 34, 34), np.uint8))
+
+
+def test_full_range_n29_vs_oracle(torch):
+    # the Ryser (2^n subsets) branch against the int128 Eq. (3) oracle, 0-1 and +-1 entries
+    A = inputs.bernoulli01((2, 29, 29), 2929)
+    assert _run(torch, A) == oracle.ryser_i01_batch(A)
+    P = inputs.bernoulli_pm1((1, 29, 29), 2930)
+    assert pb.perm_pm1(torch.from_numpy(P).cuda()) == [oracle.ryser_i8(P[0])]
