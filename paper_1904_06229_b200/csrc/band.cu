@@ -65,6 +65,12 @@ constexpr size_t band_smem_bytes(int k) {
            (k >= 6 ? (size_t)band_states(k) * (k + 1) * sizeof(int) : 0);
 }
 
+__device__ __forceinline__ double2 lds_band(uint32_t addr) {
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
+    return v;
+}
+
 template <int K>
 __global__ void __launch_bounds__(32 * kBandWarps) band_kernel(const double2* __restrict__ A, int n, int64_t B,
                                                                double2* __restrict__ per,
@@ -122,16 +128,21 @@ __global__ void __launch_bounds__(32 * kBandWarps) band_kernel(const double2* __
                 rnext = (j >= 0 && j < n) ? Ab[(int64_t)(i + 1) * W + lane] : make_double2(0.0, 0.0);
             }
             __syncwarp();
+            const uint32_t cb = (uint32_t)__cvta_generic_to_shared(cur);
+            const uint32_t rb = (uint32_t)__cvta_generic_to_shared(row);
 #pragma unroll
             for (int u = 0; u < SPL; u++) {
                 const int t = lane + 32 * u;
                 if (t < S) {
+                    // ranks < S/2 have no state bit 2k-1 set: k+1 predecessors; the others exactly one
+                    const int np = (t < S / 2) ? P1 : 1;
                     double vr = 0.0, vi = 0.0;
 #pragma unroll
                     for (int x = 0; x < P1; x++) {
+                        if (x >= np) break;
                         const int e = REG ? predr[REG ? u : 0][REG ? x : 0] : preds[t * P1 + x];
-                        if (e < 0) break;
-                        const double2 c = cur[e >> 4], a = row[e & 15];
+                        const double2 c = lds_band(cb + (uint32_t)(e >> 4) * 16u);
+                        const double2 a = lds_band(rb + (uint32_t)(e & 15) * 16u);
                         vr = fma(c.x, a.x, vr);
                         vr = fma(-c.y, a.y, vr);
                         vi = fma(c.x, a.y, vi);
