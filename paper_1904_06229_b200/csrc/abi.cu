@@ -151,7 +151,7 @@ perm_status_t plan_walk(int n, uint64_t k0, uint64_t k1, WalkPlan& p) {
     perm_status_t st = device_threads(n, &max_grid, &nt, &max_grid_c);
     if (st != PERM_OK) return st;
     p.threads = nt;
-    const uint64_t T = (uint64_t)(max_grid_c > 0 ? max_grid_c * perm::walk_block_threads(n) : max_grid * nt);
+    const uint64_t T = (uint64_t)(max_grid_c > 0 ? max_grid_c * perm::walk_body_walkers(n) : max_grid * nt);
     p.b = choose_b(n, k1 - k0, T);
     if (!decompose(n, k0, k1, p.b, p)) {
         snprintf(g_err, sizeof(g_err), "range decomposition exceeded %d segments", perm::kMaxSegments);
@@ -167,7 +167,7 @@ perm_status_t plan_walk(int n, uint64_t k0, uint64_t k1, WalkPlan& p) {
             p.use_const = 1;
             p.body = best;
             const uint64_t body = p.seg[best].count;
-            const uint64_t wc = perm::walk_block_threads(n);
+            const uint64_t wc = perm::walk_body_walkers(n);
             uint64_t need = (body + wc - 1) / wc;
             p.grid = (int)(need < (uint64_t)max_grid_c ? need : (uint64_t)max_grid_c);
             if (p.grid < 1) p.grid = 1;

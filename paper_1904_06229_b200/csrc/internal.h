@@ -72,7 +72,17 @@ constexpr int kConstMaxN = 45;
 #define PERM_CONST_ORDERS 32
 #endif
 __host__ __device__ constexpr bool walk_const_path(int n) {
-    return n <= kConstMaxN && (PERM_CONST_ORDERS == 0 || n == PERM_CONST_ORDERS);
+    return n <= kConstMaxN && (PERM_CONST_ORDERS == 0 || n == PERM_CONST_ORDERS || n == 44);
+}
+
+// Warp-pair walk (walk_pair.cuh): each chunk's rows split between two warps, three 128-thread CTAs per SM.
+#ifndef PERM_WALK_PAIR
+#define PERM_WALK_PAIR 0
+#endif
+__host__ __device__ constexpr bool walk_pair_path(int n) { return PERM_WALK_PAIR && n >= 40 && n <= 48; }
+// chunk walkers per block of the kernel that walks the aligned body (walk_kernel_c / walk_kernel_p)
+__host__ __device__ constexpr int walk_body_walkers(int n) {
+    return walk_pair_path(n) ? 64 : walk_block_threads(n);
 }
 
 struct WalkLaunch {

@@ -556,8 +556,31 @@ __device__ __forceinline__ void walk_chunk_const(const WalkParamsC<C::N>& P, uin
     }
 }
 
+// Register cap of the constant-bank walk for order N (0: the default __launch_bounds__ kernel).  Whether
+// ptxas keeps the per-use parameter loads on the uniform datapath (LDCU -> DADD R, R, UR: one vector
+// register read per update instead of two) depends on its register allocation; these caps are the ones
+// measured to produce LDCU for U = 2 (tools/const_ldcu_scan.sh, profiles/round1_const_ldcu_scan.txt), and
+// tests/test_abi_cpu.py checks the built library still does.
+__host__ __device__ constexpr int walk_const_maxnreg(int n) {
+    return n == 44 ? 248 : 0;
+}
+
+template <int N>
+__device__ __forceinline__ void walk_body_c(const WalkParamsC<N>& P);
+
 template <int N>
 __global__ void __launch_bounds__(walk_block_threads(N)) walk_kernel_c(const __grid_constant__ WalkParamsC<N> P) {
+    walk_body_c<N>(P);
+}
+
+template <int N>
+__global__ void __maxnreg__(walk_const_maxnreg(N) > 0 ? walk_const_maxnreg(N) : 255)
+    walk_kernel_cm(const __grid_constant__ WalkParamsC<N> P) {
+    walk_body_c<N>(P);
+}
+
+template <int N>
+__device__ __forceinline__ void walk_body_c(const WalkParamsC<N>& P) {
     using C = WCfg<N, 1>;
     extern __shared__ double2 smem[];
     double2* scol = smem;                                    // scol[j*N + i] = a_ij, then -a_ij at + N*N
@@ -661,7 +684,15 @@ cudaError_t walk_launch_smem(const WalkLaunch& L, const Segment* seg, int nseg, 
 // walk_kernel_c (matrix in the constant bank) on L.grid blocks and the remaining segments, if any, in
 // walk_kernel on L.grid_edge blocks; partials land in L.partials[0 .. L.grid + L.grid_edge).
 template <int N>
+cudaError_t walk_launch_pair(const WalkLaunch& L);
+template <int N>
+cudaError_t walk_occupancy_pair(int* blocks_per_sm);
+
+template <int N>
 cudaError_t walk_launch(const WalkLaunch& L) {
+    if constexpr (walk_pair_path(N)) {
+        if (L.use_const) return walk_launch_pair<N>(L);
+    }
     if constexpr (walk_const_path(N) && walk_lanes_per_chunk(N) == 1 && walk_inner_bits(N) >= 1) {
         if (L.use_const) {
             const Segment& b = L.seg[L.body];
@@ -673,7 +704,10 @@ cudaError_t walk_launch(const WalkLaunch& L) {
             P.c0 = b.c0;
             P.count = b.count;
             P.eb = b.e;
-            walk_kernel_c<N><<<L.grid, walk_block_threads(N), WCfg<N, 1>::smem_bytes, L.stream>>>(P);
+            if constexpr (walk_const_maxnreg(N) > 0)
+                walk_kernel_cm<N><<<L.grid, walk_block_threads(N), WCfg<N, 1>::smem_bytes, L.stream>>>(P);
+            else
+                walk_kernel_c<N><<<L.grid, walk_block_threads(N), WCfg<N, 1>::smem_bytes, L.stream>>>(P);
             cudaError_t err = cudaGetLastError();
             if (err != cudaSuccess || L.grid_edge == 0) return err;
             Segment rest[kMaxSegments];
@@ -690,11 +724,13 @@ cudaError_t walk_launch(const WalkLaunch& L) {
 template <int N>
 cudaError_t walk_occupancy_c(int* blocks_per_sm) {
     *blocks_per_sm = 0;
+    if constexpr (walk_pair_path(N)) return walk_occupancy_pair<N>(blocks_per_sm);
     if constexpr (walk_const_path(N) && walk_lanes_per_chunk(N) == 1 && walk_inner_bits(N) >= 1) {
-        cudaError_t err = cudaFuncSetAttribute(walk_kernel_c<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        const void* k = walk_const_maxnreg(N) > 0 ? (const void*)walk_kernel_cm<N> : (const void*)walk_kernel_c<N>;
+        cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                (int)WCfg<N, 1>::smem_bytes);
         if (err != cudaSuccess) return err;
-        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, walk_kernel_c<N>, walk_block_threads(N),
+        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k, walk_block_threads(N),
                                                              WCfg<N, 1>::smem_bytes);
     }
     return cudaSuccess;

@@ -1,7 +1,7 @@
 // walk_inst.cu -- explicit instantiations of the single-matrix walk for a range of orders N.
 // Compiled several times with -DPERM_PART=p (p = 0..7) so the 64 instantiations build in parallel;
 // part p instantiates N = 8p+1 .. 8p+8.
-#include "walk.cuh"
+#include "walk_pair.cuh"
 
 #ifndef PERM_PART
 #error "PERM_PART must be defined"

@@ -5,6 +5,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 
 import numpy as np
 import pytest
@@ -97,3 +98,21 @@ def test_sparse_plan_host_logic_matches_oracle_partition():
     out = pb.c128()
     A = np.eye(3, dtype=np.complex128)
     assert L.perm_c128_sparse(A.ctypes.data_as(ctypes.c_void_p), 49, ctypes.byref(out), None, None) == 2
+
+
+def test_const_walk_keeps_uniform_column_operands():
+    # The n = 32 and n = 44 walks take their inner columns as uniform-register operands (LDCU from the
+    # kernel-parameter bank): +12% at n = 44.  ptxas only does this for some register
+    # caps, so guard the built library's SASS against a silent fallback to per-lane LDC loads.
+    import shutil
+    import subprocess
+    cuobjdump = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(cuobjdump):
+        pytest.skip("cuobjdump not available")
+    lib = pb._LIB_PATH
+    for fn in ("_ZN4perm13walk_kernel_cILi32EEEvNS_11WalkParamsCIXT_EEE",
+               "_ZN4perm14walk_kernel_cmILi44EEEvNS_11WalkParamsCIXT_EEE"):
+        sass = subprocess.run([cuobjdump, "-sass", "-fun", fn, lib], capture_output=True, text=True).stdout
+        uniform = sum(1 for l in sass.splitlines() if "LDCU.64" in l and "c[0x0][UR" in l)
+        lane = sum(1 for l in sass.splitlines() if " LDC.64 R" in l and "c[0x0][R" in l)
+        assert uniform > 100 and lane == 0, (fn, uniform, lane)
