@@ -16,12 +16,15 @@ constexpr int kMaxSegments = 96;
 
 // Inner unrolled Gray bits U(N) of the single-matrix walk: a block of 2^U consecutive ranks is
 // fully unrolled, so the columns 0..U-1 it touches are compile-time operands.
-// U = 3 (8-term blocks) up to n = 39, U = 2 from n = 40 (the 4n-register row sums leave ptxas less room
-// to overlap an 8-term block; measured +4% at n = 44, profiles/round1_walk_variants.md).
 #ifdef PERM_WALK_U
 __host__ __device__ constexpr int walk_inner_bits(int n) { return (n - 1) < PERM_WALK_U ? (n - 1) : PERM_WALK_U; }
 #else
-__host__ __device__ constexpr int walk_inner_bits(int n) { return n >= 40 ? 2 : ((n - 1) < 3 ? (n - 1) : 3); }
+// U = 3 (8-term blocks) up to n = 39 and U = 2 beyond (the 4n-register row sums leave ptxas less room
+// to overlap an 8-term block); U = 2 also for the constant-bank orders 34, 35, 37, 39, whose register caps
+// (walk.cuh: walk_const_maxnreg) were found for U = 2.
+__host__ __device__ constexpr int walk_inner_bits(int n) {
+    return (n == 34 || n == 35 || n == 37 || n == 39 || n >= 40) ? 2 : ((n - 1) < 3 ? (n - 1) : 3);
+}
 #endif
 constexpr int kWalkThreads = 64;
 // Lanes that share one chunk in the single-matrix walk (rows split between them, K1).  The n
@@ -64,15 +67,20 @@ struct Segment {
 
 // Largest order whose whole matrix fits the 32 KB kernel-parameter space (walk_kernel_c).
 constexpr int kConstMaxN = 45;
-// Orders that use the constant-bank walk.  ptxas keeps the per-use parameter loads on the uniform
-// datapath (LDCU -> DADD R, R, UR) only for some orders; for the others it emits vector LDCs and the
-// shared-memory walk is faster.  Measured on B200 (profiles/round1_walk_variants.md): n = 32 +7%,
-// n = 44 -7%.  PERM_CONST_ORDERS=-1 disables the path, 0 enables it for every n <= kConstMaxN.
+// Orders that use the constant-bank walk: the ones for which ptxas keeps the per-use parameter loads on
+// the uniform datapath (LDCU -> DADD R, R, UR, one vector register read per update) -- n = 32 at its
+// default allocation, 34, 35, 37, 39, 42..45 under the register caps of walk_const_maxnreg (walk.cuh).
+// Measured on B200 (profiles/round1_const_table_rates.txt): +4..12% over the shared-memory walk (n = 44:
+// 6.14e10 vs 5.49e10 terms/s).  PERM_CONST_ORDERS=0 enables the path for every n <= kConstMaxN (scans).
 #ifndef PERM_CONST_ORDERS
 #define PERM_CONST_ORDERS 32
 #endif
 __host__ __device__ constexpr bool walk_const_path(int n) {
-    return n <= kConstMaxN && (PERM_CONST_ORDERS == 0 || n == PERM_CONST_ORDERS || n == 44);
+#if PERM_CONST_ORDERS == 0
+    return n <= kConstMaxN;                               // scans only
+#else
+    return n == PERM_CONST_ORDERS || n == 34 || n == 35 || n == 37 || n == 39 || (n >= 42 && n <= 45);
+#endif
 }
 
 // Warp-pair walk (walk_pair.cuh): each chunk's rows split between two warps, three 128-thread CTAs per SM.

@@ -562,7 +562,12 @@ __device__ __forceinline__ void walk_chunk_const(const WalkParamsC<C::N>& P, uin
 // measured to produce LDCU for U = 2 (tools/const_ldcu_scan.sh, profiles/round1_const_ldcu_scan.txt), and
 // tests/test_abi_cpu.py checks the built library still does.
 __host__ __device__ constexpr int walk_const_maxnreg(int n) {
-    return n == 44 ? 248 : 0;
+#ifdef PERM_CONST_MAXNREG_ALL
+    return PERM_CONST_MAXNREG_ALL;                  // scans only (tools/const_ldcu_scan.sh)
+#else
+    return n == 34 ? 200 : n == 35 ? 208 : n == 37 ? 216 : n == 39 ? 224 : n == 42 ? 208 : n == 43 ? 208
+         : n == 44 ? 248 : n == 45 ? 216 : 0;
+#endif
 }
 
 template <int N>

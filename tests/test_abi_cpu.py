@@ -101,8 +101,8 @@ def test_sparse_plan_host_logic_matches_oracle_partition():
 
 
 def test_const_walk_keeps_uniform_column_operands():
-    # The n = 32 and n = 44 walks take their inner columns as uniform-register operands (LDCU from the
-    # kernel-parameter bank): +12% at n = 44.  ptxas only does this for some register
+    # The constant-bank walks (n = 32, 34, 35, 37, 39, 42..45) take their inner columns as uniform-register
+    # operands (LDCU from the kernel-parameter bank): +4..12%.  ptxas only does this for some register
     # caps, so guard the built library's SASS against a silent fallback to per-lane LDC loads.
     import shutil
     import subprocess
@@ -110,8 +110,9 @@ def test_const_walk_keeps_uniform_column_operands():
     if not os.path.exists(cuobjdump):
         pytest.skip("cuobjdump not available")
     lib = pb._LIB_PATH
-    for fn in ("_ZN4perm13walk_kernel_cILi32EEEvNS_11WalkParamsCIXT_EEE",
-               "_ZN4perm14walk_kernel_cmILi44EEEvNS_11WalkParamsCIXT_EEE"):
+    fns = ["_ZN4perm13walk_kernel_cILi32EEEvNS_11WalkParamsCIXT_EEE"]
+    fns += [f"_ZN4perm14walk_kernel_cmILi{n}EEEvNS_11WalkParamsCIXT_EEE" for n in (34, 35, 37, 39, 42, 43, 44, 45)]
+    for fn in fns:
         sass = subprocess.run([cuobjdump, "-sass", "-fun", fn, lib], capture_output=True, text=True).stdout
         uniform = sum(1 for l in sass.splitlines() if "LDCU.64" in l and "c[0x0][UR" in l)
         lane = sum(1 for l in sass.splitlines() if " LDC.64 R" in l and "c[0x0][R" in l)

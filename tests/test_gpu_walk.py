@@ -165,6 +165,23 @@ def test_range_random_spans(n):
         assert abs(got - ref) <= 1e-12 * scale, (n, k0, k1, got, ref)
 
 
+@pytest.mark.parametrize("n", [32, 34, 35, 37, 39, 42, 43, 44, 45])
+def test_const_bank_walk_orders(n, monkeypatch):
+    # the constant-bank kernels (uniform-register column operands) for every order that uses them:
+    # PERM_FORCE_CHUNK_LOG2 = 3 makes a 2^16-term span an aligned body of 8-term chunks (e > U), which is
+    # what the planner hands to walk_kernel_c; the head/tail pieces of the unaligned span go to walk_kernel
+    monkeypatch.setenv("PERM_FORCE_CHUNK_LOG2", "3")
+    A = inputs.complex_gaussian((n, n), 3000 + n)
+    N = 1 << (n - 1)
+    rng = np.random.default_rng(3000 + n)
+    for k0 in (0, int(rng.integers(0, N - (1 << 17))) | 5):
+        k1 = k0 + (1 << 16) + 3
+        got = pb.perm_c128_range(A, k0, k1).value
+        ref = oracle.subpermanent(A, k0, k1 - k0).value
+        scale = max(abs(ref), pins.range_scale(A, k1 - k0))
+        assert abs(got - ref) <= 1e-12 * scale, (n, k0, got, ref)
+
+
 def test_range_empty_is_zero():
     A = inputs.complex_gaussian((10, 10), 1)
     assert pb.perm_c128_range(A, 17, 17).value == 0
