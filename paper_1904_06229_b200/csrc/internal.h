@@ -22,9 +22,15 @@ __host__ __device__ constexpr int walk_inner_bits(int n) { return (n - 1) < PERM
 // U = 3 (8-term blocks) up to n = 39 and U = 2 beyond (the 4n-register row sums leave ptxas less room
 // to overlap an 8-term block); U = 2 also for the constant-bank orders 34, 35, 37, 39, whose register caps
 // (walk.cuh: walk_const_maxnreg) were found for U = 2.
+#ifdef PERM_CONST_TABLE2
+__host__ __device__ constexpr int walk_inner_bits(int n) {
+    return n == 41 ? 3 : (n >= 33 ? 2 : ((n - 1) < 3 ? (n - 1) : 3));
+}
+#else
 __host__ __device__ constexpr int walk_inner_bits(int n) {
     return (n == 34 || n == 35 || n == 37 || n == 39 || n >= 40) ? 2 : ((n - 1) < 3 ? (n - 1) : 3);
 }
+#endif
 #endif
 constexpr int kWalkThreads = 64;
 // Lanes that share one chunk in the single-matrix walk (rows split between them, K1).  The n
@@ -78,6 +84,8 @@ constexpr int kConstMaxN = 45;
 __host__ __device__ constexpr bool walk_const_path(int n) {
 #if PERM_CONST_ORDERS == 0
     return n <= kConstMaxN;                               // scans only
+#elif defined(PERM_CONST_TABLE2)
+    return n == PERM_CONST_ORDERS || (n >= 33 && n <= 45);
 #else
     return n == PERM_CONST_ORDERS || n == 34 || n == 35 || n == 37 || n == 39 || (n >= 42 && n <= 45);
 #endif

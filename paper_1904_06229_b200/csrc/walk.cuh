@@ -564,6 +564,10 @@ __device__ __forceinline__ void walk_chunk_const(const WalkParamsC<C::N>& P, uin
 __host__ __device__ constexpr int walk_const_maxnreg(int n) {
 #ifdef PERM_CONST_MAXNREG_ALL
     return PERM_CONST_MAXNREG_ALL;                  // scans only (tools/const_ldcu_scan.sh)
+#elif defined(PERM_CONST_TABLE2)
+    return n == 33 ? 172 : n == 34 ? 200 : n == 35 ? 208 : n == 36 ? 212 : n == 37 ? 216 : n == 38 ? 220
+         : n == 39 ? 224 : n == 40 ? 228 : n == 41 ? 208 : n == 42 ? 208 : n == 43 ? 208 : n == 44 ? 248
+         : n == 45 ? 216 : 0;
 #else
     return n == 34 ? 200 : n == 35 ? 208 : n == 37 ? 216 : n == 39 ? 224 : n == 42 ? 208 : n == 43 ? 208
          : n == 44 ? 248 : n == 45 ? 216 : 0;
