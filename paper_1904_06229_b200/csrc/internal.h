@@ -72,7 +72,7 @@ struct Segment {
 };
 
 // Largest order whose whole matrix fits the 32 KB kernel-parameter space (walk_kernel_c).
-constexpr int kConstMaxN = 45;
+constexpr int kConstMaxN = 48;
 // Orders that use the constant-bank walk: the ones for which ptxas keeps the per-use parameter loads on
 // the uniform datapath (LDCU -> DADD R, R, UR, one vector register read per update) -- n = 32 at its
 // default allocation, 34, 35, 37, 39, 42..45 under the register caps of walk_const_maxnreg (walk.cuh).
@@ -85,7 +85,7 @@ __host__ __device__ constexpr bool walk_const_path(int n) {
 #if PERM_CONST_ORDERS == 0
     return n <= kConstMaxN;                               // scans only
 #elif defined(PERM_CONST_TABLE2)
-    return n == PERM_CONST_ORDERS || (n >= 33 && n <= 45);
+    return n == PERM_CONST_ORDERS || (n >= 33 && n <= 48);
 #else
     return n == PERM_CONST_ORDERS || n == 34 || n == 35 || n == 37 || n == 39 || (n >= 42 && n <= 45);
 #endif

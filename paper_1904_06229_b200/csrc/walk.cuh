@@ -567,7 +567,7 @@ __host__ __device__ constexpr int walk_const_maxnreg(int n) {
 #elif defined(PERM_CONST_TABLE2)
     return n == 33 ? 172 : n == 34 ? 200 : n == 35 ? 208 : n == 36 ? 212 : n == 37 ? 216 : n == 38 ? 220
          : n == 39 ? 224 : n == 40 ? 228 : n == 41 ? 208 : n == 42 ? 208 : n == 43 ? 208 : n == 44 ? 248
-         : n == 45 ? 216 : 0;
+         : n == 45 ? 216 : n == 46 ? 224 : n == 47 ? 228 : n == 48 ? 232 : 0;
 #else
     return n == 34 ? 200 : n == 35 ? 208 : n == 37 ? 216 : n == 39 ? 224 : n == 42 ? 208 : n == 43 ? 208
          : n == 44 ? 248 : n == 45 ? 216 : 0;
