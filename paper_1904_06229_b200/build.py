@@ -29,7 +29,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
                 f"-I{CSRC}", f"-I{os.path.join(ROOT, 'include')}", "-Xptxas", "-v"]
 
-HEADERS = ["common.cuh", "internal.h", "walk.cuh", "walk_pair.cuh", "sparse.cuh"]
+HEADERS = ["common.cuh", "internal.h", "walk.cuh", "walk_pair.cuh", "walk_table.cuh", "sparse.cuh"]
 
 
 def units():

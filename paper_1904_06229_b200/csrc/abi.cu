@@ -63,6 +63,7 @@ int choose_b(int n, uint64_t total, uint64_t T) {
     if (b < U) b = U;
     if (b > n - 1) b = n - 1;
     if (b > 30) b = 30;
+    if (perm::walk_table_path(n) && b > perm::walk_table_cols(n)) b = perm::walk_table_cols(n);
     if (b < 0) b = 0;
     // development override (profiling a sub-range at the full run's chunk length)
     if (const char* f = getenv("PERM_FORCE_CHUNK_LOG2")) {
@@ -163,6 +164,25 @@ perm_status_t plan_walk(int n, uint64_t k0, uint64_t k1, WalkPlan& p) {
         int best = -1;
         for (int s = 0; s < p.nseg; s++)
             if (p.seg[s].e > perm::walk_inner_bits(n) && (best < 0 || p.seg[s].count > p.seg[best].count)) best = s;
+        if (best >= 0 && perm::walk_table_path(n)) {
+            // the signed-table walk takes a body of 64k chunks (equal-parity warp passes); the remainder
+            // becomes its own segment for the edge launch
+            const uint64_t cnt = p.seg[best].count, c64 = cnt & ~63ull;
+            if (c64 == 0 || p.seg[best].e > perm::walk_table_cols(n)) {
+                best = -1;
+            } else if (c64 < cnt) {
+                if (p.nseg >= perm::kMaxSegments) {
+                    best = -1;
+                } else {
+                    for (int s = p.nseg; s > best + 1; s--) p.seg[s] = p.seg[s - 1];
+                    p.seg[best + 1].c0 = p.seg[best].c0 + c64;
+                    p.seg[best + 1].count = cnt - c64;
+                    p.seg[best + 1].e = p.seg[best].e;
+                    p.seg[best].count = c64;
+                    p.nseg++;
+                }
+            }
+        }
         if (best >= 0) {
             p.use_const = 1;
             p.body = best;

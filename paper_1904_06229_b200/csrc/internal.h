@@ -91,6 +91,31 @@ __host__ __device__ constexpr bool walk_const_path(int n) {
 #endif
 }
 
+// Signed-column-table walk (walk_table.cuh): every row-sum update takes its column from the kernel
+// parameters, columns j < walk_table_cols(n) with both signs and a zero column ((2 E + 1) n x 16 bytes <= 32 KB
+// for n <= 48).
+constexpr int kTableCols = 20;
+__host__ __device__ constexpr int walk_table_cols(int n) { return n < kTableCols ? n : kTableCols; }
+// PERM_TABLE_BSMEM: the block-boundary flip reads +-columns from shared memory instead (development)
+#ifndef PERM_TABLE_BSMEM
+#define PERM_TABLE_BSMEM 0
+#endif
+constexpr int kTableThreads = PERM_TABLE_BSMEM ? 128 : 64;
+// Off by default: measured slower than walk_kernel_c at n = 44 (5.83e10 vs 6.14e10 terms/s; DESIGN.md 5.1,
+// profiles/round1_walk_table_variants.txt).  PERM_TABLE_ORDERS=n enables it for order n (experiments).
+#ifndef PERM_TABLE_ORDERS
+#define PERM_TABLE_ORDERS -1
+#endif
+__host__ __device__ constexpr bool walk_table_path(int n) {
+#if PERM_TABLE_ORDERS == 0
+    return n >= 8 && n <= kConstMaxN;                     // scans only
+#elif PERM_TABLE_ORDERS < 0
+    return false;
+#else
+    return n == PERM_TABLE_ORDERS;
+#endif
+}
+
 // Warp-pair walk (walk_pair.cuh): each chunk's rows split between two warps, three 128-thread CTAs per SM.
 #ifndef PERM_WALK_PAIR
 #define PERM_WALK_PAIR 0
@@ -98,7 +123,7 @@ __host__ __device__ constexpr bool walk_const_path(int n) {
 __host__ __device__ constexpr bool walk_pair_path(int n) { return PERM_WALK_PAIR && n >= 40 && n <= 48; }
 // chunk walkers per block of the kernel that walks the aligned body (walk_kernel_c / walk_kernel_p)
 __host__ __device__ constexpr int walk_body_walkers(int n) {
-    return walk_pair_path(n) ? 64 : walk_block_threads(n);
+    return walk_table_path(n) ? kTableThreads : (walk_pair_path(n) ? 64 : walk_block_threads(n));
 }
 
 struct WalkLaunch {

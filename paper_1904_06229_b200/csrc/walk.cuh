@@ -469,10 +469,13 @@ __global__ void __launch_bounds__(WalkCfg<N>::NT, WalkCfg<N>::MINB) walk_kernel(
 // warp-uniform addresses, so the block loop counter is a 32-bit uniform value and each use of an
 // inner column gets its own opaque zero offset (z * (T+1), z = q >> 31 == 0): without it the
 // loop-invariant columns are hoisted into vector registers and the kernel spills.
+#ifndef PERM_CONST_MIDNEG
+#define PERM_CONST_MIDNEG 0
+#endif
 template <int N>
 struct WalkParamsC {
     static constexpr int NC = walk_inner_bits(N);   // columns held in the constant bank (the inner flips)
-    double2 col[NC][N];                    // col[j][i] = a_ij, j < U
+    double2 col[NC + PERM_CONST_MIDNEG][N];  // col[j][i] = a_ij, j < U (col[U][i] = -a_{i,U-1}: PERM_CONST_MIDNEG)
     const double2* A;                      // device, row-major (staged to shared memory)
     ddc* partials;                         // [gridDim.x]
     uint64_t c0;                           // first body chunk
@@ -492,12 +495,23 @@ struct InnerStepC {
             if constexpr (J == U - 1) {
                 // new bit = 1 ^ bit_U(rank): sign zmid = -+1 (the column is a uniform-register operand, so
                 // this DFMA reads only two vector registers)
+#if PERM_CONST_MIDNEG
+                // the column's sign by address (+a at col[U-1], -a at col[U]): DADD R, R, UR
+                const int jm = jj + (zmid < 0.0 ? 1 : 0);
+#pragma unroll
+                for (int i = 0; i < N; i++) {
+                    const double2 a = P.col[jm][i];
+                    wr[i] += a.x;
+                    wi[i] += a.y;
+                }
+#else
 #pragma unroll
                 for (int i = 0; i < N; i++) {
                     const double2 a = P.col[jj][i];
                     wr[i] = fma(zmid, a.x, wr[i]);
                     wi[i] = fma(zmid, a.y, wi[i]);
                 }
+#endif
             } else {
                 constexpr bool PLUS = ((T >> (J + 1)) & 1) == 0;  // new bit = 1 ^ bit_{J+1}(t)
 #pragma unroll
@@ -698,7 +712,23 @@ template <int N>
 cudaError_t walk_occupancy_pair(int* blocks_per_sm);
 
 template <int N>
+cudaError_t walk_launch_table(const WalkLaunch& L);
+template <int N>
+cudaError_t walk_occupancy_table(int* blocks_per_sm);
+
+template <int N>
 cudaError_t walk_launch(const WalkLaunch& L) {
+    if constexpr (walk_table_path(N)) {
+        if (L.use_const) {
+            cudaError_t err = walk_launch_table<N>(L);
+            if (err != cudaSuccess || L.grid_edge == 0) return err;
+            Segment rest[kMaxSegments];
+            int nr = 0;
+            for (int s = 0; s < L.nseg; s++)
+                if (s != L.body) rest[nr++] = L.seg[s];
+            return walk_launch_smem<N>(L, rest, nr, L.partials + L.grid, L.grid_edge);
+        }
+    }
     if constexpr (walk_pair_path(N)) {
         if (L.use_const) return walk_launch_pair<N>(L);
     }
@@ -708,6 +738,11 @@ cudaError_t walk_launch(const WalkLaunch& L) {
             WalkParamsC<N> P;
             for (int j = 0; j < WalkParamsC<N>::NC; j++)
                 for (int i = 0; i < N; i++) P.col[j][i] = L.A_host[(size_t)i * N + j];
+            if (PERM_CONST_MIDNEG)
+                for (int i = 0; i < N; i++) {
+                    const double2 a = L.A_host[(size_t)i * N + WalkParamsC<N>::NC - 1];
+                    P.col[WalkParamsC<N>::NC + PERM_CONST_MIDNEG - 1][i] = make_double2(-a.x, -a.y);
+                }
             P.A = L.A_dev;
             P.partials = L.partials;
             P.c0 = b.c0;
@@ -733,6 +768,7 @@ cudaError_t walk_launch(const WalkLaunch& L) {
 template <int N>
 cudaError_t walk_occupancy_c(int* blocks_per_sm) {
     *blocks_per_sm = 0;
+    if constexpr (walk_table_path(N)) return walk_occupancy_table<N>(blocks_per_sm);
     if constexpr (walk_pair_path(N)) return walk_occupancy_pair<N>(blocks_per_sm);
     if constexpr (walk_const_path(N) && walk_lanes_per_chunk(N) == 1 && walk_inner_bits(N) >= 1) {
         const void* k = walk_const_maxnreg(N) > 0 ? (const void*)walk_kernel_cm<N> : (const void*)walk_kernel_c<N>;

@@ -2,6 +2,7 @@
 // Compiled several times with -DPERM_PART=p (p = 0..7) so the 64 instantiations build in parallel;
 // part p instantiates N = 8p+1 .. 8p+8.
 #include "walk_pair.cuh"
+#include "walk_table.cuh"
 
 #ifndef PERM_PART
 #error "PERM_PART must be defined"
