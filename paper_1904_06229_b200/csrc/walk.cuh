@@ -469,13 +469,20 @@ __global__ void __launch_bounds__(WalkCfg<N>::NT, WalkCfg<N>::MINB) walk_kernel(
 // warp-uniform addresses, so the block loop counter is a 32-bit uniform value and each use of an
 // inner column gets its own opaque zero offset (z * (T+1), z = q >> 31 == 0): without it the
 // loop-invariant columns are hoisted into vector registers and the kernel spills.
+// Orders whose constant-bank walk takes the mid-block column with its sign by address (+a and -a both in
+// the parameters: DADD R, R, UR instead of fma(z, a, w), one vector register read fewer per update).
+// Bit-identical either way; n = 44: 6.16e10 vs 6.14e10 terms/s (profiles/round1_walk_table_variants.txt).
+// PERM_CONST_MIDNEG=1 enables it for every order (scans: the register caps of walk_const_maxnreg were
+// found without it).
 #ifndef PERM_CONST_MIDNEG
 #define PERM_CONST_MIDNEG 0
 #endif
+__host__ __device__ constexpr int walk_const_midneg(int n) { return (PERM_CONST_MIDNEG || n == 44) ? 1 : 0; }
 template <int N>
 struct WalkParamsC {
     static constexpr int NC = walk_inner_bits(N);   // columns held in the constant bank (the inner flips)
-    double2 col[NC + PERM_CONST_MIDNEG][N];  // col[j][i] = a_ij, j < U (col[U][i] = -a_{i,U-1}: PERM_CONST_MIDNEG)
+    static constexpr int MN = walk_const_midneg(N);
+    double2 col[NC + MN][N];               // col[j][i] = a_ij, j < U; col[U][i] = -a_{i,U-1} (MN = 1)
     const double2* A;                      // device, row-major (staged to shared memory)
     ddc* partials;                         // [gridDim.x]
     uint64_t c0;                           // first body chunk
@@ -493,25 +500,25 @@ struct InnerStepC {
             constexpr int J = ctz_c((unsigned)T);
             const int jj = J + z * (T + 1);          // == J; distinct expression per use (no CSE/hoist)
             if constexpr (J == U - 1) {
-                // new bit = 1 ^ bit_U(rank): sign zmid = -+1 (the column is a uniform-register operand, so
-                // this DFMA reads only two vector registers)
-#if PERM_CONST_MIDNEG
-                // the column's sign by address (+a at col[U-1], -a at col[U]): DADD R, R, UR
-                const int jm = jj + (zmid < 0.0 ? 1 : 0);
+                // new bit = 1 ^ bit_U(rank): sign zmid = -+1
+                if constexpr (WalkParamsC<N>::MN == 1) {
+                    // the column's sign by address (+a at col[U-1], -a at col[U]): DADD R, R, UR
+                    const int jm = jj + (zmid < 0.0 ? 1 : 0);
 #pragma unroll
-                for (int i = 0; i < N; i++) {
-                    const double2 a = P.col[jm][i];
-                    wr[i] += a.x;
-                    wi[i] += a.y;
-                }
-#else
+                    for (int i = 0; i < N; i++) {
+                        const double2 a = P.col[jm][i];
+                        wr[i] += a.x;
+                        wi[i] += a.y;
+                    }
+                } else {
+                    // the column is a uniform-register operand, so this DFMA reads two vector registers
 #pragma unroll
-                for (int i = 0; i < N; i++) {
-                    const double2 a = P.col[jj][i];
-                    wr[i] = fma(zmid, a.x, wr[i]);
-                    wi[i] = fma(zmid, a.y, wi[i]);
+                    for (int i = 0; i < N; i++) {
+                        const double2 a = P.col[jj][i];
+                        wr[i] = fma(zmid, a.x, wr[i]);
+                        wi[i] = fma(zmid, a.y, wi[i]);
+                    }
                 }
-#endif
             } else {
                 constexpr bool PLUS = ((T >> (J + 1)) & 1) == 0;  // new bit = 1 ^ bit_{J+1}(t)
 #pragma unroll
@@ -738,10 +745,10 @@ cudaError_t walk_launch(const WalkLaunch& L) {
             WalkParamsC<N> P;
             for (int j = 0; j < WalkParamsC<N>::NC; j++)
                 for (int i = 0; i < N; i++) P.col[j][i] = L.A_host[(size_t)i * N + j];
-            if (PERM_CONST_MIDNEG)
+            if constexpr (WalkParamsC<N>::MN == 1)
                 for (int i = 0; i < N; i++) {
                     const double2 a = L.A_host[(size_t)i * N + WalkParamsC<N>::NC - 1];
-                    P.col[WalkParamsC<N>::NC + PERM_CONST_MIDNEG - 1][i] = make_double2(-a.x, -a.y);
+                    P.col[WalkParamsC<N>::NC][i] = make_double2(-a.x, -a.y);
                 }
             P.A = L.A_dev;
             P.partials = L.partials;
