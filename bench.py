@@ -285,8 +285,15 @@ def run_ours(args):
     world, rank, local = dist_env()
     if world > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # PERM_BENCH_DIST_BACKEND=gloo is a functional test hook only (several ranks sharing the box's one
+        # GPU, results checked, timings meaningless); the measured multi-GPU path is NCCL, one rank per GPU.
+        backend = os.environ.get("PERM_BENCH_DIST_BACKEND", "nccl")
+        dev = local % torch.cuda.device_count() if backend != "nccl" else local
+        torch.cuda.set_device(dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
     else:
         torch.cuda.set_device(0)
     device = torch.device("cuda", torch.cuda.current_device())

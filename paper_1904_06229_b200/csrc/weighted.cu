@@ -10,25 +10,34 @@
 // signed-sum step as the Gray walk of walk.cuh, with the weight prod_k C(m_k, f_k) as an extra real
 // factor (an exact integer < 2^n, exact in binary64 for n <= 32).
 //
-// Mapping: one warp per problem, persistent (each warp takes the next problem from an atomic counter).  The digit with the largest multiplicity, s, is the fastest digit:
-// every "sweep" runs f_s through 0..m_s (even sweeps) or m_s..0 (odd sweeps) while the other digits,
-// numbered in input order, follow the reflected Gray code of the sweep index q.  Lane l takes the
-// contiguous sweeps [distribute(NS, 32, l)) (App. A distribute) and seeds its row sums,
-// digits and weight explicitly from q (the "chunk seeding" of the walk), so all lanes step f_s in
-// lock-step and read the same column (+cbar_s or -cbar_s: both are staged in shared memory, the
-// address picks the sign).  Between sweeps each lane changes one outer digit (lane-dependent column,
-// fma with the direction).
-// Each lane sums its terms in double per sweep and folds them into a double-double; the 32 lane
+// Mapping: one warp per problem, persistent (each warp takes the next problem from an atomic counter).  The
+// two digits with the largest multiplicities, s and s2, are the fastest digits: a "tile" walks their
+// (m_s + 1)(m_s2 + 1) values at fixed outer digits -- f_s sweeps 0..m_s or back, f_s2 steps by one, f_s
+// sweeps back, ... -- while the other digits, numbered in input order, follow the reflected Gray code of
+// the tile index q.  Lane l takes the contiguous tiles [distribute(NT, 32, l)) (App. A distribute,
+// P:1086-1093) and seeds its row sums, digits and weight explicitly from q (the "chunk seeding" of the
+// walk), so all lanes step f_s and f_s2 in lock-step and read the same column (+-cbar_s, +-cbar_s2: all
+// four are staged in shared memory, the address picks the sign).  Between tiles each lane changes one
+// outer digit (lane-dependent column, fma with the direction) and its binomial weight.  Tiles amortise
+// that per-tile work (successor search, exact weight update, double-double fold) over ~4x more terms
+// than one-digit sweeps.
+// Each lane sums its terms in double per tile and folds them into a double-double; the 32 lane
 // partials are combined by a fixed shuffle tree; lane 0 applies (-1)^n and writes per and |per|^2.
 #include "walk.cuh"
 
 namespace perm {
 
+// unroll factor of the sweep loop (1: rolled)
+#ifndef PERM_WGT_UNROLL
+#define PERM_WGT_UNROLL 1
+#endif
+constexpr int kWgtUnroll = PERM_WGT_UNROLL;
+
 template <int N>
 struct WgtCfg {
     static constexpr int NT = 32;                    // one warp (one problem at a time) per block
 #ifndef PERM_WGT_REG_EXTRA
-#define PERM_WGT_REG_EXTRA 64
+#define PERM_WGT_REG_EXTRA 96
 #endif
     static constexpr int REGS = ((4 * N + PERM_WGT_REG_EXTRA + 7) / 8) * 8;
     static constexpr int MINB_RAW = 65536 / (NT * (REGS < 255 ? REGS : 255));
@@ -44,10 +53,10 @@ __device__ __forceinline__ double binom_d(int m, int f) {
 
 // Shared-memory slot (bytes) of one warp for R distinct columns of order N.
 __host__ __device__ constexpr size_t wgt_slot_bytes(int N, int R) {
-    // cbar (R N double2) and -cbar_s of the sweep digit (N double2), binomial row of each digit
-    // (R (N+1) doubles), the sweep table (N+1 doubles), radices / multiplicities / digit order (3 R ints),
-    // the lanes' outer digits and directions (2 R x 32 bytes)
-    return ((size_t)(R + 1) * N * 16 + (size_t)(R + 1) * (N + 1) * 8 + (size_t)3 * R * 4 + (size_t)2 * R * 32 + 15) &
+    // cbar (R N double2) and -cbar of the two sweep digits (2 N double2), binomial row of each digit
+    // (R (N+1) doubles), the two sweep tables (2 (N+1) doubles), radices / multiplicities / digit order
+    // (3 R ints), the lanes' outer digits and directions (2 R x 32 bytes)
+    return ((size_t)(R + 2) * N * 16 + (size_t)(R + 2) * (N + 1) * 8 + (size_t)3 * R * 4 + (size_t)2 * R * 32 + 15) &
            ~(size_t)15;
 }
 
@@ -58,16 +67,19 @@ __global__ void __launch_bounds__(WgtCfg<N>::NT, WgtCfg<N>::MINB)
     extern __shared__ __align__(16) unsigned char wsm[];
     const int lane = threadIdx.x & 31;
     double2* col = (double2*)wsm;                                         // col[k*N + i] = cbar_i(k)
-    double2* negs = col + (size_t)R * N;                                  // -cbar_s (sweep digit)
-    double* bin = (double*)(wsm + (size_t)(R + 1) * N * 16);              // bin[k*(N+1) + f] = C(m_k, f)
+    double2* negs = col + (size_t)R * N;                                  // -cbar_s (fast sweep digit)
+    double2* negs2 = negs + N;                                            // -cbar_s2 (second sweep digit)
+    double* bin = (double*)(wsm + (size_t)(R + 2) * N * 16);              // bin[k*(N+1) + f] = C(m_k, f)
     double* tsw = bin + (size_t)R * (N + 1);                              // tsw[j] = (-1)^j C(m_s, j)
-    int* order = (int*)(tsw + (N + 1));                                   // order[0] = s, then the outer digits
+    double* tsw2 = tsw + (N + 1);                                         // tsw2[j] = (-1)^j C(m_s2, j)
+    int* order = (int*)(tsw2 + (N + 1));                                  // order[0] = s, then the outer digits
     int* rad = order + R;                                                 // rad[p] = m_{order[p]} + 1
     int* mlt = rad + R;                                                   // mlt[p] = m_{order[p]}
     unsigned char* gdig = (unsigned char*)(mlt + R);                      // gdig[p*32 + lane]: outer digit p
     signed char* gdir = (signed char*)(gdig + R * 32);                    // its direction (+-1)
     const uint32_t base = (uint32_t)__cvta_generic_to_shared(col);
     const uint32_t nbase = (uint32_t)__cvta_generic_to_shared(negs);
+    const uint32_t nbase2 = (uint32_t)__cvta_generic_to_shared(negs2);
 
     for (;;) {                                                            // persistent: a shared work queue
         __syncwarp();
@@ -83,6 +95,10 @@ __global__ void __launch_bounds__(WgtCfg<N>::NT, WgtCfg<N>::MINB)
             mbad |= (m < 0) | (m > N);
             if (m > ms) { ms = m; s = k; }
         }
+        // the second sweep digit: the largest other multiplicity >= 1 (none: m_s2 = 0, a one-row tile)
+        int s2 = -1, ms2 = 0;
+        for (int k = 0; k < R; k++)
+            if (k != s && mb[k] > ms2) { ms2 = mb[k]; s2 = k; }
         // stage the columns, column-major, and the negated sweep column
         const double2* src = C + b * (int64_t)N * R;
         for (int k = lane; k < N * R; k += 32) {
@@ -90,6 +106,7 @@ __global__ void __launch_bounds__(WgtCfg<N>::NT, WgtCfg<N>::MINB)
             const double2 a = src[k];
             col[j * N + i] = a;
             if (j == s) negs[i] = make_double2(-a.x, -a.y);
+            if (j == s2) negs2[i] = make_double2(-a.x, -a.y);
         }
         if (msum != N || mbad) {                                          // not a valid multiplicity vector
             if (lane == 0) {
@@ -105,37 +122,45 @@ __global__ void __launch_bounds__(WgtCfg<N>::NT, WgtCfg<N>::MINB)
             bin[k] = (f <= m) ? binom_d(m, f) : 0.0;
         }
         for (int j = lane; j <= ms; j += 32) tsw[j] = (j & 1) ? -binom_d(ms, j) : binom_d(ms, j);
+        for (int j = lane; j <= ms2; j += 32) tsw2[j] = (j & 1) ? -binom_d(ms2, j) : binom_d(ms2, j);
         int P = 0;                                                        // outer digits with m_k > 0
         if (lane == 0) {
             order[0] = s;
             rad[0] = ms + 1;
             mlt[0] = ms;
             for (int k = 0; k < R; k++)
-                if (k != s && mb[k] > 0) { order[1 + P] = k; rad[1 + P] = mb[k] + 1; mlt[1 + P] = mb[k]; P++; }
+                if (k != s && k != s2 && mb[k] > 0) { order[1 + P] = k; rad[1 + P] = mb[k] + 1; mlt[1 + P] = mb[k]; P++; }
         }
         __syncwarp();
         P = __shfl_sync(0xffffffffu, P, 0);
 
-        // sweeps: NS = prod of the outer radices (<= 2^31 for N <= 32); lane l takes [q0, q0 + nq)
+        // tiles: NS = prod of the outer radices (<= 2^31 for N <= 32); lane l takes [q0, q0 + nq).  A tile is
+        // the (m_s + 1)(m_s2 + 1) terms of the two sweep digits at fixed outer digits, walked as the two
+        // fastest digits of the reflected mixed-radix Gray code: f_s sweeps, f_s2 steps, f_s reverses ...
         uint32_t NS = 1;
         for (int p = 1; p <= P; p++) NS *= (uint32_t)rad[p];
         const uint32_t qb = NS / 32u, qr = NS % 32u;
         const uint32_t q0 = (uint32_t)lane * qb + ((uint32_t)lane < qr ? (uint32_t)lane : qr);
         const uint32_t nq = qb + ((uint32_t)lane < qr ? 1u : 0u);
         const uint32_t cs = base + (uint32_t)(s * N) * 16u;               // +cbar_s
+        const uint32_t cs2 = base + (uint32_t)((s2 < 0 ? s : s2) * N) * 16u;   // +cbar_s2 (unused if none)
 
         ddc acc;
         acc.re.hi = acc.re.lo = acc.im.hi = acc.im.lo = 0.0;
         if (nq > 0) {
-            // seed at sweep q0 (reflected mixed-radix Gray code, the sweep digit fastest): outer digit p
-            // has ordinary value t_p and runs forward iff the number formed by the digits above it is
-            // even; its Gray value is t_p forward, r_p - 1 - t_p backward.  f_s = 0 (q0 even) or m_s.
+            // seed at tile q0: f_s has completed q0 (m_s2 + 1) sweeps and f_s2 q0 sweeps (each runs forward
+            // iff that count is even); outer digit p has ordinary value t_p and runs forward iff the number
+            // formed by the digits above it is even; its Gray value is t_p forward, r_p - 1 - t_p backward
             double wr[N], wi[N];
-            int fsum = (q0 & 1u) ? ms : 0;
+            bool fwd1 = ((q0 * (uint32_t)(ms2 + 1)) & 1u) == 0;
+            bool fwd2 = (q0 & 1u) == 0;
+            int f1 = fwd1 ? 0 : ms, f2 = fwd2 ? 0 : ms2;
+            int fsum = 0;
             double wout = 1.0;
 #pragma unroll
             for (int i = 0; i < N; i++) { wr[i] = 0.0; wi[i] = 0.0; }
-            flip_dyn<N>(cs, (q0 & 1u) ? (double)ms : 0.0, wr, wi);
+            flip_dyn<N>(cs, (double)f1, wr, wi);
+            flip_dyn<N>(cs2, (double)f2, wr, wi);
             {
                 uint32_t x = q0;
                 for (int p = 1; p <= P; p++) {
@@ -151,27 +176,40 @@ __global__ void __launch_bounds__(WgtCfg<N>::NT, WgtCfg<N>::MINB)
                     x = up;
                 }
             }
-            // (-1)^{|f|} at the sweep start; along a sweep f_s moves m_s times (the weights
-            // (-1)^j C(m_s, f_s) are the same sequence tsw[j] forwards and backwards)
+            // outer factor (-1)^{sum of outer digits} prod C(m_p, g_p); each term multiplies in
+            // tsw2[f2] tsw[f1] = (-1)^{f1 + f2} C(m_s, f1) C(m_s2, f2)   (all exact integers < 2^n)
             double scale = (fsum & 1) ? -wout : wout;
-            const double flip_after = (ms & 1) ? 1.0 : -1.0;              // (-1)^{m_s + 1}
             for (uint32_t q = q0;; q++) {
-                const uint32_t step = (q & 1u) ? nbase : cs;
                 double ar = 0.0, ai = 0.0;
-                for (int j = 0; j <= ms; j++) {
-                    const double wt = scale * tsw[j];                     // exact: +-integer < 2^n
-                    double xr, xi, yr, yi;
-                    two_factors<N, (N >= 4 ? 2 : 1)>(wr, wi, xr, xi, yr, yi);
-                    if constexpr (N == 1) { yr = 1.0; yi = 0.0; }
-                    xr *= wt;
-                    xi *= wt;
-                    fused_acc<+1>(xr, xi, yr, yi, ar, ai);
-                    if (j < ms) flip_add<N>(step, wr, wi);
+                for (int r = 0; r <= ms2; r++) {
+                    const double sc2 = scale * tsw2[f2];
+                    const uint32_t step = fwd1 ? cs : nbase;
+                    const int d1 = fwd1 ? 1 : -1;
+#pragma unroll (kWgtUnroll)
+                    for (int j = 0; j <= ms; j++) {
+                        const double wt = sc2 * tsw[f1];
+                        double xr, xi, yr, yi;
+                        two_factors<N, (N >= 4 ? 2 : 1)>(wr, wi, xr, xi, yr, yi);
+                        if constexpr (N == 1) { yr = 1.0; yi = 0.0; }
+                        xr *= wt;
+                        xi *= wt;
+                        fused_acc<+1>(xr, xi, yr, yi, ar, ai);
+                        if (j < ms) {
+                            flip_add<N>(step, wr, wi);
+                            f1 += d1;
+                        }
+                    }
+                    fwd1 = !fwd1;
+                    if (r < ms2) {
+                        flip_add<N>(fwd2 ? cs2 : nbase2, wr, wi);
+                        f2 += fwd2 ? 1 : -1;
+                    }
                 }
+                fwd2 = !fwd2;
                 acc.re = dd_add_d(acc.re, ar);
                 acc.im = dd_add_d(acc.im, ai);
                 if (q + 1 >= q0 + nq) break;
-                // next sweep: the lowest outer digit that can move in its direction moves; the digits
+                // next tile: the lowest outer digit that can move in its direction moves; the digits
                 // below it (at an end) reverse direction -- the reflected Gray successor of q
                 int p = 1;
                 int g = 0, d = 0;
@@ -185,9 +223,8 @@ __global__ void __launch_bounds__(WgtCfg<N>::NT, WgtCfg<N>::MINB)
                 gdig[(p - 1) * 32 + lane] = (unsigned char)(g + d);
                 const double* bk = bin + order[p] * (N + 1);
                 wout = __dmul_rn(__ddiv_rn(wout, bk[g]), bk[g + d]);      // exact: integer quotient
-                flip_dyn<N>(base + (uint32_t)(order[p] * N) * 16u, (double)d, wr, wi);   // once per sweep
-                const double sg = scale < 0.0 ? -1.0 : 1.0;
-                scale = sg * flip_after * wout;
+                flip_dyn<N>(base + (uint32_t)(order[p] * N) * 16u, (double)d, wr, wi);   // once per tile
+                scale = scale < 0.0 ? wout : -wout;                       // one outer digit moved by +-1
             }
         }
 #pragma unroll
