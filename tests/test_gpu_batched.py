@@ -49,6 +49,25 @@ def test_larger_orders(torch, n):
     _check_batch(torch, A, ref)
 
 
+@pytest.mark.parametrize("n", [28, 32])
+def test_max_orders_block_diagonal(torch, n):
+    # up to the kernel's largest order (32): P (B1 + B2) Q (direct sum, scrambled rows and columns) has
+    # per = per(B1) per(B2), each block's permanent from the oracle's Eq. (3)
+    h = n // 2
+    rng = np.random.default_rng(900 + n)
+    A = np.zeros((2, n, n), dtype=np.complex128)
+    ref = []
+    for b in range(2):
+        B1 = inputs.complex_gaussian((h, h), 910 + n + b)
+        B2 = inputs.complex_gaussian((n - h, n - h), 930 + n + b)
+        M = np.zeros((n, n), dtype=np.complex128)
+        M[:h, :h] = B1
+        M[h:, h:] = B2
+        A[b] = M[rng.permutation(n)][:, rng.permutation(n)]
+        ref.append(oracle.ryser(B1).value * oracle.ryser(B2).value)
+    _check_batch(torch, A, np.array(ref))
+
+
 def test_empty_batch_and_errors(torch):
     A = torch.zeros((0, 8, 8), dtype=torch.complex128, device="cuda")
     per, abs2 = pb.perm_c128_batched(A)

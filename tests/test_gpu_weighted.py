@@ -74,7 +74,7 @@ def test_single_column_factorial(torch):
     # R = 1: n copies of one column, per = n! prod_i c_i.  For the all-ones column every term
     # (-1)^f C(n,f) f^n is an integer; up to n = 13 they are below 2^53, the double sum is exact and so
     # is per = n!; beyond, the terms (~n^n) cancel down to n! and the error is bounded by REL * sum|term|
-    for n in (1, 5, 13, 20):
+    for n in (1, 5, 13, 20, 32):
         C = np.ones((1, n, 1), dtype=np.complex128)
         per, _ = _run(torch, C, np.array([[n]], dtype=np.int32))
         if n <= 13:
@@ -82,6 +82,20 @@ def test_single_column_factorial(torch):
         else:
             asum = sum(math.comb(n, f) * f ** n for f in range(n + 1))
             assert abs(per[0] - math.factorial(n)) <= REL * asum
+
+
+def test_max_order_vs_oracle(torch):
+    # the largest order (n = 32): 8 distinct columns four times each (5^8 terms, two-digit tiles of 25),
+    # and a ragged vector over 6 columns whose second sweep digit is small
+    n = 32
+    C = inputs.complex_gaussian((2, n, 8), 932)
+    mult = np.array([[4] * 8, [9, 7, 6, 5, 3, 2, 0, 0]], dtype=np.int32)
+    assert np.all(mult.sum(axis=1) == n)
+    per, _ = _run(torch, C, mult)
+    for b in range(2):
+        R = int(np.count_nonzero(mult[b]))
+        ref, asum = oracle.ryser_weighted(C[b][:, :R], mult[b][:R])
+        assert abs(per[b] - ref.value) <= REL * asum + 1e-300, (b, per[b], ref.value, asum)
 
 
 def test_collision_patterns_vs_oracle(torch):
