@@ -32,6 +32,12 @@ namespace perm {
 #define PERM_WGT_UNROLL 1
 #endif
 constexpr int kWgtUnroll = PERM_WGT_UNROLL;
+// independent product chains per term (walk.cuh two_factors)
+#ifndef PERM_WGT_K4_MIN
+#define PERM_WGT_K4_MIN 99
+#endif
+template <int N>
+constexpr int kWgtChains = N >= PERM_WGT_K4_MIN ? 4 : (N >= 4 ? 2 : 1);
 
 template <int N>
 struct WgtCfg {
@@ -189,7 +195,7 @@ __global__ void __launch_bounds__(WgtCfg<N>::NT, WgtCfg<N>::MINB)
                     for (int j = 0; j <= ms; j++) {
                         const double wt = sc2 * tsw[f1];
                         double xr, xi, yr, yi;
-                        two_factors<N, (N >= 4 ? 2 : 1)>(wr, wi, xr, xi, yr, yi);
+                        two_factors<N, kWgtChains<N>>(wr, wi, xr, xi, yr, yi);
                         if constexpr (N == 1) { yr = 1.0; yi = 0.0; }
                         xr *= wt;
                         xi *= wt;
