@@ -34,7 +34,7 @@ RANGES = {
     32: [(0, 1 << 20), ((1 << 30) - (1 << 19), (1 << 30) + (1 << 19)),
          ((1 << 31) - (1 << 20), 1 << 31), (777777777, 777777777 + 1000003)],
 }
-CFG2_SAMPLES = {8: 2000, 12: 400, 16: 64, 20: 16}
+CFG2_SAMPLES = {8: 2000, 12: 400, 16: 256, 20: 64}
 BLOCK_SEEDS = (4401, 4402, 4403)          # B1 seed, B2 seed, permutation seed
 
 

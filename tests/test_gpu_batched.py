@@ -101,6 +101,21 @@ def test_boson_sampling_normalization(torch, m, n):
     assert abs(total - 1.0) < 1e-12, total
 
 
+@pytest.mark.parametrize("n,count", [(8, 100000), (12, 10000)])
+def test_cfg2_full_batch_every_output(torch, n, count):
+    """Config 2 at full size (the bench launch, 10^5 submatrices): every output for n = 8 and a seeded
+    10^4 subset for n = 12 against the oracle's Eq. (3), computed here (SURVEY 8(c) parity plan)."""
+    A = inputs.cfg2(n)
+    per, _ = pb.perm_c128_batched(torch.from_numpy(A).cuda())
+    per = per.cpu().numpy()
+    idx = np.arange(A.shape[0]) if count >= A.shape[0] else \
+        np.sort(np.random.default_rng(9100 + n).choice(A.shape[0], count, replace=False))
+    ref = oracle.ryser_batch(np.ascontiguousarray(A[idx]))
+    floor = 2.0 ** (-n / 2) * np.prod(np.linalg.norm(A[idx], axis=2), axis=1)
+    err = np.abs(per[idx] - ref) / np.maximum(np.abs(ref), floor)
+    assert err.max() <= TOL, (n, int(idx[np.argmax(err)]), err.max())
+
+
 @pytest.mark.parametrize("n", [8, 12, 16, 20])
 def test_cfg2_full_batch_samples(torch, golden_dir, n):
     """Config 2 at full size (10^5 submatrices, the bench launch): sampled outputs vs the oracle,
