@@ -206,6 +206,27 @@ perm_status_t perm_int01(const uint8_t* A_dev, int n, int64_t B, perm_i128_t* ou
 perm_status_t perm_pm1(const int8_t* A_dev, int n, int64_t B, perm_i128_t* out_dev,
                        void* workspace, size_t workspace_bytes, void* stream);
 
+/* Sharding ONE exact 0-1 permanent (App. A partition): the
+ * raw signed integer Gray sum over the ranks [k_begin, k_end) of the walk perm_int01 runs,
+ *     n <= 28:       P = sum_{r} (-1)^{r+1} prod_i g_i(gray r)   (half range, ranks < 2^{n-1})
+ *     29 <= n <= 33: P = sum_{r} (-1)^{|gray r|} prod_i r_i(gray r)   (Eq. (3), ranks < 2^n)
+ * modulo 2^128 (the exact value's two's-complement bits).  Partials of disjoint spans add exactly (mod
+ * 2^128, in any order); perm_int01_finalize turns their sum into per(A).
+ *   A_dev     device, n*n bytes, each 0 or 1, row-major.
+ *   partial   host, one perm_i128_t (raw bits mod 2^128).
+ * Synchronizes `stream`.  Workspace is allocated internally (stream-ordered).
+ * Errors: PERM_E_ARG (null pointer, k_begin > k_end), PERM_E_ORDER (n outside 1..33, k_end beyond the
+ *         rank space), PERM_E_NOT01, PERM_E_CUDA.  k_begin == k_end gives 0. */
+perm_status_t perm_int01_range(const uint8_t* A_dev, int n, uint64_t k_begin, uint64_t k_end,
+                               perm_i128_t* partial, void* stream);
+
+/* per(A) from the partials of spans covering the whole rank space exactly once (host only): their sum
+ * mod 2^128 is Sum; n <= 28: per = (-1)^n Sum / 2^{n-1} after checking the low n-1 bits are zero
+ * (PERM_E_CHECK otherwise); 29 <= n <= 33: per = (-1)^{n+1} Sum.
+ *   partials  host, count perm_i128_t;  out  host, one perm_i128_t.
+ * Errors: PERM_E_ARG (null pointer, count < 0), PERM_E_ORDER, PERM_E_CHECK. */
+perm_status_t perm_int01_finalize(const perm_i128_t* partials, int count, int n, perm_i128_t* out);
+
 /* ------------------------------------------------------------------------------------------
  * Diagnostics.
  * ------------------------------------------------------------------------------------------ */

@@ -126,6 +126,8 @@ def lib() -> ctypes.CDLL:
         "perm_int01_workspace_bytes": [i32, i64, ctypes.POINTER(sz)],
         "perm_int01": [P, i32, i64, P, P, sz, P],
         "perm_pm1": [P, i32, i64, P, P, sz, P],
+        "perm_int01_range": [P, i32, u64, u64, P, P],
+        "perm_int01_finalize": [P, i32, i32, P],
         "perm_c128_seed": [P, i32, P, i32, P, P],
         "perm_fp64_probe": [i32, i32, i32, P, P],
     }
@@ -442,6 +444,37 @@ def perm_pm1(A, *, workspace=None, out=None, stream=None, as_int: bool = True):
     return [(int(hi) << 64) + (int(lo) & ((1 << 64) - 1)) for lo, hi in raw]
 
 
+def perm_int01_range(A, k_begin: int, k_end: int, *, stream=None) -> int:
+    """Raw exact Gray sum of ONE 0-1 matrix (an (n, n) or (1, n, n) uint8 CUDA tensor) over the ranks
+    [k_begin, k_end) of perm_int01's walk, as a Python int in [0, 2^128) (two's-complement bits mod
+    2^128) -- the unit of sharding one exact permanent across GPUs (perm.h).  Synchronizes."""
+    torch = _torch()
+    if not (_is_torch(A) and A.is_cuda and A.dtype == torch.uint8):
+        raise ValueError("perm_int01_range expects a CUDA uint8 tensor (n, n)")
+    A = A.contiguous()
+    n = A.shape[-1]
+    if A.numel() != n * n:
+        raise ValueError("perm_int01_range takes one square matrix")
+    out = i128()
+    _check(lib().perm_int01_range(ctypes.c_void_p(A.data_ptr()), n, int(k_begin), int(k_end), ctypes.byref(out),
+                                  _stream_ptr(stream)))
+    return ((int(out.hi) << 64) + int(out.lo)) & ((1 << 128) - 1)
+
+
+def perm_int01_finalize(partials, n: int) -> int:
+    """per(A) from the raw partials (ints mod 2^128) of spans covering the rank space exactly once."""
+    parts = list(partials)
+    arr = (i128 * max(1, len(parts)))()
+    for k, v in enumerate(parts):
+        v = int(v) & ((1 << 128) - 1)
+        arr[k].lo = v & ((1 << 64) - 1)
+        hi = v >> 64
+        arr[k].hi = hi - (1 << 64) if hi >= (1 << 63) else hi
+    out = i128()
+    _check(lib().perm_int01_finalize(arr, len(parts), n, ctypes.byref(out)))
+    return (int(out.hi) << 64) + int(out.lo)
+
+
 def perm_c128_seed(A, ranks) -> np.ndarray:
     """w(r) (App. A steps 2, 5-8) computed by the device seeding code, for each rank r -> (count, n)."""
     ptr, n, keep = _matrix_ptr(A)
@@ -459,7 +492,7 @@ def perm_fp64_probe(blocks: int, threads: int, iters: int, sink, stream=None):
 
 
 __all__ = ["perm_c128", "perm_c128_range", "perm_c128_finalize", "perm_c128_batched", "perm_c128_weighted_batched",
-           "perm_int01", "perm_pm1", "perm_c128_sparse", "perm_sparse_plan",
+           "perm_int01", "perm_pm1", "perm_int01_range", "perm_int01_finalize", "perm_c128_sparse", "perm_sparse_plan",
            "perm_c128_band_batched", "band_storage",
            "perm_c128_seed", "perm_fp64_probe", "workspace_bytes", "make_workspace", "int01_workspace_bytes",
            "PermError", "DD", "lib", "header_functions", "last_launches"]

@@ -670,6 +670,52 @@ perm_status_t perm_pm1(const int8_t* A_dev, int n, int64_t B, perm_i128_t* out_d
     return run_int((const uint8_t*)A_dev, true, n, B, out_dev, workspace, workspace_bytes, stream);
 }
 
+perm_status_t perm_int01_range(const uint8_t* A_dev, int n, uint64_t k_begin, uint64_t k_end, perm_i128_t* partial,
+                               void* stream) {
+    g_launches = 0;
+    if (!A_dev || !partial || k_begin > k_end) return PERM_E_ARG;
+    if (n < 1 || n > perm::kMaxInt01N) return PERM_E_ORDER;
+    const int bits = n > perm::kMaxGlynnInt01N ? n : n - 1;     // rank space of the walk
+    if (k_end > (1ull << bits)) return PERM_E_ORDER;
+    partial->lo = 0;
+    partial->hi = 0;
+    if (k_begin == k_end) return PERM_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    char* ws = nullptr;
+    PERM_CUDA(cudaMallocAsync((void**)&ws, perm::int01_range_workspace_bytes(), s), "cudaMallocAsync(workspace)");
+    unsigned long long raw[2] = {0, 0};
+    int flag = 0, l = 0;
+    const cudaError_t e = perm::int01_range_launch(A_dev, n, k_begin, k_end, ws, s, raw, &flag, &l);
+    cudaFreeAsync(ws, s);
+    if (e != cudaSuccess) return cuda_fail(e, "int01 range kernel");
+    if (flag & 1) return PERM_E_NOT01;
+    partial->lo = raw[0];
+    partial->hi = (int64_t)raw[1];
+    g_launches = (uint32_t)l;
+    return PERM_OK;
+}
+
+perm_status_t perm_int01_finalize(const perm_i128_t* partials, int count, int n, perm_i128_t* out) {
+    if (!out || count < 0 || (count > 0 && !partials)) return PERM_E_ARG;
+    if (n < 1 || n > perm::kMaxInt01N) return PERM_E_ORDER;
+    unsigned __int128 sum = 0;                                  // mod 2^128: exact, order-free
+    for (int k = 0; k < count; k++)
+        sum += ((unsigned __int128)(uint64_t)partials[k].hi << 64) | (unsigned __int128)partials[k].lo;
+    __int128 v;
+    if (n > perm::kMaxGlynnInt01N) {                            // full-range Ryser: per = (-1)^{n+1} Sum
+        v = (__int128)sum;
+        if (!(n & 1)) v = -v;
+    } else {
+        const unsigned __int128 mask = (((unsigned __int128)1) << (n - 1)) - 1;
+        if (sum & mask) return PERM_E_CHECK;
+        v = (__int128)sum >> (n - 1);                           // Sum / 2^{n-1}
+        if (n & 1) v = -v;                                      // per = (-1)^n Sum / 2^{n-1}
+    }
+    out->lo = (uint64_t)v;
+    out->hi = (int64_t)((unsigned __int128)v >> 64);
+    return PERM_OK;
+}
+
 perm_status_t perm_c128_seed(const perm_c128_t* A, int n, const uint64_t* ranks, int count, perm_c128_t* w_out,
                              void* stream) {
     g_launches = 0;

@@ -180,7 +180,7 @@ __device__ __forceinline__ void int_chunk(uint32_t sc, uint32_t sbase, uint64_t 
 template <int N, bool PM1>
 __global__ void __launch_bounds__(I01Cfg<N>::NT) int01_kernel(const uint8_t* __restrict__ A, int e,
                                                               uint64_t chunks, u128* __restrict__ partials,
-                                                              int* __restrict__ flag) {
+                                                              int* __restrict__ flag, uint64_t c0, int accum) {
     constexpr int NP = I01Cfg<N>::NP;
     constexpr bool FULL = I01Cfg<N>::FULL;
     constexpr int CM = FULL ? 1 : 2;               // column increment: 2 a_ij (Glynn) or a_ij (Ryser)
@@ -208,7 +208,7 @@ __global__ void __launch_bounds__(I01Cfg<N>::NT) int01_kernel(const uint8_t* __r
     u128 acc = 0;
     const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; c < chunks; c += T)
-        int_chunk<N>(sc, sbase, c, e, acc);
+        int_chunk<N>(sc, sbase, c0 + c, e, acc);       // chunk c0 + c: ranks [(c0+c) 2^e, (c0+c+1) 2^e)
     // block reduction (exact; order irrelevant)
     unsigned long long lo = (unsigned long long)acc, hi = (unsigned long long)(acc >> 64);
 #pragma unroll
@@ -225,7 +225,8 @@ __global__ void __launch_bounds__(I01Cfg<N>::NT) int01_kernel(const uint8_t* __r
     if (threadIdx.x == 0) {
         u128 t = 0;
         for (int w = 0; w < I01Cfg<N>::NT / 32; w++) t += s_w[w];
-        partials[m * gridDim.x + blockIdx.x] = t;
+        u128* slot = partials + m * gridDim.x + blockIdx.x;
+        *slot = accum ? *slot + t : t;                  // accum: later segments of a range add in (exact)
     }
 }
 
@@ -285,8 +286,8 @@ template <int N>
 cudaError_t int01_launch_t(const uint8_t* A, int64_t B, const I01Plan& p, u128* partials, int* flag, bool pm1,
                            cudaStream_t s) {
     dim3 grid((unsigned)p.nblk, (unsigned)B);
-    if (pm1) int01_kernel<N, true><<<grid, I01Cfg<N>::NT, 0, s>>>(A, p.e, p.chunks, partials, flag);
-    else     int01_kernel<N, false><<<grid, I01Cfg<N>::NT, 0, s>>>(A, p.e, p.chunks, partials, flag);
+    if (pm1) int01_kernel<N, true><<<grid, I01Cfg<N>::NT, 0, s>>>(A, p.e, p.chunks, partials, flag, 0, 0);
+    else     int01_kernel<N, false><<<grid, I01Cfg<N>::NT, 0, s>>>(A, p.e, p.chunks, partials, flag, 0, 0);
     return cudaGetLastError();
 }
 
@@ -325,6 +326,75 @@ cudaError_t int01_launch(const uint8_t* A, int n, int64_t B, bool pm1, void* out
     *flag_host_status = hflag;
     (void)ws_bytes;
     return cudaSuccess;
+}
+
+// ---- one matrix, a span of ranks (perm_int01_range): the span is cut like the complex walk's plan into
+// maximal aligned pieces of 2^e ranks (e <= b; pieces with 0 < e < U become single ranks), one launch per
+// run of equal pieces, all into the same per-block partial slots (accumulated), then one summing kernel.
+__global__ void int01_range_final_kernel(const u128* __restrict__ partials, int nblk, u128* __restrict__ out) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    u128 s = 0;
+    for (int k = 0; k < nblk; k++) s += partials[k];
+    *out = s;
+}
+
+template <int N>
+cudaError_t int01_range_seg(const uint8_t* A, int e, uint64_t c0, uint64_t count, int nblk, u128* partials, int* flag,
+                            int accum, cudaStream_t s) {
+    int01_kernel<N, false><<<dim3((unsigned)nblk, 1), I01Cfg<N>::NT, 0, s>>>(A, e, count, partials, flag, c0, accum);
+    return cudaGetLastError();
+}
+
+size_t int01_range_workspace_bytes() { return 16 + 16 + (size_t)kInt01RangeBlocks * sizeof(u128); }
+
+cudaError_t int01_range_launch(const uint8_t* A, int n, uint64_t k0, uint64_t k1, void* ws, cudaStream_t s,
+                               unsigned long long* raw_host, int* flag_host_status, int* launches) {
+    *launches = 0;
+    *flag_host_status = 0;
+    raw_host[0] = raw_host[1] = 0;
+    if (k1 <= k0) return cudaSuccess;
+    const int U = walk_inner_bits(n);
+    const int nblk = kInt01RangeBlocks;
+    int* flag = (int*)ws;
+    u128* out = (u128*)((char*)ws + 16);
+    u128* partials = (u128*)((char*)ws + 32);
+    // chunk length 2^b: ~8 chunks per thread of the nblk x 128 grid (>= 2^U, <= 2^30)
+    const uint64_t T = (uint64_t)nblk * 128u;
+    int b = 0;
+    while (b < 30 && ((k1 - k0) >> (b + 1)) >= T * 8u) b++;
+    if (b < U) b = U;
+    cudaError_t err = cudaMemsetAsync(flag, 0, sizeof(int), s);
+    int accum = 0;
+    uint64_t r = k0;
+    while (err == cudaSuccess && r < k1) {
+        int e = (r == 0) ? 63 : __builtin_ctzll(r);
+        if (e > b) e = b;
+        while (e > 0 && (k1 - r) < (1ull << e)) e--;
+        if (e < U) e = 0;
+        uint64_t cnt = 1;
+        if (e == b && e > 0) cnt = (k1 - r) >> b;                       // a run of whole 2^b chunks
+        switch (n) {
+#define PERM_CASE(N) case N: err = int01_range_seg<N>(A, e, r >> e, cnt, nblk, partials, flag, accum, s); break;
+            PERM_R8(PERM_CASE, 0) PERM_R8(PERM_CASE, 8) PERM_R8(PERM_CASE, 16) PERM_R8(PERM_CASE, 24)
+            PERM_CASE(33)
+#undef PERM_CASE
+            default: return cudaErrorInvalidValue;
+        }
+        accum = 1;
+        ++*launches;
+        r += cnt << e;
+    }
+    if (err != cudaSuccess) return err;
+    int01_range_final_kernel<<<1, 32, 0, s>>>(partials, nblk, out);
+    err = cudaGetLastError();
+    if (err != cudaSuccess) return err;
+    ++*launches;
+    int hflag = 0;
+    err = cudaMemcpyAsync(raw_host, out, sizeof(u128), cudaMemcpyDeviceToHost, s);
+    if (err == cudaSuccess) err = cudaMemcpyAsync(&hflag, flag, sizeof(int), cudaMemcpyDeviceToHost, s);
+    if (err == cudaSuccess) err = cudaStreamSynchronize(s);
+    *flag_host_status = hflag;
+    return err;
 }
 
 }  // namespace perm

@@ -195,5 +195,10 @@ cudaError_t weighted_launch(const double2* C, const int32_t* mult, int n, int R,
 size_t int01_workspace_bytes(int n, int64_t B);
 cudaError_t int01_launch(const uint8_t* A, int n, int64_t B, bool pm1, void* out, void* ws, size_t ws_bytes,
                          cudaStream_t s, int* flag_host_status, int* launches);
+// one 0-1 matrix over ranks [k0, k1): raw Gray sum mod 2^128 -> raw_host[0] (lo), raw_host[1] (hi)
+constexpr int kInt01RangeBlocks = 148 * 8;
+size_t int01_range_workspace_bytes();
+cudaError_t int01_range_launch(const uint8_t* A, int n, uint64_t k0, uint64_t k1, void* ws, cudaStream_t s,
+                               unsigned long long* raw_host, int* flag_host_status, int* launches);
 
 }  // namespace perm

@@ -15,7 +15,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from . import DD, perm_c128_finalize, perm_c128_range
+from . import DD, perm_c128_finalize, perm_c128_range, perm_int01_finalize, perm_int01_range
 
 
 def rank_span(total: int, world: int, rank: int) -> tuple[int, int]:
@@ -58,4 +58,46 @@ def sharded_permanent(A, group=None, *, workspace=None, stream=None, partial_out
     return combine(gathered.cpu().numpy(), n)
 
 
-__all__ = ["rank_span", "combine", "sharded_permanent", "DD"]
+def int01_rank_space(n: int) -> int:
+    """Ranks of perm_int01's walk: 2^{n-1} (half-range Glynn, n <= 28) or 2^n (Eq. (3), 29 <= n <= 33)."""
+    return 1 << (n if n > 28 else n - 1)
+
+
+def pack_i128(v: int) -> np.ndarray:
+    """A raw partial (int mod 2^128) as two int64 {lo, hi} -- what the collective exchanges (exact)."""
+    v = int(v) & ((1 << 128) - 1)
+    lo, hi = v & ((1 << 64) - 1), v >> 64
+    return np.array([lo - (1 << 64) if lo >= (1 << 63) else lo, hi - (1 << 64) if hi >= (1 << 63) else hi],
+                    dtype=np.int64)
+
+
+def combine_int01(gathered, n: int) -> int:
+    """Exact per(A) from a (G, 2) int64 array of raw partials {lo, hi}: summed mod 2^128 in any order."""
+    arr = np.asarray(gathered, dtype=np.int64).reshape(-1, 2)
+    parts = [((int(hi) & ((1 << 64) - 1)) << 64) | (int(lo) & ((1 << 64) - 1)) for lo, hi in arr]
+    return perm_int01_finalize(parts, n)
+
+
+def sharded_int01(A, group=None, *, stream=None) -> int:
+    """Exact per(A) of ONE 0-1 matrix (an (n, n) uint8 CUDA tensor) with its rank space split over the
+    ranks of a process group: each rank walks its distribute span (perm_int01_range), one all-gather of
+    the 16-byte raw partials, exact combine mod 2^128 on every rank ("sharding a single
+    int01 permanent")."""
+    import torch
+    import torch.distributed as dist
+
+    n = A.shape[-1]
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    k0, k1 = rank_span(int01_rank_space(n), world, rank)
+    part = torch.from_numpy(pack_i128(perm_int01_range(A, k0, k1, stream=stream))).to(A.device)
+    if world > 1:
+        gathered = torch.empty(2 * world, dtype=torch.int64, device=A.device)
+        dist.all_gather_into_tensor(gathered, part, group=group)
+    else:
+        gathered = part
+    return combine_int01(gathered.cpu().numpy(), n)
+
+
+__all__ = ["rank_span", "combine", "sharded_permanent", "int01_rank_space", "pack_i128", "combine_int01",
+           "sharded_int01", "DD"]

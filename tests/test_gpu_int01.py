@@ -75,3 +75,40 @@ def test_full_range_n29_vs_oracle(torch):
     assert _run(torch, A) == oracle.ryser_i01_batch(A)
     P = inputs.bernoulli_pm1((1, 29, 29), 2930)
     assert pb.perm_pm1(torch.from_numpy(P).cuda()) == [oracle.ryser_i8(P[0])]
+
+
+@pytest.mark.parametrize("n", [1, 2, 7, 12, 20, 24, 29])
+def test_int01_range_partition_is_exact(torch, n):
+    # one exact permanent from disjoint rank spans (perm_int01_range + perm_int01_finalize):
+    # ragged and unaligned cuts, a single-rank span and an empty span, against the oracle's Eq. (3)
+    from paper_1904_06229_b200 import shard
+    A = inputs.bernoulli01((1, n, n), 3300 + n)
+    ref = oracle.ryser_i01_batch(A)[0]
+    Ad = torch.from_numpy(A[0]).cuda()
+    N = shard.int01_rank_space(n)
+    cuts = sorted({0, N, N // 3, N // 3 + 1, (N // 2) | 1, max(0, N - 5)})
+    parts = [pb.perm_int01_range(Ad, cuts[i], cuts[i + 1]) for i in range(len(cuts) - 1)]
+    parts.append(pb.perm_int01_range(Ad, N // 3, N // 3))              # empty span -> 0
+    assert pb.perm_int01_finalize(parts, n) == ref
+    assert pb.perm_int01_finalize([pb.perm_int01_range(Ad, 0, N)], n) == ref
+    for G in (1, 3, 8):                                                  # distribute over G shards
+        spans = [shard.rank_span(N, G, r) for r in range(G)]
+        assert pb.perm_int01_finalize([pb.perm_int01_range(Ad, a, b) for a, b in spans], n) == ref
+
+
+def test_int01_range_closed_forms_and_errors(torch):
+    from paper_1904_06229_b200 import shard
+    n = 26
+    J = torch.ones((n, n), dtype=torch.uint8, device="cuda")
+    N = shard.int01_rank_space(n)
+    spans = [shard.rank_span(N, 5, r) for r in range(5)]
+    assert pb.perm_int01_finalize([pb.perm_int01_range(J, a, b) for a, b in spans], n) == math.factorial(n)
+    assert shard.sharded_int01(J) == math.factorial(n)                  # world = 1 path
+    bad = J.clone()
+    bad[3, 4] = 2
+    with pytest.raises(pb.PermError) as e:
+        pb.perm_int01_range(bad, 0, 1 << 10)
+    assert e.value.name == "PERM_E_NOT01"
+    with pytest.raises(pb.PermError) as e:
+        pb.perm_int01_range(J, 0, N + 1)
+    assert e.value.name == "PERM_E_ORDER"

@@ -74,3 +74,72 @@ def test_rank_span_matches_paper_distribute():
         for r in range(world):
             k, l = oracle.distribute(total, world, r)
             assert shard.rank_span(total, world, r) == (k, k + l)
+
+
+def _int01_raw_partial(A, k0, k1):
+    """Raw Gray sum of App. A in integers over ranks [k0, k1) (g_i = 2 w_i, term sign (-1)^{r+1}),
+    straight from the definition -- stands in for the GPU's perm_int01_range in this CPU test."""
+    n = A.shape[0]
+    a = [[int(v) for v in row] for row in A]
+    tot = 0
+    for r in range(k0, k1):
+        x = r ^ (r >> 1)
+        prod = 1
+        for i in range(n):
+            g = a[i][n - 1] - sum(a[i][j] for j in range(n - 1)) + 2 * sum(a[i][j] for j in range(n - 1) if (x >> j) & 1)
+            prod *= g
+        tot += prod if (r & 1) else -prod
+    return tot & ((1 << 128) - 1)
+
+
+def _int01_worker(rank, world, port, n, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1904_06229_b200 import inputs, shard
+        A = inputs.bernoulli01((1, n, n), 31)[0]
+        k0, k1 = shard.rank_span(shard.int01_rank_space(n), world, rank)
+        part = torch.from_numpy(shard.pack_i128(_int01_raw_partial(A, k0, k1)))
+        gathered = torch.empty(2 * world, dtype=torch.int64)
+        dist.all_gather_into_tensor(gathered, part)
+        q.put((rank, shard.combine_int01(gathered.numpy(), n)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_int01_combine_is_exact(world):
+    # one exact 0-1 permanent split over ranks: 16-byte raw partials, one all-gather, exact combine
+    n = 11
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_int01_worker, args=(r, world, port, n, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    import oracle
+    from paper_1904_06229_b200 import inputs
+    A = inputs.bernoulli01((1, n, n), 31)
+    ref = oracle.ryser_i01_batch(A)[0]
+    assert all(v == ref for _, v in res), (res, ref)
+
+
+def test_int01_finalize_host_logic():
+    # the ABI's finalize (host only, no GPU): divisibility check, sign, exact wrap-around of partials
+    from paper_1904_06229_b200 import shard, perm_int01_finalize, PermError
+    import oracle
+    from paper_1904_06229_b200 import inputs
+    n = 9
+    A = inputs.bernoulli01((1, n, n), 5)[0]
+    N = shard.int01_rank_space(n)
+    cuts = [0, 1, 100, 101, N]
+    parts = [_int01_raw_partial(A, cuts[i], cuts[i + 1]) for i in range(len(cuts) - 1)]
+    assert perm_int01_finalize(parts, n) == oracle.ryser_i01_batch(A[None])[0]
+    assert perm_int01_finalize(parts[::-1], n) == oracle.ryser_i01_batch(A[None])[0]   # order-free
+    with pytest.raises(PermError):
+        perm_int01_finalize(parts[:2], n)          # an incomplete cover is not divisible by 2^{n-1}
