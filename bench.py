@@ -13,6 +13,7 @@ Workloads (BASELINE.json configs; synthetic inputs from paper_1904_06229_b200/in
   cfg1: one 16x16 complex Gaussian (latency-bound).
   cfg2: 10^5 submatrices of an n^2 x n^2 Haar unitary for each n in {8,12,16,20}; batched perms/s.
   cfg3: 64 Bernoulli 0-1 matrices of order 24; exact int128; perms/s.
+  cfg3s: one 0-1 matrix of order 33, exact int128 via 2^33 Eq. (3) terms, rank space sharded; terms/s.
   cfgbd: 10^4 band matrices, n = 100, k = 5, App. C transfer method (NEXT-4); perms/s.
   cfgsp: one sparse 48x48 complex matrix (4% + a matching), App. B restricted enumeration (NEXT-3); sets/s.
   cfgpm: 1024 Bernoulli +-1 matrices of order 24 (Sec. V ensemble); exact; perms/s.
@@ -236,6 +237,16 @@ def oracle_rate_cfg(cfg: str, seconds: float = 12.0) -> dict:
         dt = time.perf_counter() - t0
         return {"value": k / dt, "unit": "perms/s", "cores": cores, "kind": "oracle",
                 "sample": f"Eq. (3) int128 oracle on {k} of the 64 config-3 matrices, {dt:.1f} s"}
+    if cfg == "cfg3s":
+        import numpy as np
+        A = inputs.bernoulli01((1, 33, 33), 33)[0]
+        B = np.ascontiguousarray(A[:24, :24])
+        t0 = time.perf_counter()
+        oracle.ryser_i01(B)
+        dt = time.perf_counter() - t0
+        return {"value": (1 << 24) / dt, "unit": "terms/s", "cores": cores, "kind": "oracle",
+                "sample": f"Eq. (3) int128 oracle on the leading 24x24 block of the cfg3s matrix (2^24 terms in "
+                          f"{dt:.1f} s); the rate per term extrapolates to the 2^33 terms at n = 33 within n/24"}
     if cfg == "cfgbd":
         A = inputs.cfgbd(64)
         t0 = time.perf_counter()
@@ -447,6 +458,50 @@ def run_ours(args):
                                "64 Bernoulli(1/2) 0-1 matrices of order 24 (seed 24), exact int128 permanents"),
                   "parallelism": f"batch x{world}", "l2": "input 0.6 MB; compute-bound" if pm1 else "input 37 KB; compute-bound"}
         scaling = "weak" if world > 1 else "strong"
+    elif cfg == "cfg3s":
+        # one exact 0-1 permanent of order 33 (2^33 terms of Eq. (3)), the rank space sharded over ranks
+        n = 33
+        A_np = inputs.bernoulli01((1, n, n), 33)[0]
+        total = shard.int01_rank_space(n)
+        k0, k1 = shard.rank_span(total, world, rank)
+        host = torch.from_numpy(np.ascontiguousarray(A_np)).pin_memory()
+        dev_in = host.to(device)
+        gathered = torch.empty(2 * world, dtype=torch.int64, device=device)
+        e0, e1 = ev(), ev()
+        h2d, d2h = host.numel(), 16 * world
+        walk_launches_per_step = 1
+        nlaunch = [0]
+
+        def step():
+            es = torch.cuda.Event(enable_timing=True)
+            es.record(stream)
+            dev_in.copy_(host, non_blocking=True)
+            e0.record(stream)
+            raw = pb.perm_int01_range(dev_in, k0, k1, stream=stream)      # synchronizes the stream
+            nlaunch[0] = pb.last_launches()
+            part = torch.from_numpy(shard.pack_i128(raw)).to(device, non_blocking=False)
+            if world > 1:
+                import torch.distributed as dist
+                dist.all_gather_into_tensor(gathered, part)
+                src = gathered
+            else:
+                src = part
+            e1.record(stream)
+            val = shard.combine_int01(src.cpu().numpy(), n)
+            ee = torch.cuda.Event(enable_timing=True)
+            ee.record(stream)
+            torch.cuda.synchronize()
+            return {"dev": e0.elapsed_time(e1), "e2e": es.elapsed_time(ee), "walk": e0.elapsed_time(e1),
+                    "result": val}
+
+        units_per_step = total
+        unit = "terms/s"
+        gpu_launches_per_step = 0                      # counted from the library after the warm-up
+        config = {"workload": "one Bernoulli(1/2) 0-1 matrix of order 33 (seed 33): exact per(A) via the 2^33 "
+                              "terms of Eq. (3) in int128, rank space sharded",
+                  "n": n, "terms_per_step": total, "parallelism": f"Gray-range x{world}",
+                  "l2": "input 1 KB; compute-bound"}
+        scaling = "strong"
     elif cfg == "cfgbd":
         kb = 5
         A_np = inputs.cfgbd()
@@ -606,7 +661,7 @@ def run_ours(args):
     e2e_val = units_per_step * K / (e2e_ms * 1e-3)
     out = {"metric": METRIC, "value": value, "unit": unit, "n_gpus": world, "steps": K, "warmup": args.warmup,
            "ms_per_step": dev_ms / K, "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
-           "dtype": "int128" if cfg in ("cfg3", "cfgpm") else "f64",
+           "dtype": "int128" if cfg in ("cfg3", "cfgpm", "cfg3s") else "f64",
            "data": "synthetic (seeded generators, paper_1904_06229_b200/inputs.py)",
            "config": config}
     nominal = fp64_nominal_tflops()
@@ -656,17 +711,22 @@ def run_ours(args):
                                "peak_measured_probe": peak_meas}
         else:
             # algorithmic integer ops per Gray term: n row-sum adds + (n-1) multiplies + 1 signed add
-            n3 = 24
-            ops = units_per_step / world * (1 << (n3 - 1)) * 2 * n3
-            kname = "int01_kernel<24, pm1> (INT fma + alu pipes)" if cfg == "cfgpm" else "int01_kernel<24> (INT fma + alu pipes)"
+            n3 = 33 if cfg == "cfg3s" else 24
+            ops = (units_per_step / world * 2 * n3 if cfg == "cfg3s"
+                   else units_per_step / world * (1 << (n3 - 1)) * 2 * n3)
+            kname = {"cfgpm": "int01_kernel<24, pm1> (INT fma + alu pipes)",
+                     "cfg3s": "int01_kernel<33> (Eq. (3) branch, INT fma + alu pipes)"}.get(cfg, "int01_kernel<24> (INT fma + alu pipes)")
             achieved = ops / (dev_ms / K * 1e-3) / 1e12
             ipeak = int_nominal_tops()
             out["roofline"] = {"bound": "alu", "achieved": achieved, "peak": ipeak, "unit": "Tops/s",
                                "frac": achieved / ipeak, "traffic": ncu_traffic(cfg),
                                "kernel": kname,
-                               "algorithmic": "2n integer ops per Gray term x 2^(n-1) terms x matrices",
+                               "algorithmic": ("2n integer ops per Gray term x 2^n terms / ranks" if cfg == "cfg3s" else
+                                               "2n integer ops per Gray term x 2^(n-1) terms x matrices"),
                                "peak_note": "derived: 148 SMs x 128 int lanes/clk (issue-bound) x 1965 MHz"}
     out["e2e"] = {"value": e2e_val, "unit": unit, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
+    if cfg == "cfg3s":
+        gpu_launches_per_step = nlaunch[0]             # range pieces + the summing kernel (library count)
     out["gpu_launches"] = gpu_launches_per_step * K
     out["clocks"] = clocks
     out["wall_s_timed_region"] = t_wall
@@ -711,7 +771,8 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=1)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="cfg5", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "cfgw", "cfgpm", "cfgsp", "cfgbd"])
+    ap.add_argument("--config", default="cfg5", choices=["cfg1", "cfg2", "cfg3", "cfg3s", "cfg4", "cfg5", "cfgw", "cfgpm",
+                                                          "cfgsp", "cfgbd"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
