@@ -16,6 +16,9 @@
 // round-robin over the resident warps): lane l owns the states l, l+32, ... and keeps their predecessor
 // ranks (combinatorial number system) in registers; the row's 2k+1 entries are prefetched one row
 // ahead and broadcast from shared memory; coefficients are double-buffered in shared memory.
+#include <mutex>
+#include <vector>
+
 #include "internal.h"
 
 namespace perm {
@@ -58,10 +61,20 @@ __device__ __forceinline__ uint32_t band_unrank(int r, int k, int width) {
     return m;
 }
 
-// per warp: 2 S double2 coefficients (double buffer) + the current row (2k+1 double2); for k = 6 the
-// predecessor table (S (k+1) ints) follows
+// Coefficient slots: state rank t lives at slot[t] of a (S rounded up to 8)-entry array.  The slots are
+// chosen on the host (band_layout) so that the 16-byte gathers of a warp hit distinct bank groups as
+// often as possible: a 128-bit shared load is served per quarter warp (8 lanes x 16 B = the 32 banks),
+// and two lanes of a quarter reading different slots with equal slot mod 8 cost an extra wavefront.
+__host__ __device__ constexpr int band_nslots(int k) { return (band_states(k) + 7) / 8 * 8; }
+constexpr int kBandMaxStates = 924;                    // C(12, 6)
+struct BandSlots {
+    int16_t slot[kBandMaxStates];                      // rank -> slot
+};
+
+// per warp: 2 nslots double2 coefficients (double buffer) + the current row (2k+1 double2); for k = 6
+// the predecessor table (S (k+1) ints) follows
 constexpr size_t band_smem_bytes(int k) {
-    return (size_t)kBandWarps * ((size_t)2 * band_states(k) + 2 * k + 1) * sizeof(double2) +
+    return (size_t)kBandWarps * ((size_t)2 * band_nslots(k) + 2 * k + 1) * sizeof(double2) +
            (k >= 6 ? (size_t)band_states(k) * (k + 1) * sizeof(int) : 0);
 }
 
@@ -74,20 +87,21 @@ __device__ __forceinline__ double2 lds_band(uint32_t addr) {
 template <int K>
 __global__ void __launch_bounds__(32 * kBandWarps) band_kernel(const double2* __restrict__ A, int n, int64_t B,
                                                                double2* __restrict__ per,
-                                                               double* __restrict__ abs2) {
-    constexpr int S = band_states(K), W = 2 * K + 1, P1 = K + 1;
+                                                               double* __restrict__ abs2,
+                                                               const __grid_constant__ BandSlots L) {
+    constexpr int S = band_states(K), W = 2 * K + 1, P1 = K + 1, NS = band_nslots(K);
     constexpr int SPL = (S + 31) / 32;                                     // states per lane
     extern __shared__ __align__(16) unsigned char bsm[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    double2* cur = (double2*)bsm + (size_t)warp * (2 * S + W);
-    double2* nxt = cur + S;
-    double2* row = cur + 2 * S;
+    double2* cur = (double2*)bsm + (size_t)warp * (2 * NS + W);
+    double2* nxt = cur + NS;
+    double2* row = cur + 2 * NS;
     // this lane's states t = lane + 32 u and their predecessors, packed (old state rank << 4 | window bit
     // p): new state t <- old state (t's mask << 1 | 1) without bit p, for each set bit p.  In registers
     // up to k = 5; for k = 6 (29 states per lane) in shared memory, built once per block.
     constexpr bool REG = SPL * P1 <= 64;
     int predr[REG ? SPL : 1][REG ? P1 : 1];
-    int* preds = (int*)(cur + (size_t)(kBandWarps - warp) * (2 * S + W));  // after the warps' slots
+    int* preds = (int*)(cur + (size_t)(kBandWarps - warp) * (2 * NS + W));  // after the warps' slots
 #pragma unroll
     for (int u = 0; u < (REG ? SPL : (S + 32 * kBandWarps - 1) / (32 * kBandWarps)); u++) {
         const int t = REG ? lane + 32 * u : (int)threadIdx.x + u * 32 * kBandWarps;
@@ -102,7 +116,7 @@ __global__ void __launch_bounds__(32 * kBandWarps) band_kernel(const double2* __
             if (m >> (2 * K)) continue;                                    // must fit the 2k-bit window
 #pragma unroll
             for (int x = 0; x < P1; x++)
-                if (x == q) packed[x] = (band_rank(m) << 4) | p;
+                if (x == q) packed[x] = ((int)L.slot[band_rank(m)] << 4) | p;
             q++;
         }
         if constexpr (REG) {
@@ -113,11 +127,15 @@ __global__ void __launch_bounds__(32 * kBandWarps) band_kernel(const double2* __
             for (int x = 0; x < P1; x++) preds[t * P1 + x] = packed[x];
         }
     }
+    int st[SPL];                                                           // this lane's store slots
+#pragma unroll
+    for (int u = 0; u < SPL; u++) st[u] = (lane + 32 * u < S) ? (int)L.slot[lane + 32 * u] : 0;
     if constexpr (!REG) __syncthreads();
     const int64_t nwarps = (int64_t)gridDim.x * kBandWarps;
     for (int64_t b = (int64_t)blockIdx.x * kBandWarps + warp; b < B; b += nwarps) {
         const double2* Ab = A + b * (int64_t)n * W;
-        for (int s = lane; s < S; s += 32) cur[s] = make_double2(s == 0 ? 1.0 : 0.0, 0.0);
+        const int slot0 = L.slot[0];
+        for (int s = lane; s < NS; s += 32) cur[s] = make_double2(s == slot0 ? 1.0 : 0.0, 0.0);
         double2 rnext = make_double2(0.0, 0.0);
         if (lane < W) rnext = (lane - K >= 0 && lane - K < n) ? Ab[lane] : make_double2(0.0, 0.0);
         for (int i = 0; i < n; i++) {
@@ -148,7 +166,7 @@ __global__ void __launch_bounds__(32 * kBandWarps) band_kernel(const double2* __
                         vi = fma(c.x, a.y, vi);
                         vi = fma(c.y, a.x, vi);
                     }
-                    nxt[t] = make_double2(vr, vi);
+                    nxt[st[u]] = make_double2(vr, vi);
                 }
             }
             double2* tmp = cur;
@@ -157,11 +175,101 @@ __global__ void __launch_bounds__(32 * kBandWarps) band_kernel(const double2* __
         }
         __syncwarp();
         if (lane == 0) {
-            const double2 r = cur[0];
+            const double2 r = cur[L.slot[0]];
             if (per) per[b] = r;
             if (abs2) abs2[b] = __dadd_rn(__dmul_rn(r.x, r.x), __dmul_rn(r.y, r.y));
         }
     }
+}
+
+// ---- host: the slot layout (computed once per k) --------------------------------------------------
+static uint32_t h_unrank(int r, int k, int width) {
+    uint32_t m = 0;
+    for (int i = k; i >= 1; i--) {
+        int c = i - 1;
+        while (c + 1 < width && binom_i(c + 1, i) <= r) c++;
+        r -= binom_i(c, i);
+        m |= 1u << c;
+    }
+    return m;
+}
+
+static int h_rank(uint32_t m) {
+    int r = 0, i = 1;
+    for (int c = 0; m; c++, m >>= 1)
+        if (m & 1u) r += binom_i(c, i++);
+    return r;
+}
+
+// Colours (slot mod 8) by local search: start from slot = rank, swap the colours of two states when that
+// does not increase the number of wavefronts of the gathers (every (state group u, predecessor x,
+// quarter warp) of the kernel's loop) and of the coefficient stores; swaps keep the colour classes equal
+// in size, so the slots fill 8 x ceil(S/8) entries.  Deterministic (fixed LCG).
+static void band_layout_compute(int k, BandSlots& out) {
+    const int S = band_states(k), P1 = k + 1, SPL = (S + 31) / 32;
+    std::vector<int> np(S), pr((size_t)S * P1, -1);
+    for (int t = 0; t < S; t++) {
+        const uint32_t nw = (h_unrank(t, k, 2 * k) << 1) | 1u;
+        int q = 0;
+        for (int p = 0; p <= 2 * k; p++) {
+            if (!((nw >> p) & 1u)) continue;
+            const uint32_t m = nw & ~(1u << p);
+            if (m >> (2 * k)) continue;
+            pr[(size_t)t * P1 + q++] = h_rank(m);
+        }
+        np[t] = q;
+    }
+    std::vector<std::vector<int>> groups;                 // distinct states read / written together
+    for (int u = 0; u < SPL; u++)
+        for (int x = 0; x <= P1; x++)                     // x == P1: the stores nxt[slot[t]]
+            for (int ph = 0; ph < 4; ph++) {
+                std::vector<int> g;
+                for (int l = 8 * ph; l < 8 * ph + 8; l++) {
+                    const int t = l + 32 * u;
+                    if (t >= S) continue;
+                    const int v = x == P1 ? t : (x < np[t] ? pr[(size_t)t * P1 + x] : -1);
+                    if (v < 0) continue;
+                    bool dup = false;
+                    for (int w : g) dup |= (w == v);
+                    if (!dup) g.push_back(v);
+                }
+                if (g.size() > 1) groups.push_back(g);
+            }
+    std::vector<std::vector<int>> member(S);
+    for (int gi = 0; gi < (int)groups.size(); gi++)
+        for (int v : groups[gi]) member[v].push_back(gi);
+    std::vector<int> col(S);
+    for (int t = 0; t < S; t++) col[t] = t % 8;
+    auto gcost = [&](int gi) {
+        int cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0}, mx = 0;
+        for (int v : groups[gi]) mx = std::max(mx, ++cnt[col[v]]);
+        return mx;
+    };
+    uint64_t rng = 0x9e3779b97f4a7c15ull + (uint64_t)k;
+    auto next = [&]() { rng = rng * 6364136223846793005ull + 1442695040888963407ull; return (uint32_t)(rng >> 33); };
+    std::vector<int> touched;
+    const int iters = (k <= 5 ? 1500 : 300) * S;       // one-time host cost: ~0.1 s at k = 5
+    for (int it = 0; it < iters; it++) {
+        const int a = (int)(next() % (uint32_t)S), b = (int)(next() % (uint32_t)S);
+        if (col[a] == col[b]) continue;
+        touched.clear();
+        for (int gi : member[a]) touched.push_back(gi);
+        for (int gi : member[b]) touched.push_back(gi);
+        int before = 0, after = 0;
+        for (int gi : touched) before += gcost(gi);
+        std::swap(col[a], col[b]);
+        for (int gi : touched) after += gcost(gi);
+        if (after > before) std::swap(col[a], col[b]);    // (groups shared by a and b count twice: harmless)
+    }
+    int fill[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int t = 0; t < S; t++) out.slot[t] = (int16_t)(col[t] + 8 * fill[col[t]]++);
+}
+
+static const BandSlots& band_layout(int k) {
+    static std::once_flag once[kMaxBandK + 1];
+    static BandSlots lay[kMaxBandK + 1];
+    std::call_once(once[k], [k] { band_layout_compute(k, lay[k]); });
+    return lay[k];
 }
 
 template <int K>
@@ -178,7 +286,7 @@ cudaError_t band_launch_t(const double2* A, int n, int64_t B, double2* per, doub
     if (bps < 1) bps = 1;
     const int64_t need = (B + kBandWarps - 1) / kBandWarps;
     const int64_t grid = need < (int64_t)sms * bps ? need : (int64_t)sms * bps;
-    band_kernel<K><<<(unsigned)grid, 32 * kBandWarps, smem, s>>>(A, n, B, per, abs2);
+    band_kernel<K><<<(unsigned)grid, 32 * kBandWarps, smem, s>>>(A, n, B, per, abs2, band_layout(K));
     return cudaGetLastError();
 }
 
