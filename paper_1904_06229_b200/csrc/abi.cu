@@ -516,6 +516,7 @@ perm_status_t perm_c128_sparse(const perm_c128_t* A, int n, perm_c128_t* out_hos
     L.n = n;
     L.d = (int)I.d;
     L.nt = (int)I.nt;
+    L.A_host = (const double2*)Ah;
     int slot = 0;
     for (int j = 0; j < n; j++)
         if ((I.tmask >> j) & 1ull) L.col[slot++] = j;

@@ -174,6 +174,7 @@ struct SparseLaunch {
     int col[64];            // permuted column order: T columns, then S_1, S_2, ...
     int soff[kSparseMaxD];  // first slot of S_l
     int ssz[kSparseMaxD];   // |S_l|
+    const double2* A_host;  // host, row-major n x n (inner T columns for the constant-bank walk)
     cudaStream_t stream;
 };
 template <int N> cudaError_t sparse_launch_t(const SparseLaunch& L);

@@ -14,6 +14,8 @@
 // |gray r| = r (mod 2) the item's contribution is -(-1)^{|s|} times that.  Partials: dd per thread ->
 // warp -> block -> fixed-order reduction (reduce.cu) with the final factor (-1)^n.
 #pragma once
+#include <cstring>
+
 #include "walk.cuh"
 
 namespace perm {
@@ -30,6 +32,118 @@ struct SparseParams {   // kernel-parameter copy of SparseLaunch
     int32_t soff[kSparseMaxD];    // slot of S_l's first column (in the permuted order)
     int32_t ssz[kSparseMaxD];     // |S_l|
 };
+
+// Constant-bank variant (walk.cuh, walk_kernel_c): the T walk's inner U columns ride in the kernel
+// parameters (slots 0..U-1 of the permuted order are T's first columns) and reach the row-sum updates as
+// uniform-register operands.  Needs a warp-uniform item loop (every lane runs every iteration; lanes past
+// the end walk a valid item and drop it) and e > U; the e <= U case keeps the shared-memory walk.
+// Orders for which ptxas keeps those loads on the uniform datapath (LDCU -> DADD R, R, UR; scanned with
+// PERM_SPARSE_CONST=2, guarded by tests/test_abi_cpu.py); n = 48: 4.96e10 -> 5.55e10 sets/s.
+#ifndef PERM_SPARSE_CONST
+#define PERM_SPARSE_CONST 1
+#endif
+__host__ __device__ constexpr bool sparse_const_path(int n) {
+    return PERM_SPARSE_CONST == 2 ? true
+         : PERM_SPARSE_CONST == 1 ? ((n >= 17 && n <= 33 && n != 24) || n == 47 || n == 48) : false;
+}
+
+template <int N>
+struct SparseParamsC {
+    WalkParamsC<N> w;             // col[][]: inner T columns (w.A, w.partials, c0, count, eb unused)
+    SparseParams s;
+};
+
+// The walk of one aligned chunk c of the T walk (2^e ranks, e > U) from seeded row sums, inner columns
+// from the constant bank (as walk_chunk_const), block-boundary columns from shared memory.
+template <class C>
+__device__ __forceinline__ void walk_seeded_cbank(const WalkParamsC<C::N>& Pw, uint32_t lc, uint64_t c, int e,
+                                                 double (&wr)[C::N], double (&wi)[C::N], ddc& acc) {
+    constexpr int N = C::N, U = C::U;
+    const int nblk = 1 << (e - U);
+    const uint64_t cpar = c & 1ull;
+    constexpr int kFoldMask = (U >= kWalkFoldBits) ? 0 : ((1 << (kWalkFoldBits - U)) - 1);
+    double ar = 0.0, ai = 0.0;
+    for (int q = 0; q < nblk; q++) {
+        const int z = q >> 30;
+        if (q > 0) {
+            const int j = U + __ffs(q) - 1;
+            const uint64_t nb = (j + 1 < e) ? (uint64_t)((q >> (j + 1 - U)) & 1) : cpar;
+            flip_add<N>(lc + (uint32_t)(j * N) * 16u + (nb ? C::NEG : 0u), wr, wi);
+        }
+        InnerStepC<C, 0>::run(Pw, z, wr, wi, (q & 1) ? -1.0 : 1.0, ar, ai);
+        if (((q + 1) & kFoldMask) == 0 || q + 1 == nblk) {
+            acc.re = dd_add_d(acc.re, ar);
+            acc.im = dd_add_d(acc.im, ai);
+            ar = 0.0;
+            ai = 0.0;
+        }
+    }
+}
+
+template <int N>
+__global__ void __launch_bounds__(walk_block_threads(N)) sparse_kernel_c(const __grid_constant__ SparseParamsC<N> PC) {
+    using C = WCfg<N, 1>;
+    const SparseParams& P = PC.s;
+    extern __shared__ double2 smem[];
+    for (int k = threadIdx.x; k < N * C::P; k += blockDim.x) {
+        const int slot = k / C::P, i = k - slot * C::P;
+        const double2 a = (i < N) ? P.A[i * N + P.col[slot]] : make_double2(0.0, 0.0);
+        smem[k] = a;
+        smem[N * C::P + k] = make_double2(-a.x, -a.y);
+    }
+    __syncthreads();
+    const uint32_t lc = (uint32_t)__cvta_generic_to_shared(smem);
+    ddc acc;
+    acc.re.hi = acc.re.lo = acc.im.hi = acc.im.lo = 0.0;
+    const uint64_t total = P.outer * P.chunks;
+    const uint32_t ln = threadIdx.x & 31u;
+    const uint64_t wid = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (uint64_t)__shfl_sync(0xffffffffu, threadIdx.x >> 5, 0);
+    const uint64_t nw = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    for (uint64_t base = wid * 32u; base < total; base += nw * 32u) {
+        const uint64_t gg = base + ln;
+        const bool valid = gg < total;
+        const uint64_t g = valid ? gg : base;
+        uint64_t o = g / P.chunks;
+        const uint64_t c = g - o * P.chunks;
+        double wr[N], wi[N];
+#pragma unroll
+        for (int i = 0; i < N; i++) { wr[i] = 0.0; wi[i] = 0.0; }
+        int ssum = 0;
+        for (int l = 0; l < P.d; l++) {
+            const uint64_t r = (1ull << P.ssz[l]) - 1ull;
+            const uint64_t m = o % r + 1ull;
+            o /= r;
+            for (int q = 0; q < P.ssz[l]; q++) {
+                const double f = (double)((m >> q) & 1ull);
+                flip_dyn<N>(lc + (uint32_t)((P.soff[l] + q) * C::P) * 16u, f, wr, wi);
+            }
+            ssum += __popcll(m);
+        }
+        ddc part;
+        part.re.hi = part.re.lo = part.im.hi = part.im.lo = 0.0;
+        const int e = P.e;                                   // > U on this path (sparse_launch_t)
+        const uint64_t x = ((c ^ (c >> 1)) << e) | ((c & 1ull) << (e - 1));
+        for (int q = e - 1; q < P.nt; q++)
+            flip_dyn<N>(lc + (uint32_t)(q * C::P) * 16u, (double)((x >> q) & 1ull), wr, wi);
+        walk_seeded_cbank<C>(PC.w, lc, c, e, wr, wi, part);
+        if ((ssum & 1) == 0) {
+            part.re.hi = -part.re.hi; part.re.lo = -part.re.lo;
+            part.im.hi = -part.im.hi; part.im.lo = -part.im.lo;
+        }
+        if (valid) acc = ddc_add(acc, part);
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) acc = ddc_add(acc, shfl_down_ddc(acc, off));
+    __shared__ ddc swarp[32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) swarp[warp] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        ddc b = swarp[0];
+        for (int w = 1; w < (int)(blockDim.x >> 5); w++) b = ddc_add(b, swarp[w]);
+        P.partials[blockIdx.x] = b;
+    }
+}
 
 template <int N>
 __global__ void __launch_bounds__(walk_block_threads(N)) sparse_kernel(const __grid_constant__ SparseParams P) {
@@ -120,6 +234,20 @@ cudaError_t sparse_launch_t(const SparseLaunch& L) {
     for (int l = 0; l < kSparseMaxD; l++) {
         P.soff[l] = l < L.d ? L.soff[l] : 0;
         P.ssz[l] = l < L.d ? L.ssz[l] : 0;
+    }
+    if constexpr (sparse_const_path(N) && C::U >= 1 && WalkParamsC<N>::MN == 0) {
+        if (L.e > C::U) {
+            SparseParamsC<N> PC;
+            memset(&PC.w, 0, sizeof(PC.w));
+            for (int j = 0; j < WalkParamsC<N>::NC; j++)
+                for (int i = 0; i < N; i++) PC.w.col[j][i] = L.A_host[(size_t)i * N + L.col[j]];
+            PC.s = P;
+            cudaError_t err = cudaFuncSetAttribute(sparse_kernel_c<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   (int)C::smem_bytes);
+            if (err != cudaSuccess) return err;
+            sparse_kernel_c<N><<<L.grid, walk_block_threads(N), C::smem_bytes, L.stream>>>(PC);
+            return cudaGetLastError();
+        }
     }
     cudaError_t err = cudaFuncSetAttribute(sparse_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)C::smem_bytes);

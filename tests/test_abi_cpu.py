@@ -112,6 +112,9 @@ def test_const_walk_keeps_uniform_column_operands():
     lib = pb._LIB_PATH
     fns = ["_ZN4perm13walk_kernel_cILi32EEEvNS_11WalkParamsCIXT_EEE"]
     fns += [f"_ZN4perm14walk_kernel_cmILi{n}EEEvNS_11WalkParamsCIXT_EEE" for n in (34, 35, 37, 39, 42, 43, 44, 45)]
+    # the sparse kernel's constant-bank variant (sparse.cuh, sparse_const_path)
+    fns += [f"_ZN4perm15sparse_kernel_cILi{n}EEEvNS_13SparseParamsCIXT_EEE"
+            for n in list(range(17, 24)) + list(range(25, 34)) + [47, 48]]
     for fn in fns:
         sass = subprocess.run([cuobjdump, "-sass", "-fun", fn, lib], capture_output=True, text=True).stdout
         uniform = sum(1 for l in sass.splitlines() if "LDCU.64" in l and "c[0x0][UR" in l)
