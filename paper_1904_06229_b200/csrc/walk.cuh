@@ -44,7 +44,10 @@ struct WCfg {
 #ifdef PERM_WALK_K
     static constexpr int K = R >= 16 ? PERM_WALK_K : (R >= 4 ? 2 : 1);
 #else
-    static constexpr int K = R >= 4 ? 2 : 1;                 // independent product chains per lane
+    // independent product chains per lane: four (rows dealt round-robin) for the n = 44 constant-bank walk,
+    // where the shorter dependency chains measured +2.7% (6.16e10 -> 6.33e10 terms/s); two elsewhere (four
+    // measured slower at n = 32, 43, 45..48 and in the batched kernel: profiles/round1_walk_chains.txt)
+    static constexpr int K = (N == 44 && S == 1) ? 4 : (R >= 4 ? 2 : 1);
 #endif
     // columns a_{.j} (j < N), then their negations -a_{.j}, then the step-5 base vector
     static constexpr uint32_t NEG = (uint32_t)(N * P) * 16u;   // byte offset of -a_{.j} from a_{.j}
@@ -134,15 +137,87 @@ __device__ __forceinline__ void two_factors(const double (&wr)[R], const double 
         yr = wr[R - 1];
         yi = wi[R - 1];
     } else if constexpr (K == 2) {
+#ifdef PERM_CHAIN_STRIDE2
+        // rows interleaved between the chains (even rows / odd rows): both chains can start as soon as the
+        // first rows of a flip are updated
+        xr = wr[0]; xi = wi[0];
+        yr = wr[1]; yi = wi[1];
+#pragma unroll
+        for (int i = 2; i < R; i++) {
+            if (i & 1) cmul2(yr, yi, wr[i], wi[i]);
+            else       cmul2(xr, xi, wr[i], wi[i]);
+        }
+#else
         chain<0, R / 2, R>(wr, wi, xr, xi);
         chain<R / 2, R, R>(wr, wi, yr, yi);
+#endif
+    } else if constexpr (K == 3) {
+        constexpr int t = R / 3;
+        double zr, zi;
+        chain<0, t, R>(wr, wi, xr, xi);
+        chain<t, 2 * t, R>(wr, wi, yr, yi);
+        chain<2 * t, R, R>(wr, wi, zr, zi);
+        cmul2(xr, xi, yr, yi);
+        yr = zr;
+        yi = zi;
+    } else if constexpr (K == 8) {
+        // eight chains of ~R/8 rows, combined as a tree: (01)(23) and (45)(67) -> two factors
+        double cr[8], ci[8];
+#pragma unroll
+        for (int c = 0; c < 8; c++) {
+            const int b = c * R / 8, e = (c + 1) * R / 8;
+            cr[c] = wr[b];
+            ci[c] = wi[b];
+#pragma unroll
+            for (int i = b + 1; i < e; i++) cmul2(cr[c], ci[c], wr[i], wi[i]);
+        }
+        cmul2(cr[0], ci[0], cr[1], ci[1]);
+        cmul2(cr[2], ci[2], cr[3], ci[3]);
+        cmul2(cr[4], ci[4], cr[5], ci[5]);
+        cmul2(cr[6], ci[6], cr[7], ci[7]);
+        cmul2(cr[0], ci[0], cr[2], ci[2]);
+        cmul2(cr[4], ci[4], cr[6], ci[6]);
+        xr = cr[0]; xi = ci[0];
+        yr = cr[4]; yi = ci[4];
+    } else if constexpr (K >= 5) {
+        // K chains of ~R/K rows, folded into two factors (K - 2 extra multiplies, same total n - 1)
+        double cr[K], ci[K];
+#pragma unroll
+        for (int c = 0; c < K; c++) {
+            const int b = c * R / K, e = (c + 1) * R / K;
+            cr[c] = wr[b];
+            ci[c] = wi[b];
+#pragma unroll
+            for (int i = b + 1; i < e; i++) cmul2(cr[c], ci[c], wr[i], wi[i]);
+        }
+#pragma unroll
+        for (int c = 2; c < K; c++) {
+            if (c & 1) cmul2(cr[1], ci[1], cr[c], ci[c]);
+            else       cmul2(cr[0], ci[0], cr[c], ci[c]);
+        }
+        xr = cr[0]; xi = ci[0];
+        yr = cr[1]; yi = ci[1];
     } else {
         constexpr int q = R / 4;
         double r0, i0, r1, i1, r2, i2, r3, i3;
+#ifndef PERM_CHAIN_BLOCK4
+        // rows dealt round-robin to the four chains (chain c: rows c, c+4, ...); the two products then
+        // multiply each other in the fused accumulation
+        r0 = wr[0]; i0 = wi[0]; r1 = wr[1]; i1 = wi[1]; r2 = wr[2]; i2 = wi[2]; r3 = wr[3]; i3 = wi[3];
+#pragma unroll
+        for (int i = 4; i < R; i++) {
+            if ((i & 3) == 0) cmul2(r0, i0, wr[i], wi[i]);
+            else if ((i & 3) == 1) cmul2(r1, i1, wr[i], wi[i]);
+            else if ((i & 3) == 2) cmul2(r2, i2, wr[i], wi[i]);
+            else cmul2(r3, i3, wr[i], wi[i]);
+        }
+        (void)q;
+#else
         chain<0, q, R>(wr, wi, r0, i0);
         chain<q, 2 * q, R>(wr, wi, r1, i1);
         chain<2 * q, 3 * q, R>(wr, wi, r2, i2);
         chain<3 * q, R, R>(wr, wi, r3, i3);
+#endif
         cmul2(r0, i0, r1, i1);
         cmul2(r2, i2, r3, i3);
         xr = r0; xi = i0; yr = r2; yi = i2;
