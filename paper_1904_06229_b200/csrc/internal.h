@@ -62,6 +62,9 @@ __host__ __device__ constexpr int walk_block_threads(int n) {
 #define PERM_WALK_FOLD 5
 #endif
 constexpr int kWalkFoldBits = PERM_WALK_FOLD;
+// The n = 44 constant-bank walk folds every 2^7 terms: +0.3% (profiles/round1_walk_chains.txt); the plain
+// partial over 128 terms of |prod w| ~ 1e23 carries ~1e9 absolute rounding, 1e-20 of the error floor.
+__host__ __device__ constexpr int walk_fold_bits_const(int n) { return n == 44 ? 7 : kWalkFoldBits; }
 
 // A run of `count` aligned chunks of 2^e ranks: chunk k covers ranks [(c0+k) 2^e, (c0+k+1) 2^e).
 // e == 0 chunks are single terms (seeded from scratch).

@@ -629,7 +629,7 @@ __device__ __forceinline__ void walk_chunk_const(const WalkParamsC<C::N>& P, uin
     }
     const int nblk = 1 << (e - U);                        // >= 2: the planner sends only e > U here
     const uint64_t cpar = c & 1ull;
-    constexpr int kFoldMask = (U >= kWalkFoldBits) ? 0 : ((1 << (kWalkFoldBits - U)) - 1);
+    constexpr int kFoldMask = (U >= walk_fold_bits_const(N)) ? 0 : ((1 << (walk_fold_bits_const(N) - U)) - 1);
     double ar = 0.0, ai = 0.0;
     for (int q = 0; q < nblk; q++) {
 #ifdef PERM_CONST_SHFL_Z
