@@ -205,9 +205,16 @@ def oracle_rate_cfg(cfg: str, seconds: float = 12.0) -> dict:
             t0 = time.perf_counter()
             oracle.subpermanent(A, 0, span, parts=4 * cores)
             dt = time.perf_counter() - t0
+        # 1-core rate: the serial App. A subpermanent (parts = 1) on a proportionally smaller span
+        span1 = max(1, min(total, int(span / cores / 3)))
+        t0 = time.perf_counter()
+        oracle.subpermanent(A, 0, span1, parts=1)
+        dt1 = time.perf_counter() - t0
         return {"value": span / dt, "unit": "terms/s", "cores": cores, "kind": "oracle",
+                "value_1core": span1 / dt1,
                 "sample": f"App. A subpermanent (binary128) over {span} of the {total} Gray ranks of the {cfg} "
-                          f"matrix, {dt:.1f} s on {cores} host threads; rate extrapolates linearly"}
+                          f"matrix, {dt:.1f} s on {cores} host threads (1 core: {span1} ranks in {dt1:.1f} s); "
+                          f"rate extrapolates linearly"}
     if cfg == "cfg2":
         rates, parts = [], []
         for n in (8, 12, 16, 20):
@@ -293,11 +300,13 @@ def oracle_rate_cfg(cfg: str, seconds: float = 12.0) -> dict:
 
 def run_ours(args):
     import torch
+    import torch.distributed as dist
     world, rank, local = dist_env()
-    if world > 1:
-        import torch.distributed as dist
-        # PERM_BENCH_DIST_BACKEND=gloo is a functional test hook only (several ranks sharing the box's one
-        # GPU, results checked, timings meaningless); the measured multi-GPU path is NCCL, one rank per GPU.
+    # Launched by torchrun (even with one rank): one process per GPU over NCCL.  PERM_BENCH_DIST_BACKEND=gloo
+    # is a functional test hook only (several ranks sharing the box's one GPU, results checked, timings
+    # meaningless).
+    dist_on = world > 1 or ("MASTER_ADDR" in os.environ and "RANK" in os.environ)
+    if dist_on:
         backend = os.environ.get("PERM_BENCH_DIST_BACKEND", "nccl")
         dev = local % torch.cuda.device_count() if backend != "nccl" else local
         torch.cuda.set_device(dev)
@@ -322,6 +331,7 @@ def run_ours(args):
         return e
 
     result = {}
+    warm_step = None
     gpu_launches_per_step = 0
     h2d = d2h = 0
     walk_launches_per_step = 0
@@ -331,43 +341,110 @@ def run_ours(args):
         A_np = {"cfg5": inputs.cfg5, "cfg4": inputs.cfg4, "cfg1": inputs.cfg1}[cfg]()
         n = A_np.shape[0]
         total = 1 << (n - 1)
-        k0, k1 = shard.rank_span(total, world, rank)
+        b = pb.chunk_log2(n)
+        chunks = 1 << (n - 1 - b)
+        c0, c1 = shard.chunk_span(n, world, rank, b)            # whole aligned chunks per GPU
+        wave = pb.chunk_walkers(n, b)                           # chunks one launch walks per round
+        # One permanent per step when it takes seconds at most; otherwise ONE permanent per run, its chunk
+        # range cut into K steps of whole rounds (each step: walk + tree + all-gather of the nodes).
+        est_s = total / world / 6.0e10
+        perm_steps = args.steps_per_perm or (args.steps if est_s > 4.0 else 1)
+        if args.steps % perm_steps:
+            raise SystemExit("--steps must be a multiple of --steps-per-perm")
+        slices = shard.step_slices(c0, c1, perm_steps, wave)
+        warm = (c0, min(c1, c0 + wave))                        # warm-up: one round of the rank's first chunks
+        max_slice = max([s1 - s0 for s0, s1 in slices] + [warm[1] - warm[0], 1])
         A_pin = torch.from_numpy(A_np).pin_memory()
-        ws = pb.make_workspace(n, k0, k1, device=device)
-        part = torch.empty(4, dtype=torch.float64, device=device)
-        gathered = torch.empty(4 * world, dtype=torch.float64, device=device)
-        gathered_host = torch.empty(4 * world, dtype=torch.float64).pin_memory()
+        parts = torch.empty((max_slice, 4), dtype=torch.float64, device=device)
+        ws_a = torch.empty(n * n * 16, dtype=torch.uint8, device=device)
+        tree_ws = torch.empty(pb.tree_workspace_bytes(max_slice), dtype=torch.uint8, device=device)
+        nodes = torch.empty((pb.TREE_MAX_NODES, 6), dtype=torch.int64, device=device)
+        gathered = torch.empty((world * pb.TREE_MAX_NODES, 6), dtype=torch.int64, device=device)
+        gathered_host = torch.empty((world * pb.TREE_MAX_NODES, 6), dtype=torch.int64).pin_memory()
         ew0, ew1, ec1, es0, es1 = ev(), ev(), ev(), ev(), ev()
-        h2d, d2h = A_np.nbytes, 4 * world * 8
+        h2d, d2h = A_np.nbytes, gathered_host.numel() * 8
         walk_launches_per_step = 1
-        roofline_units = 8.0 * n * (k1 - k0)       # algorithmic flops of this rank's walk launch
+        collected: list = []
+        step_idx = [0]
+        terms_walked = [0]
+        launch_count = [0]
 
-        def step():
+        # One process and a whole permanent per step: the single-call public API perm_c128 (for n <= 16 one
+        # cluster launch; else the chunk walk + tree inside the library -- the same chunks and tree, same bits).
+        single = not dist_on and perm_steps == 1
+        out_dev = torch.empty(1, dtype=torch.complex128, device=device)
+        out_host = torch.empty(1, dtype=torch.complex128).pin_memory()
+        ws_single = pb.make_workspace(n, device=device) if single else None
+        if single:
+            d2h = 16
+
+        def step_single(sl=None):
+            warmup = sl is not None
             es0.record(stream)
-            pb.perm_c128_range(A_pin, k0, k1, workspace=ws, out=part, events=(ew0, ew1), stream=stream)
-            if world > 1:
-                import torch.distributed as dist
-                dist.all_gather_into_tensor(gathered, part)
-                src = gathered
-            else:
-                src = part
+            pb.perm_c128(A_pin, workspace=ws_single, out=out_dev, stream=stream, events=(ew0, ew1))
+            nl = pb.last_launches()
             ec1.record(stream)
-            gathered_host.copy_(src, non_blocking=True)
+            out_host.copy_(out_dev, non_blocking=True)
             es1.record(stream)
             torch.cuda.synchronize()
-            val = shard.combine(gathered_host.numpy(), n)
+            if not warmup:
+                launch_count[0] += nl
+                terms_walked[0] += total
+                step_idx[0] += 1
+            return {"dev": ew0.elapsed_time(ec1), "e2e": es0.elapsed_time(es1), "walk": ew0.elapsed_time(ew1),
+                    "result": complex(out_host.item())}
+
+        def step(sl=None):
+            if single:
+                return step_single(sl)
+            warmup = sl is not None
+            s0, s1 = sl if warmup else slices[step_idx[0] % perm_steps]
+            es0.record(stream)                                  # e2e: from the H2D of A (inside the call)
+            pb.perm_c128_chunks(A_pin, s0, s1, partials=parts, workspace=ws_a, stream=stream, events=(ew0, ew1))
+            nl = pb.last_launches()
+            pb.perm_c128_tree(parts, s0, s1, nodes=nodes, workspace=tree_ws, stream=stream)
+            nl += pb.last_launches()
+            if dist_on:
+                dist.all_gather_into_tensor(gathered, nodes)
+                src = gathered
+            else:
+                src = nodes
+            ec1.record(stream)
+            gathered_host[: src.shape[0]].copy_(src, non_blocking=True)
+            es1.record(stream)
+            torch.cuda.synchronize()
+            val = None
+            if not warmup:
+                launch_count[0] += nl
+                terms_walked[0] += (s1 - s0) << b
+                collected.append(gathered_host[: src.shape[0]].numpy().copy())
+                if step_idx[0] % perm_steps == perm_steps - 1:
+                    val = shard.combine_nodes(np.concatenate(collected), n)
+                    collected.clear()
+                step_idx[0] += 1
             return {"dev": ew0.elapsed_time(ec1), "e2e": es0.elapsed_time(es1), "walk": ew0.elapsed_time(ew1),
                     "result": val}
 
-        units_per_step = total
+        warm_step = lambda: step(warm)
         unit = "terms/s"
-        gpu_launches_per_step = 2
+        gpu_launches_per_step = None                            # counted below from the library
         workload = {"cfg5": "one 44x44 complex Gaussian matrix (re, im ~ N(0,1/2), seed 44): per(A) via 2^43 Gray terms",
                     "cfg4": "32x32 leading block of a 1024x1024 Haar unitary (seed 1024): per(A) via 2^31 Gray terms",
                     "cfg1": "one 16x16 complex Gaussian matrix (seed 16): per(A) via 2^15 Gray terms"}[cfg]
-        config = {"workload": workload, "n": n, "terms_per_step": total, "parallelism": f"Gray-range x{world}",
-                  "shard_terms_rank0": shard.rank_span(total, world, 0)[1], "input_bytes": A_np.nbytes,
-                  "l2": "flushed between steps (256 MiB write)"}
+        config = {"workload": workload, "n": n, "chunk_log2": b, "chunks": chunks,
+                  "parallelism": f"Gray-chunk range x{world}",
+                  "permanents_per_run": args.steps // perm_steps,
+                  "steps_per_permanent": perm_steps,
+                  "terms_per_step": (total // perm_steps if perm_steps > 1 else total),
+                  "slicing": ("one full permanent per run: the rank's chunk span cut into K steps of whole "
+                              f"rounds of {wave} chunks; every step walks its slice, reduces it by the canonical "
+                              "chunk tree and all-gathers the tree nodes; the last step merges all nodes -> per(A)"
+                              if perm_steps > 1 else "one full permanent per step"),
+                  "api": ("perm_c128 (one call per permanent)" if single else
+                          "perm_c128_chunks + perm_c128_tree per step, all-gather of the tree nodes, "
+                          "perm_c128_tree_combine + perm_c128_finalize"),
+                  "chunks_rank0": shard.chunk_span(n, world, 0, b)[1], "input_bytes": A_np.nbytes,
+                  "l2": "compute-bound (input 31 KB); L2 flushed between steps (256 MiB write)"}
         scaling = "strong"
     elif cfg == "cfg2":
         ns = (8, 12, 16, 20)
@@ -621,14 +698,13 @@ def run_ours(args):
 
     # warm-up (untimed)
     for _ in range(args.warmup):
-        step()
+        (warm_step or step)()
         flush_l2(l2buf)
     torch.cuda.synchronize()
     peak_meas = measure_fp64_peak(pb, torch) if rank == 0 else None
 
     # timed region: barrier + synchronize on both sides
-    if world > 1:
-        import torch.distributed as dist
+    if dist_on:
         dist.barrier()
     torch.cuda.synchronize()
     devs, e2es, walks, res = [], [], [], None
@@ -639,11 +715,12 @@ def run_ours(args):
             devs.append(r["dev"])
             e2es.append(r["e2e"])
             walks.append(r["walk"])
-            res = r["result"]
+            if r["result"] is not None:
+                res = r["result"]
             flush_l2(l2buf)
         torch.cuda.synchronize()
         t_wall = time.perf_counter() - t_wall0
-    if world > 1:
+    if dist_on:
         dist.barrier()
     torch.cuda.synchronize()
     dev_ms = max_over_ranks(sum(devs), world, device)
@@ -651,9 +728,14 @@ def run_ours(args):
     walk_ms_local = sum(walks) / len(walks)
     walk_ms = max_over_ranks(walk_ms_local, world, device)
     clocks = clk.summary()
+    if cfg in ("cfg5", "cfg4", "cfg1"):
+        # roofline of the walk kernel: algorithmic flops of rank 0's walk launches / their event-timed duration
+        roofline_units = 8.0 * n * terms_walked[0] / args.steps
+        walk_ms = sum(walks) / len(walks)
+        units_per_step = total / perm_steps
 
     if rank != 0:
-        if world > 1:
+        if dist_on:
             dist.destroy_process_group()
         return
     K = args.steps
@@ -727,14 +809,16 @@ def run_ours(args):
     out["e2e"] = {"value": e2e_val, "unit": unit, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
     if cfg == "cfg3s":
         gpu_launches_per_step = nlaunch[0]             # range pieces + the summing kernel (library count)
-    out["gpu_launches"] = gpu_launches_per_step * K
+    if cfg in ("cfg5", "cfg4", "cfg1"):
+        gpu_launches_per_step = launch_count[0] / K
+    out["gpu_launches"] = int(round(gpu_launches_per_step * K))
     out["clocks"] = clocks
     out["wall_s_timed_region"] = t_wall
     out["result_sample"] = str(res)
     if not args.no_cpu_baseline and world == 1:
         out["cpu_baseline"] = oracle_rate_cfg(cfg, seconds=args.cpu_seconds)
     print(json.dumps(out), flush=True)
-    if world > 1:
+    if dist_on:
         dist.destroy_process_group()
 
 
@@ -776,6 +860,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--steps-per-perm", type=int, default=0,
+                    help="cfg5/cfg4/cfg1: steps one permanent is sliced into (default: K when a permanent takes more "
+                         "than a few seconds at this GPU count, i.e. one permanent per run; else 1, a permanent per step)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)

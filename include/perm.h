@@ -53,7 +53,21 @@ typedef struct {
     void* ev_walk_begin;   /* in, optional cudaEvent_t: recorded on `stream` just before the walk
                               kernel is launched (NULL = not recorded)                            */
     void* ev_walk_end;     /* in, optional cudaEvent_t: recorded just after the walk kernel        */
+    uint64_t items;        /* out: walked items (aligned chunks + single-rank pieces), one dd partial each */
+    uint32_t const_path;   /* out: 1 if the aligned body ran in the constant-bank walk (walk_kernel_c*) */
+    uint32_t reserved;
 } perm_stats_t;
+
+/* One node of the canonical reduction tree (perm_c128_tree): the dd sum of the chunk partials
+ * [index * 2^level, (index + 1) * 2^level), combined as node(L+1, k) = node(L, 2k) + node(L, 2k+1).
+ * level == 0xffffffff marks an unused slot. */
+typedef struct {
+    uint32_t level;
+    uint32_t reserved;
+    uint64_t index;
+    double hi_re, lo_re, hi_im, lo_im;
+} perm_tree_node_t;
+#define PERM_TREE_MAX_NODES 128
 
 typedef enum {
     PERM_OK = 0,
@@ -70,8 +84,15 @@ typedef enum {
  * Single matrix (BASELINE configs 1, 4, 5).
  * ------------------------------------------------------------------------------------------ */
 
-/* Scratch bytes needed by perm_c128 / perm_c128_range for order n and rank range [k_begin, k_end). */
+/* Scratch bytes needed by perm_c128 / perm_c128_range for order n and rank range [k_begin, k_end)
+ * (one 32-byte dd partial per walked chunk plus the reduction tree: for a whole permanent
+ * 2^{n-1-b} * 32 bytes, b = perm_chunk_log2(n) -- 1 GiB at n = 44). */
 perm_status_t perm_workspace_bytes(int n, uint64_t k_begin, uint64_t k_end, size_t* bytes);
+
+/* The chunk length 2^b a whole permanent of order n is walked in (perm_c128, and the default of the
+ * chunk walk below): a function of n alone, so the result never depends on the grid, the number of GPUs
+ * or the slicing.  -1 if n is outside 1..64. */
+int perm_chunk_log2(int n);
 
 /* per(A) of one n x n complex matrix, 1 <= n <= 64 (ranks are 64-bit words).
  *   A          host or device, n*n perm_c128_t, row-major, read only, all entries finite.
@@ -79,6 +100,12 @@ perm_status_t perm_workspace_bytes(int n, uint64_t k_begin, uint64_t k_end, size
  *   out_dd     optional (may be NULL), host or device: the dd value of per(A) before rounding.
  *   workspace  device scratch of >= perm_workspace_bytes(n, 0, 2^{n-1}) bytes, or NULL.
  *   stats      optional host struct (may be NULL).
+ * The 2^{n-1} ranks are walked as 2^{n-1-b} aligned chunks of 2^b ranks (b = perm_chunk_log2(n)), each
+ * seeded explicitly (App. A steps 5-8); the chunks' dd partials are combined by the canonical
+ * pairwise tree (perm_c128_tree), so the value is bit-identical to the chunk walk + tree + combine below
+ * over ANY split of the chunks into launches or GPUs.
+ * A non-finite entry: PERM_E_NONFINITE when `out` / `out_dd` are host memory; with device outputs (no host
+ * synchronization) a device-resident A is checked by the kernel and the outputs become NaN.
  * Errors: PERM_E_ARG (A or out NULL), PERM_E_ORDER, PERM_E_NONFINITE, PERM_E_WORKSPACE, PERM_E_CUDA.
  * Cite: problem P:56-59; method App. A P:1126-1163 (subpermanent + permanent). */
 perm_status_t perm_c128(const perm_c128_t* A, int n, perm_c128_t* out, perm_dd_c128_t* out_dd,
@@ -87,12 +114,65 @@ perm_status_t perm_c128(const perm_c128_t* A, int n, perm_c128_t* out, perm_dd_c
 /* Raw partial P(k_begin, k_end) over the Gray ranks [k_begin, k_end) subset of [0, 2^{n-1}),
  * WITHOUT the 2(-1)^n factor: App. A subpermanent for the rank span that
  * distribute hands one worker.  Used to shard one permanent over GPUs/processes;
- * any split of [0, 2^{n-1}) into spans combined by perm_c128_finalize gives per(A).
+ * any split of [0, 2^{n-1}) into spans combined by perm_c128_finalize gives per(A) (up to rounding;
+ * for bit-identity across splits use the chunk walk + tree above).  The span is cut into maximal aligned
+ * pieces (chunks of 2^b ranks, b chosen from the span and the device, plus single ranks at unaligned
+ * ends); their dd partials are combined by the canonical tree over the piece index.
  *   partial    host or device, one perm_dd_c128_t.  k_begin == k_end gives 0.
  * Errors: as perm_c128, plus PERM_E_ORDER if k_end > 2^{n-1}, PERM_E_ARG if k_begin > k_end. */
 perm_status_t perm_c128_range(const perm_c128_t* A, int n, uint64_t k_begin, uint64_t k_end,
                               perm_dd_c128_t* partial, void* workspace, size_t workspace_bytes,
                               void* stream, perm_stats_t* stats);
+
+/* ------------------------------------------------------------------------------------------
+ * The chunk walk and its canonical reduction: one permanent split over launches / steps / GPUs
+ * (App. A distribute P:1077-1095, subpermanent P:1133-1151, step 4 P:1162;
+ * "partial sums ... stored in an array before the final summation").
+ * ------------------------------------------------------------------------------------------ */
+
+/* Walks the aligned chunks c in [c_begin, c_end) of 2^chunk_log2 ranks each (ranks [c 2^b, (c+1) 2^b))
+ * and writes chunk c's raw dd partial sum_{r in chunk} (-1)^{r+1} prod_i w_i(gray r) to
+ * partials_dev[c - c_begin].  A chunk's partial depends only on (A, n, b, c): the seed is recomputed from
+ * gray(c 2^b) and the accumulator starts at zero.
+ *   A            host or device, n*n perm_c128_t row-major (a device A is copied back once and checked).
+ *   chunk_log2   b: 0 or U(n) <= b <= min(n-1, 30) (U(n) = 3 for 4 <= n <= 33, 2 for most larger n;
+ *                perm_chunk_log2(n) always qualifies).
+ *   partials_dev device, (c_end - c_begin) perm_dd_c128_t.  c_end <= 2^{n-1-b}.
+ *   workspace    device, >= n*n*16 bytes when A is host memory (the H2D copy of A), else unused; NULL =
+ *                allocated stream-ordered.
+ * Stream-ordered when A is host memory (no synchronization); a device A is synchronized once.
+ * Errors: PERM_E_ARG (NULL, c_begin > c_end, bad b, partials not device), PERM_E_ORDER, PERM_E_NONFINITE,
+ *         PERM_E_WORKSPACE, PERM_E_CUDA. */
+perm_status_t perm_c128_chunks(const perm_c128_t* A, int n, int chunk_log2, uint64_t c_begin, uint64_t c_end,
+                               perm_dd_c128_t* partials_dev, void* workspace, size_t workspace_bytes, void* stream,
+                               perm_stats_t* stats);
+
+/* Chunk walkers one perm_c128_chunks launch of order n and chunk length 2^chunk_log2 keeps resident on
+ * the current device (grid x walkers per block): a span of k * walkers chunks leaves no partial last round
+ * of the static round-robin (bench.py slices one permanent into steps of whole rounds).
+ * Errors: PERM_E_ARG (NULL), PERM_E_ORDER, PERM_E_CUDA. */
+perm_status_t perm_chunk_walkers(int n, int chunk_log2, uint64_t* walkers);
+
+/* Scratch bytes of perm_c128_tree for `count` partials. */
+perm_status_t perm_tree_workspace_bytes(uint64_t count, size_t* bytes);
+
+/* Reduces the chunk partials of [c_begin, c_end) (partials_dev[i] = chunk c_begin + i) by the canonical
+ * binary tree over ABSOLUTE chunk indices to the span's maximal complete nodes (at most two per level),
+ * sorted by position, in `nodes` (PERM_TREE_MAX_NODES slots, unused ones marked level = 0xffffffff), and
+ * optionally their left-to-right dd sum in `raw` (the span's raw partial).  nodes / raw: host or device
+ * (either may be NULL, not both).  Synchronizes if an output is host memory.
+ * Errors: PERM_E_ARG, PERM_E_WORKSPACE, PERM_E_CUDA. */
+perm_status_t perm_c128_tree(const perm_dd_c128_t* partials_dev, uint64_t c_begin, uint64_t c_end,
+                             perm_tree_node_t* nodes, perm_dd_c128_t* raw, void* workspace, size_t workspace_bytes,
+                             void* stream);
+
+/* Host only: merges the nodes of disjoint spans (e.g. every GPU's perm_c128_tree output, in any order;
+ * unused slots are skipped): sibling nodes combine left + right until none remain, the rest are summed
+ * left to right.  raw receives the result; *root_level (optional) the level L if the nodes merged into
+ * the single node covering chunks [0, 2^L), else -1.  With the chunks of a whole permanent
+ * (L = n-1-b) raw is bit-identical to perm_c128's, and perm_c128_finalize(raw, 1, n) gives per(A).
+ * Errors: PERM_E_ARG (NULL raw, count < 0, overlapping or invalid nodes). */
+perm_status_t perm_c128_tree_combine(const perm_tree_node_t* nodes, int count, perm_dd_c128_t* raw, int* root_level);
 
 /* Host-only: out = 2(-1)^n * sum_{k=0}^{count-1} partials[k], summed in index order in double-double
  * (App. A permanent step 4; "stored in an array before the final ... summation").

@@ -10,6 +10,9 @@ Names follow the C ABI:
 * :func:`perm_c128`          -- per(A) of one complex matrix (App. A permanent)
 * :func:`perm_c128_range`    -- raw partial over a Gray-rank span (App. A subpermanent)
 * :func:`perm_c128_finalize` -- 2(-1)^n * ordered dd sum of partials
+* :func:`perm_c128_chunks`   -- dd partial of every aligned chunk of a chunk span (App. A subpermanent per chunk)
+* :func:`perm_c128_tree`     -- canonical pairwise tree over a span's chunk partials -> its maximal nodes
+* :func:`perm_c128_tree_combine` -- merge the nodes of disjoint spans (other steps / GPUs) -> raw partial
 * :func:`perm_c128_batched`  -- per and |per|^2 of a batch of small matrices
 * :func:`perm_c128_weighted_batched` -- repeated columns, weighted Ryser Eq. (4)
 * :func:`perm_int01`         -- exact int128 permanents of 0-1 matrices
@@ -57,7 +60,24 @@ class i128(ctypes.Structure):
 class stats_t(ctypes.Structure):
     _fields_ = [("terms", ctypes.c_uint64), ("chunk_log2", ctypes.c_uint32), ("threads", ctypes.c_uint32),
                 ("blocks", ctypes.c_uint32), ("launches", ctypes.c_uint32),
-                ("ev_walk_begin", ctypes.c_void_p), ("ev_walk_end", ctypes.c_void_p)]
+                ("ev_walk_begin", ctypes.c_void_p), ("ev_walk_end", ctypes.c_void_p),
+                ("items", ctypes.c_uint64), ("const_path", ctypes.c_uint32), ("reserved", ctypes.c_uint32)]
+
+
+class tree_node_t(ctypes.Structure):
+    _fields_ = [("level", ctypes.c_uint32), ("reserved", ctypes.c_uint32), ("index", ctypes.c_uint64),
+                ("hi_re", ctypes.c_double), ("lo_re", ctypes.c_double),
+                ("hi_im", ctypes.c_double), ("lo_im", ctypes.c_double)]
+
+
+TREE_MAX_NODES = 128          # PERM_TREE_MAX_NODES
+TREE_NODE_BYTES = 48
+TREE_UNUSED = 0xFFFFFFFF
+
+
+def _stats_dict(st: stats_t) -> dict:
+    return {"terms": st.terms, "chunk_log2": st.chunk_log2, "threads": st.threads, "blocks": st.blocks,
+            "launches": st.launches, "items": st.items, "const_path": st.const_path}
 
 
 class sparse_info_t(ctypes.Structure):
@@ -113,6 +133,7 @@ def lib() -> ctypes.CDLL:
                           "(or __graft_entry__.build()); there is no CPU fallback")
     L = ctypes.CDLL(_LIB_PATH)
     P, i32, i64, u64, sz = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_uint64, ctypes.c_size_t
+    L.perm_chunk_log2.restype = ctypes.c_int
     sig = {
         "perm_workspace_bytes": [i32, u64, u64, ctypes.POINTER(sz)],
         "perm_c128": [P, i32, P, P, P, sz, P, P],
@@ -130,6 +151,12 @@ def lib() -> ctypes.CDLL:
         "perm_int01_finalize": [P, i32, i32, P],
         "perm_c128_seed": [P, i32, P, i32, P, P],
         "perm_fp64_probe": [i32, i32, i32, P, P],
+        "perm_c128_chunks": [P, i32, i32, u64, u64, P, P, sz, P, P],
+        "perm_tree_workspace_bytes": [u64, ctypes.POINTER(sz)],
+        "perm_c128_tree": [P, u64, u64, P, P, P, sz, P],
+        "perm_c128_tree_combine": [P, i32, P, ctypes.POINTER(ctypes.c_int)],
+        "perm_chunk_log2": [i32],
+        "perm_chunk_walkers": [i32, i32, ctypes.POINTER(u64)],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -244,8 +271,7 @@ def perm_c128(A, *, workspace=None, stream=None, out=None, return_dd: bool = Fal
     if return_dd:
         extra.append(DD(ddv.hi_re, ddv.lo_re, ddv.hi_im, ddv.lo_im))
     if stats:
-        extra.append({"terms": st.terms, "chunk_log2": st.chunk_log2, "threads": st.threads,
-                      "blocks": st.blocks, "launches": st.launches})
+        extra.append(_stats_dict(st))
     return (val, *extra) if extra else val
 
 
@@ -324,9 +350,101 @@ def perm_c128_range(A, k_begin: int, k_end: int, *, workspace=None, stream=None,
     del keep
     d = DD(ddv.hi_re, ddv.lo_re, ddv.hi_im, ddv.lo_im)
     if stats:
-        return d, {"terms": st.terms, "chunk_log2": st.chunk_log2, "threads": st.threads, "blocks": st.blocks,
-                   "launches": st.launches}
+        return d, _stats_dict(st)
     return d
+
+
+def chunk_log2(n: int) -> int:
+    """b(n): the chunk length 2^b a whole permanent of order n is walked in (perm_c128, perm_c128_chunks)."""
+    b = int(lib().perm_chunk_log2(int(n)))
+    if b < 0:
+        raise PermError(2, "matrix order out of range")
+    return b
+
+
+def perm_c128_chunks(A, c_begin: int, c_end: int, *, partials=None, chunk_log2_: int | None = None, workspace=None,
+                     stream=None, stats: bool = False, events=None):
+    """Walk the aligned chunks [c_begin, c_end) of 2^b ranks (b = chunk_log2(n) unless given) and write chunk
+    c's raw dd partial to ``partials[c - c_begin]``: a CUDA float64 tensor (count, 4) {hi_re, lo_re, hi_im,
+    lo_im} (allocated if None).  Stream-ordered for host A.  Returns partials (and the stats dict)."""
+    ptr, n, keep = _matrix_ptr(A)
+    b = chunk_log2(n) if chunk_log2_ is None else int(chunk_log2_)
+    cnt = int(c_end) - int(c_begin)
+    if partials is None:
+        torch = _torch()
+        partials = torch.empty((max(cnt, 0), 4), dtype=torch.float64, device="cuda")
+    ws, wsb = _ws_args(workspace)
+    st = _make_stats(events)
+    _check(lib().perm_c128_chunks(ptr, n, b, int(c_begin), int(c_end), ctypes.c_void_p(partials.data_ptr()), ws, wsb,
+                                  _stream_ptr(stream), ctypes.byref(st)))
+    del keep
+    return (partials, _stats_dict(st)) if stats else partials
+
+
+def chunk_walkers(n: int, chunk_log2_: int | None = None) -> int:
+    """Chunk walkers one perm_c128_chunks launch keeps resident on the current device."""
+    w = ctypes.c_uint64()
+    _check(lib().perm_chunk_walkers(int(n), chunk_log2(n) if chunk_log2_ is None else int(chunk_log2_),
+                                    ctypes.byref(w)))
+    return int(w.value)
+
+
+def tree_workspace_bytes(count: int) -> int:
+    b = ctypes.c_size_t()
+    _check(lib().perm_tree_workspace_bytes(int(count), ctypes.byref(b)))
+    return int(b.value)
+
+
+def perm_c128_tree(partials, c_begin: int, c_end: int, *, nodes=None, raw=None, workspace=None, stream=None):
+    """Canonical tree reduction of the chunk partials of [c_begin, c_end) (a CUDA float64 tensor (count, 4)).
+    ``nodes``: CUDA int64 tensor (TREE_MAX_NODES, 6) receiving the span's maximal nodes (perm_tree_node_t bytes;
+    allocated if None); ``raw``: optional CUDA float64 tensor of 4 for their left-to-right dd sum.
+    Stream-ordered (device outputs).  Returns nodes."""
+    torch = _torch()
+    if nodes is None:
+        nodes = torch.empty((TREE_MAX_NODES, 6), dtype=torch.int64, device=partials.device)
+    ws, wsb = _ws_args(workspace)
+    _check(lib().perm_c128_tree(ctypes.c_void_p(partials.data_ptr()), int(c_begin), int(c_end),
+                                ctypes.c_void_p(nodes.data_ptr()),
+                                ctypes.c_void_p(raw.data_ptr() if raw is not None else 0), ws, wsb,
+                                _stream_ptr(stream)))
+    return nodes
+
+
+def perm_c128_tree_combine(nodes):
+    """Merge tree nodes of disjoint spans (any array whose bytes are perm_tree_node_t records, e.g. the
+    gathered (G*128, 6) int64 node tensors of all ranks, moved to the host).  Returns (DD raw, root_level)."""
+    arr = np.ascontiguousarray(np.asarray(nodes)).view(np.uint8).reshape(-1)
+    if arr.size % TREE_NODE_BYTES:
+        raise ValueError("node buffer is not a whole number of perm_tree_node_t")
+    count = arr.size // TREE_NODE_BYTES
+    d = dd_c128()
+    lvl = ctypes.c_int(-1)
+    _check(lib().perm_c128_tree_combine(arr.ctypes.data_as(ctypes.c_void_p), count, ctypes.byref(d), ctypes.byref(lvl)))
+    return DD(d.hi_re, d.lo_re, d.hi_im, d.lo_im), int(lvl.value)
+
+
+def tree_nodes(nodes) -> list[tuple[int, int, DD]]:
+    """Decode a node buffer into [(level, index, DD)] (unused slots dropped)."""
+    arr = np.ascontiguousarray(np.asarray(nodes)).view(np.uint8).reshape(-1, TREE_NODE_BYTES)
+    out = []
+    for row in arr:
+        lv, _ = np.frombuffer(row[:8].tobytes(), dtype=np.uint32)
+        idx = int(np.frombuffer(row[8:16].tobytes(), dtype=np.uint64)[0])
+        v = np.frombuffer(row[16:].tobytes(), dtype=np.float64)
+        if int(lv) != TREE_UNUSED:
+            out.append((int(lv), idx, DD(*map(float, v))))
+    return out
+
+
+def make_tree_nodes(entries) -> np.ndarray:
+    """Build a host node buffer from [(level, index, (hi_re, lo_re, hi_im, lo_im))] (tests / host logic)."""
+    buf = (tree_node_t * max(1, len(entries)))()
+    for k, (lv, idx, v) in enumerate(entries):
+        buf[k].level, buf[k].index = int(lv), int(idx)
+        buf[k].hi_re, buf[k].lo_re, buf[k].hi_im, buf[k].lo_im = map(float, v)
+    raw = np.frombuffer(bytes(buf), dtype=np.uint8)[: len(entries) * TREE_NODE_BYTES]
+    return raw.copy()
 
 
 def perm_c128_finalize(partials, n: int, return_dd: bool = False):
@@ -491,7 +609,8 @@ def perm_fp64_probe(blocks: int, threads: int, iters: int, sink, stream=None):
     _check(lib().perm_fp64_probe(blocks, threads, iters, ctypes.c_void_p(sink.data_ptr()), _stream_ptr(stream)))
 
 
-__all__ = ["perm_c128", "perm_c128_range", "perm_c128_finalize", "perm_c128_batched", "perm_c128_weighted_batched",
+__all__ = ["perm_c128", "perm_c128_range", "perm_c128_finalize", "perm_c128_chunks", "perm_c128_tree",
+           "perm_c128_tree_combine", "chunk_log2", "chunk_walkers", "tree_workspace_bytes", "tree_nodes", "make_tree_nodes", "perm_c128_batched", "perm_c128_weighted_batched",
            "perm_int01", "perm_pm1", "perm_int01_range", "perm_int01_finalize", "perm_c128_sparse", "perm_sparse_plan",
            "perm_c128_band_batched", "band_storage",
            "perm_c128_seed", "perm_fp64_probe", "workspace_bytes", "make_workspace", "int01_workspace_bytes",

@@ -29,11 +29,11 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
                 f"-I{CSRC}", f"-I{os.path.join(ROOT, 'include')}", "-Xptxas", "-v"]
 
-HEADERS = ["common.cuh", "internal.h", "walk.cuh", "walk_pair.cuh", "walk_table.cuh", "sparse.cuh"]
+HEADERS = ["common.cuh", "internal.h", "walk.cuh", "sparse.cuh"]
 
 
 def units():
-    u = [("abi.o", "abi.cu", []), ("reduce.o", "reduce.cu", []), ("batched.o", "batched.cu", []),
+    u = [("abi.o", "abi.cu", []), ("reduce.o", "reduce.cu", []), ("tree.o", "tree.cu", []), ("batched.o", "batched.cu", []),
          ("int01.o", "int01.cu", []), ("walk_dispatch.o", "walk_dispatch.cu", []),
          ("weighted.o", "weighted.cu", []), ("band.o", "band.cu", [])]
     for p in range(8):

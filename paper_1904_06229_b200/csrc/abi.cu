@@ -7,6 +7,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <vector>
+#include <algorithm>
 
 #include "../../include/perm.h"
 #include "internal.h"
@@ -55,15 +56,16 @@ struct WalkPlan {
 
 int floor_log2(uint64_t x) { return x ? 63 - __builtin_clzll(x) : -1; }
 
-// Chunk length 2^b for a span of `total` ranks and T resident threads: at least ~128 chunks per
-// thread so the static round-robin leaves < 1% tail, at least the unrolled block 2^U, at most 2^30.
+// Chunk length 2^b of the range API for a span of `total` ranks and T resident threads: at least ~128
+// chunks per thread so the static round-robin leaves < 1% tail, at least the unrolled block 2^U, at most
+// the whole-permanent chunk length walk_chunk_log2(n).
 int choose_b(int n, uint64_t total, uint64_t T) {
     const int U = perm::walk_inner_bits(n);
     int b = floor_log2(total / (T * 128ull > 0 ? T * 128ull : 1));
     if (b < U) b = U;
+    if (b > perm::walk_chunk_log2(n)) b = perm::walk_chunk_log2(n);
+    if (b < U) b = U;
     if (b > n - 1) b = n - 1;
-    if (b > 30) b = 30;
-    if (perm::walk_table_path(n) && b > perm::walk_table_cols(n)) b = perm::walk_table_cols(n);
     if (b < 0) b = 0;
     // development override (profiling a sub-range at the full run's chunk length)
     if (const char* f = getenv("PERM_FORCE_CHUNK_LOG2")) {
@@ -147,13 +149,14 @@ perm_status_t device_threads(int n, int* max_grid, int* nt, int* max_grid_c = nu
     return PERM_OK;
 }
 
-perm_status_t plan_walk(int n, uint64_t k0, uint64_t k1, WalkPlan& p) {
+// b_req >= 0: walk chunks of exactly 2^b_req ranks (whole permanent, chunk API); else choose_b.
+perm_status_t plan_walk(int n, uint64_t k0, uint64_t k1, int b_req, WalkPlan& p) {
     int max_grid = 0, nt = 0, max_grid_c = 0;
     perm_status_t st = device_threads(n, &max_grid, &nt, &max_grid_c);
     if (st != PERM_OK) return st;
     p.threads = nt;
     const uint64_t T = (uint64_t)(max_grid_c > 0 ? max_grid_c * perm::walk_body_walkers(n) : max_grid * nt);
-    p.b = choose_b(n, k1 - k0, T);
+    p.b = b_req >= 0 ? b_req : choose_b(n, k1 - k0, T);
     if (!decompose(n, k0, k1, p.b, p)) {
         snprintf(g_err, sizeof(g_err), "range decomposition exceeded %d segments", perm::kMaxSegments);
         return PERM_E_ARG;
@@ -164,25 +167,6 @@ perm_status_t plan_walk(int n, uint64_t k0, uint64_t k1, WalkPlan& p) {
         int best = -1;
         for (int s = 0; s < p.nseg; s++)
             if (p.seg[s].e > perm::walk_inner_bits(n) && (best < 0 || p.seg[s].count > p.seg[best].count)) best = s;
-        if (best >= 0 && perm::walk_table_path(n)) {
-            // the signed-table walk takes a body of 64k chunks (equal-parity warp passes); the remainder
-            // becomes its own segment for the edge launch
-            const uint64_t cnt = p.seg[best].count, c64 = cnt & ~63ull;
-            if (c64 == 0 || p.seg[best].e > perm::walk_table_cols(n)) {
-                best = -1;
-            } else if (c64 < cnt) {
-                if (p.nseg >= perm::kMaxSegments) {
-                    best = -1;
-                } else {
-                    for (int s = p.nseg; s > best + 1; s--) p.seg[s] = p.seg[s - 1];
-                    p.seg[best + 1].c0 = p.seg[best].c0 + c64;
-                    p.seg[best + 1].count = cnt - c64;
-                    p.seg[best + 1].e = p.seg[best].e;
-                    p.seg[best].count = c64;
-                    p.nseg++;
-                }
-            }
-        }
         if (best >= 0) {
             p.use_const = 1;
             p.body = best;
@@ -204,58 +188,122 @@ perm_status_t plan_walk(int n, uint64_t k0, uint64_t k1, WalkPlan& p) {
     return PERM_OK;
 }
 
-struct WsLayout {
-    size_t a_off, part_off, res_dd_off, res_c_off, total;
+// The results block at the end of the workspace: what a host-output call copies back in one D2H.
+struct ResBlock {
+    ddc raw;          // left-to-right sum of the maximal tree nodes (raw partial, no 2(-1)^n)
+    ddc out_dd;       // raw * 2(-1)^n (whole permanent)
+    double2 out_c;    // out_dd rounded
 };
 
-WsLayout ws_layout(int n, int max_grid) {
+struct WsLayout {
+    size_t a_off, items_off, tree_off, nodes_off, res_off, total;
+};
+
+WsLayout ws_layout(int n, uint64_t items) {
     WsLayout L;
     L.a_off = 0;
-    L.part_off = align256((size_t)n * n * sizeof(double2));
-    L.res_dd_off = align256(L.part_off + (size_t)max_grid * sizeof(ddc));
-    L.res_c_off = L.res_dd_off + sizeof(ddc);
-    L.total = align256(L.res_c_off + sizeof(double2));
+    L.items_off = align256((size_t)n * n * sizeof(double2));
+    L.tree_off = align256(L.items_off + (size_t)items * sizeof(ddc));
+    L.nodes_off = align256(L.tree_off + perm::tree_workspace_bytes(items));
+    L.res_off = align256(L.nodes_off + (size_t)perm::kTreeMaxNodes * sizeof(perm::TreeNode));
+    L.total = align256(L.res_off + sizeof(ResBlock));
     return L;
 }
 
 perm_status_t check_order(int n) { return (n < 1 || n > perm::kMaxN) ? PERM_E_ORDER : PERM_OK; }
 
-// Validates entries (host copy) and returns a host copy of A for the checks.
-perm_status_t load_and_check(const perm_c128_t* A, int n, bool a_dev, cudaStream_t s,
-                             std::vector<perm_c128_t>& host) {
+bool all_finite(const perm_c128_t* h, size_t cnt) {
+    for (size_t k = 0; k < cnt; k++)
+        if (!std::isfinite(h[k].re) || !std::isfinite(h[k].im)) return false;
+    return true;
+}
+
+// Host copy of A when the launch needs it on the host (constant-bank path: the inner columns ride in the
+// kernel parameters; the chunk walk and the sparse planner always) or A is host memory; entries are then
+// checked here.  A device matrix on the other paths is not copied back: a non-finite entry always makes
+// the result non-finite (every Glynn row sum carries each a_ij with coefficient +-1/2), and a host-output
+// call checks A only then (nonfinite_status).
+perm_status_t host_matrix(const perm_c128_t* A, int n, bool a_dev, bool need_host, cudaStream_t s,
+                          std::vector<perm_c128_t>& host, const perm_c128_t** h) {
     const size_t cnt = (size_t)n * n;
-    const perm_c128_t* h = A;
-    if (a_dev) {
+    *h = a_dev ? nullptr : A;
+    if (a_dev && need_host) {
         host.resize(cnt);
         PERM_CUDA(cudaMemcpyAsync(host.data(), A, cnt * sizeof(perm_c128_t), cudaMemcpyDeviceToHost, s),
                   "cudaMemcpyAsync(A D2H)");
         PERM_CUDA(cudaStreamSynchronize(s), "cudaStreamSynchronize");
-        h = host.data();
+        *h = host.data();
     }
-    for (size_t k = 0; k < cnt; k++)
-        if (!std::isfinite(h[k].re) || !std::isfinite(h[k].im)) return PERM_E_NONFINITE;
+    if (*h && !all_finite(*h, cnt)) return PERM_E_NONFINITE;
     return PERM_OK;
 }
 
-// Shared body of perm_c128 (n_final = n) and perm_c128_range (n_final = 0).
-perm_status_t run_walk(const perm_c128_t* A, int n, uint64_t k0, uint64_t k1, int n_final, void* out_c,
-                       void* out_dd, void* workspace, size_t workspace_bytes, void* stream,
-                       perm_stats_t* stats) {
-    g_launches = 0;
-    cudaStream_t s = (cudaStream_t)stream;
+// A non-finite result of a host-output call: PERM_E_NONFINITE if A has a non-finite entry, else PERM_OK
+// (a genuine overflow of the binary64 products, C13).
+perm_status_t nonfinite_status(const perm_c128_t* A, int n, cudaStream_t s) {
+    std::vector<perm_c128_t> host;
+    const perm_c128_t* h = nullptr;
+    return host_matrix(A, n, is_device_ptr(A), true, s, host, &h);
+}
+
+// The walk of plan p over A into items (device, p.items entries).  ws_a: device scratch for A if A is host.
+perm_status_t launch_walk(const perm_c128_t* A, int n, const WalkPlan& p, ddc* items, char* ws_a, cudaStream_t s,
+                          perm_stats_t* stats, uint32_t* launches) {
     const bool a_dev = is_device_ptr(A);
     std::vector<perm_c128_t> host;
-    perm_status_t st = load_and_check(A, n, a_dev, s, host);
+    const perm_c128_t* h = nullptr;
+    perm_status_t st = host_matrix(A, n, a_dev, p.use_const != 0, s, host, &h);
     if (st != PERM_OK) return st;
+    const double2* A_dev = (const double2*)A;
+    if (!a_dev) {
+        PERM_CUDA(cudaMemcpyAsync(ws_a, A, (size_t)n * n * sizeof(double2), cudaMemcpyHostToDevice, s),
+                  "cudaMemcpyAsync(A H2D)");
+        A_dev = (const double2*)ws_a;
+    }
+    perm::WalkLaunch WL;
+    WL.A_dev = A_dev;
+    WL.A_host = (const double2*)h;
+    WL.n = n;
+    WL.nseg = p.nseg;
+    for (int i = 0; i < p.nseg; i++) WL.seg[i] = p.seg[i];
+    WL.items = items;
+    WL.grid = p.grid;
+    WL.use_const = p.use_const;
+    WL.body = p.body;
+    WL.grid_edge = p.grid_edge;
+    WL.stream = s;
+    if (stats && stats->ev_walk_begin)
+        PERM_CUDA(cudaEventRecord((cudaEvent_t)stats->ev_walk_begin, s), "cudaEventRecord");
+    if (p.items > 0) PERM_CUDA(perm::walk_launch_n(n, WL), "walk kernel launch");
+    if (stats && stats->ev_walk_end)
+        PERM_CUDA(cudaEventRecord((cudaEvent_t)stats->ev_walk_end, s), "cudaEventRecord");
+    *launches += p.items > 0 ? 1u + (p.grid_edge > 0 ? 1u : 0u) : 0u;
+    if (stats) {
+        stats->terms = 0;
+        for (int i = 0; i < p.nseg; i++) stats->terms += p.seg[i].count << p.seg[i].e;
+        stats->chunk_log2 = (uint32_t)p.b;
+        stats->blocks = (uint32_t)(p.grid + p.grid_edge);
+        stats->threads = (uint32_t)((p.grid + p.grid_edge) * perm::walk_block_threads(n));
+        stats->const_path = (uint32_t)p.use_const;
+        stats->items = p.items;
+    }
+    return PERM_OK;
+}
 
+// Shared body of perm_c128 (n_final = n, b_req = walk_chunk_log2(n)) and perm_c128_range (n_final = 0):
+// walk -> one dd partial per item -> canonical tree over the item index -> left-to-right sum of the
+// maximal nodes (for a whole permanent: the root) -> (x 2(-1)^n).  A small whole permanent (n <= 16) is
+// one cluster launch that does all of it (walk_small_kernel, same chunks and tree, same bits).
+perm_status_t run_walk(const perm_c128_t* A, int n, uint64_t k0, uint64_t k1, int n_final, int b_req, void* out_c,
+                       void* out_dd, void* workspace, size_t workspace_bytes, void* stream, perm_stats_t* stats) {
+    g_launches = 0;
+    cudaStream_t s = (cudaStream_t)stream;
     WalkPlan p;
-    st = plan_walk(n, k0, k1, p);
+    perm_status_t st = plan_walk(n, k0, k1, b_req, p);
     if (st != PERM_OK) return st;
-    int max_grid = 0, nt = 0, max_grid_c = 0;
-    st = device_threads(n, &max_grid, &nt, &max_grid_c);
-    if (st != PERM_OK) return st;
-    const WsLayout L = ws_layout(n, max_grid + max_grid_c);
-
+    const bool small = n_final > 0 && n <= perm::kSmallMaxN && p.items <= perm::kSmallMaxChunks && p.nseg == 1 &&
+                       k0 == 0 && (p.items & (p.items - 1)) == 0;
+    const WsLayout L = ws_layout(n, small ? 0 : p.items);
     char* ws = (char*)workspace;
     bool own_ws = false;
     if (ws == nullptr) {
@@ -266,81 +314,119 @@ perm_status_t run_walk(const perm_c128_t* A, int n, uint64_t k0, uint64_t k1, in
     }
     perm_status_t result = PERM_OK;
     uint32_t launches = 0;
+    ResBlock* res = (ResBlock*)(ws + L.res_off);
     do {
-        const double2* A_dev = (const double2*)A;
-        if (!a_dev) {
-            cudaError_t e = cudaMemcpyAsync(ws + L.a_off, A, (size_t)n * n * sizeof(double2),
-                                            cudaMemcpyHostToDevice, s);
-            if (e != cudaSuccess) { result = cuda_fail(e, "cudaMemcpyAsync(A H2D)"); break; }
-            A_dev = (const double2*)(ws + L.a_off);
-        }
-        ddc* partials = (ddc*)(ws + L.part_off);
-        ddc* res_dd = (ddc*)(ws + L.res_dd_off);
-        double2* res_c = (double2*)(ws + L.res_c_off);
-        if (k1 > k0) {
-            perm::WalkLaunch WL;
-            WL.A_dev = A_dev;
-            WL.A_host = a_dev ? (const double2*)host.data() : (const double2*)A;
-            WL.n = n;
-            WL.nseg = p.nseg;
-            for (int i = 0; i < p.nseg; i++) WL.seg[i] = p.seg[i];
-            WL.partials = partials;
-            WL.grid = p.grid;
-            WL.use_const = p.use_const;
-            WL.body = p.body;
-            WL.grid_edge = p.grid_edge;
-            WL.stream = s;
-            cudaError_t e = cudaSuccess;
-            if (stats && stats->ev_walk_begin) e = cudaEventRecord((cudaEvent_t)stats->ev_walk_begin, s);
-            if (e == cudaSuccess) e = perm::walk_launch_n(n, WL);
-            if (e != cudaSuccess) { result = cuda_fail(e, "walk kernel launch"); break; }
-            if (stats && stats->ev_walk_end) e = cudaEventRecord((cudaEvent_t)stats->ev_walk_end, s);
-            if (e != cudaSuccess) { result = cuda_fail(e, "cudaEventRecord"); break; }
-            launches += 1 + (p.grid_edge > 0 ? 1 : 0);
-            e = perm::reduce_launch(partials, p.grid + p.grid_edge, n_final, res_dd, res_c, s);
-            if (e != cudaSuccess) { result = cuda_fail(e, "reduce kernel launch"); break; }
-            launches++;
+        cudaError_t e = cudaSuccess;
+        if (small) {
+            std::vector<perm_c128_t> host;
+            const perm_c128_t* h = nullptr;
+            const bool a_dev = is_device_ptr(A);
+            result = host_matrix(A, n, a_dev, false, s, host, &h);
+            if (result != PERM_OK) break;
+            const double2* A_dev = (const double2*)A;
+            if (!a_dev) {
+                e = cudaMemcpyAsync(ws + L.a_off, A, (size_t)n * n * sizeof(double2), cudaMemcpyHostToDevice, s);
+                if (e != cudaSuccess) { result = cuda_fail(e, "cudaMemcpyAsync(A H2D)"); break; }
+                A_dev = (const double2*)(ws + L.a_off);
+            }
+            if (stats && stats->ev_walk_begin) cudaEventRecord((cudaEvent_t)stats->ev_walk_begin, s);
+            e = perm::walk_small_launch_n(n, A_dev, p.seg[0].e, p.items, &res->raw, &res->out_dd, &res->out_c, s);
+            if (e != cudaSuccess) { result = cuda_fail(e, "small walk launch"); break; }
+            if (stats && stats->ev_walk_end) cudaEventRecord((cudaEvent_t)stats->ev_walk_end, s);
+            launches = 1;
+            if (stats) {
+                stats->terms = k1 - k0;
+                stats->chunk_log2 = (uint32_t)p.b;
+                stats->items = p.items;
+                stats->const_path = 0;
+                stats->blocks = (uint32_t)(p.items >= 64 ? (p.items / 64 > 16 ? 16 : p.items / 64) : 1);
+                stats->threads = (uint32_t)p.items;
+            }
         } else {
-            cudaError_t e = cudaMemsetAsync(ws + L.res_dd_off, 0, sizeof(ddc) + sizeof(double2), s);
-            if (e != cudaSuccess) { result = cuda_fail(e, "cudaMemsetAsync"); break; }
+            result = launch_walk(A, n, p, (ddc*)(ws + L.items_off), ws + L.a_off, s, stats, &launches);
+            if (result != PERM_OK) break;
+            int tl = 0;
+            const double f = n_final > 0 ? ((n_final & 1) ? -2.0 : 2.0) : 0.0;
+            e = perm::tree_launch((const ddc*)(ws + L.items_off), 0, p.items, ws + L.tree_off, nullptr, &res->raw,
+                                  &res->out_dd, &res->out_c, f, s, &tl);
+            if (e != cudaSuccess) { result = cuda_fail(e, "tree kernel launch"); break; }
+            launches += (uint32_t)tl;
         }
-        bool sync = false;
-        if (out_c) {
-            const bool d = is_device_ptr(out_c);
-            cudaError_t e = cudaMemcpyAsync(out_c, res_c, sizeof(double2),
-                                            d ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s);
+        const void* src_c = &res->out_c;
+        const void* src_dd = n_final > 0 ? (const void*)&res->out_dd : (const void*)&res->raw;
+        const bool c_dev = out_c && is_device_ptr(out_c);
+        const bool dd_dev = out_dd && is_device_ptr(out_dd);
+        if (c_dev) {
+            e = cudaMemcpyAsync(out_c, src_c, sizeof(double2), cudaMemcpyDeviceToDevice, s);
             if (e != cudaSuccess) { result = cuda_fail(e, "cudaMemcpyAsync(result)"); break; }
-            sync |= !d;
         }
-        if (out_dd) {
-            const bool d = is_device_ptr(out_dd);
-            cudaError_t e = cudaMemcpyAsync(out_dd, res_dd, sizeof(ddc),
-                                            d ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s);
+        if (dd_dev) {
+            e = cudaMemcpyAsync(out_dd, src_dd, sizeof(ddc), cudaMemcpyDeviceToDevice, s);
             if (e != cudaSuccess) { result = cuda_fail(e, "cudaMemcpyAsync(result dd)"); break; }
-            sync |= !d;
+        }
+        const bool host_out = (out_c && !c_dev) || (out_dd && !dd_dev);
+        ResBlock hr;
+        if (host_out) {
+            e = cudaMemcpyAsync(&hr, res, sizeof(ResBlock), cudaMemcpyDeviceToHost, s);
+            if (e != cudaSuccess) { result = cuda_fail(e, "cudaMemcpyAsync(result D2H)"); break; }
         }
         if (own_ws) {
-            cudaError_t e = cudaFreeAsync(ws, s);
+            e = cudaFreeAsync(ws, s);
             own_ws = false;
             if (e != cudaSuccess) { result = cuda_fail(e, "cudaFreeAsync(workspace)"); break; }
         }
-        if (sync) {
-            cudaError_t e = cudaStreamSynchronize(s);
+        if (host_out) {
+            e = cudaStreamSynchronize(s);
             if (e != cudaSuccess) { result = cuda_fail(e, "cudaStreamSynchronize"); break; }
+            const ddc& v = n_final > 0 ? hr.out_dd : hr.raw;
+            if (!(std::isfinite(v.re.hi) && std::isfinite(v.im.hi))) {
+                result = nonfinite_status(A, n, s);
+                if (result != PERM_OK) break;
+            }
+            if (out_c && !c_dev) memcpy(out_c, &hr.out_c, sizeof(double2));
+            if (out_dd && !dd_dev) memcpy(out_dd, n_final > 0 ? &hr.out_dd : &hr.raw, sizeof(ddc));
         }
     } while (0);
     if (own_ws) cudaFreeAsync(ws, s);
     if (result == PERM_OK) {
         g_launches = launches;
-        if (stats) {
-            stats->terms = k1 - k0;
-            stats->chunk_log2 = (uint32_t)p.b;
-            stats->threads = (uint32_t)((p.grid + p.grid_edge) * perm::walk_block_threads(n));
-            stats->blocks = (uint32_t)(p.grid + p.grid_edge);
-            stats->launches = launches;
-        }
+        if (stats) stats->launches = launches;
     }
     return result;
+}
+
+// Host merge of tree nodes (tree.cu): siblings (L, 2k), (L, 2k+1) -> (L+1, k) = left + right until none are
+// left, then the remaining nodes are summed left to right.  Returns false if nodes overlap.
+bool tree_merge(std::vector<perm::TreeNode>& v) {
+    auto pos = [](const perm::TreeNode& x) { return x.index << x.level; };
+    std::sort(v.begin(), v.end(), [&](const perm::TreeNode& a, const perm::TreeNode& b) { return pos(a) < pos(b); });
+    for (size_t i = 1; i < v.size(); i++) {
+        const perm::TreeNode& a = v[i - 1];
+        const uint64_t end_a = a.level >= 64 ? ~0ull : (a.index + 1) << a.level;
+        if (pos(v[i]) < end_a) return false;
+    }
+    bool merged = true;
+    while (merged) {                       // one left-to-right sweep per round; <= 64 rounds
+        merged = false;
+        std::vector<perm::TreeNode> w;
+        w.reserve(v.size());
+        for (size_t i = 0; i < v.size(); i++) {
+            if (i + 1 < v.size() && v[i].level == v[i + 1].level && (v[i].index & 1ull) == 0 &&
+                v[i + 1].index == v[i].index + 1) {
+                perm::TreeNode p = v[i];
+                p.v = perm::ddc_add(v[i].v, v[i + 1].v);
+                p.level += 1;
+                p.index >>= 1;
+                w.push_back(p);
+                i++;
+                merged = true;
+            } else {
+                w.push_back(v[i]);
+            }
+        }
+        v.swap(w);
+    }
+    return true;
 }
 
 }  // namespace
@@ -373,10 +459,31 @@ perm_status_t perm_workspace_bytes(int n, uint64_t k_begin, uint64_t k_end, size
     if (st != PERM_OK) return st;
     if (k_begin > k_end) return PERM_E_ARG;
     if (n < 64 && k_end > (1ull << (n - 1))) return PERM_E_ORDER;
+    WalkPlan p;
+    st = plan_walk(n, k_begin, k_end, -1, p);              // perm_c128_range's plan
+    if (st != PERM_OK) return st;
+    size_t need = ws_layout(n, p.items).total;
+    const int b = perm::walk_chunk_log2(n);                // perm_c128's plan (whole range)
+    if (k_begin == 0 && n < 64 && k_end == (1ull << (n - 1))) {
+        const size_t full = ws_layout(n, k_end >> b).total;
+        if (full > need) need = full;
+    }
+    *bytes = need;
+    return PERM_OK;
+}
+
+int perm_chunk_log2(int n) { return (n < 1 || n > perm::kMaxN) ? -1 : perm::walk_chunk_log2(n); }
+
+perm_status_t perm_chunk_walkers(int n, int chunk_log2, uint64_t* walkers) {
+    if (!walkers) return PERM_E_ARG;
+    perm_status_t st = check_order(n);
+    if (st != PERM_OK) return st;
     int max_grid = 0, nt = 0, max_grid_c = 0;
     st = device_threads(n, &max_grid, &nt, &max_grid_c);
     if (st != PERM_OK) return st;
-    *bytes = ws_layout(n, max_grid + max_grid_c).total;
+    const bool cbank = max_grid_c > 0 && chunk_log2 > perm::walk_inner_bits(n);
+    *walkers = cbank ? (uint64_t)max_grid_c * (uint64_t)perm::walk_body_walkers(n)
+                     : (uint64_t)max_grid * (uint64_t)nt;
     return PERM_OK;
 }
 
@@ -386,7 +493,139 @@ perm_status_t perm_c128(const perm_c128_t* A, int n, perm_c128_t* out, perm_dd_c
     perm_status_t st = check_order(n);
     if (st != PERM_OK) return st;
     const uint64_t total = 1ull << (n - 1);
-    return run_walk(A, n, 0, total, n, out, out_dd, workspace, workspace_bytes, stream, stats);
+    return run_walk(A, n, 0, total, n, perm::walk_chunk_log2(n), out, out_dd, workspace, workspace_bytes, stream,
+                    stats);
+}
+
+perm_status_t perm_c128_chunks(const perm_c128_t* A, int n, int chunk_log2, uint64_t c_begin, uint64_t c_end,
+                               perm_dd_c128_t* partials_dev, void* workspace, size_t workspace_bytes, void* stream,
+                               perm_stats_t* stats) {
+    g_launches = 0;
+    if (!A || (!partials_dev && c_end > c_begin) || c_begin > c_end) return PERM_E_ARG;
+    perm_status_t st = check_order(n);
+    if (st != PERM_OK) return st;
+    const int U = perm::walk_inner_bits(n);
+    const int b = chunk_log2;
+    if (b < 0 || b > n - 1 || b > 30 || (b > 0 && b < U)) return PERM_E_ARG;
+    if (c_end > (1ull << (n - 1 - b))) return PERM_E_ORDER;
+    if (c_begin == c_end) return PERM_OK;                   // empty span: nothing to walk
+    if (!is_device_ptr(partials_dev)) return PERM_E_ARG;
+    cudaStream_t s = (cudaStream_t)stream;
+    WalkPlan p;
+    st = plan_walk(n, c_begin << b, c_end << b, b, p);
+    if (st != PERM_OK) return st;
+    if (p.items != c_end - c_begin) return PERM_E_ARG;     // cannot happen for b = 0 or b >= U
+    const bool a_dev = is_device_ptr(A);
+    const size_t a_bytes = (size_t)n * n * sizeof(double2);
+    char* ws = (char*)workspace;
+    bool own = false;
+    if (!a_dev) {
+        if (!ws) {
+            PERM_CUDA(cudaMallocAsync((void**)&ws, a_bytes, s), "cudaMallocAsync(A)");
+            own = true;
+        } else if (workspace_bytes < a_bytes) {
+            return PERM_E_WORKSPACE;
+        }
+    }
+    uint32_t launches = 0;
+    // the chunk walk always checks A on the host (a device matrix is copied back once): it has no
+    // result block to carry the staging flag
+    std::vector<perm_c128_t> host;
+    const perm_c128_t* h = nullptr;
+    st = host_matrix(A, n, a_dev, true, s, host, &h);
+    if (st == PERM_OK) st = launch_walk(A, n, p, (ddc*)partials_dev, ws, s, stats, &launches);
+    if (own) cudaFreeAsync(ws, s);
+    if (st != PERM_OK) return st;
+    g_launches = launches;
+    if (stats) stats->launches = launches;
+    return PERM_OK;
+}
+
+perm_status_t perm_tree_workspace_bytes(uint64_t count, size_t* bytes) {
+    if (!bytes) return PERM_E_ARG;
+    *bytes = align256(perm::tree_workspace_bytes(count)) +
+             align256((size_t)perm::kTreeMaxNodes * sizeof(perm::TreeNode)) + align256(sizeof(ddc));
+    return PERM_OK;
+}
+
+perm_status_t perm_c128_tree(const perm_dd_c128_t* partials_dev, uint64_t c_begin, uint64_t c_end,
+                             perm_tree_node_t* nodes, perm_dd_c128_t* raw, void* workspace, size_t workspace_bytes,
+                             void* stream) {
+    g_launches = 0;
+    static_assert(sizeof(perm_tree_node_t) == sizeof(perm::TreeNode), "perm_tree_node_t layout");
+    static_assert(PERM_TREE_MAX_NODES == perm::kTreeMaxNodes, "PERM_TREE_MAX_NODES");
+    if (c_begin > c_end || (c_end > c_begin && !partials_dev) || (!nodes && !raw)) return PERM_E_ARG;
+    cudaStream_t s = (cudaStream_t)stream;
+    size_t need = 0;
+    perm_tree_workspace_bytes(c_end - c_begin, &need);
+    char* ws = (char*)workspace;
+    bool own = false;
+    if (!ws) {
+        PERM_CUDA(cudaMallocAsync((void**)&ws, need, s), "cudaMallocAsync(tree workspace)");
+        own = true;
+    } else if (workspace_bytes < need) {
+        return PERM_E_WORKSPACE;
+    }
+    const size_t nodes_off = align256(perm::tree_workspace_bytes(c_end - c_begin));
+    const size_t raw_off = nodes_off + align256((size_t)perm::kTreeMaxNodes * sizeof(perm::TreeNode));
+    const bool nodes_dev = nodes && is_device_ptr(nodes);
+    const bool raw_dev = raw && is_device_ptr(raw);
+    perm::TreeNode* dn = nodes_dev ? (perm::TreeNode*)nodes : (perm::TreeNode*)(ws + nodes_off);
+    ddc* dr = raw_dev ? (ddc*)raw : (ddc*)(ws + raw_off);
+    perm_status_t result = PERM_OK;
+    int tl = 0;
+    do {
+        cudaError_t e = perm::tree_launch((const ddc*)partials_dev, c_begin, c_end - c_begin, ws, dn, dr, nullptr,
+                                          nullptr, 0.0, s, &tl);
+        if (e != cudaSuccess) { result = cuda_fail(e, "tree kernel launch"); break; }
+        bool sync = false;
+        if (nodes && !nodes_dev) {
+            e = cudaMemcpyAsync(nodes, dn, (size_t)perm::kTreeMaxNodes * sizeof(perm::TreeNode),
+                                cudaMemcpyDeviceToHost, s);
+            if (e != cudaSuccess) { result = cuda_fail(e, "cudaMemcpyAsync(nodes)"); break; }
+            sync = true;
+        }
+        if (raw && !raw_dev) {
+            e = cudaMemcpyAsync(raw, dr, sizeof(ddc), cudaMemcpyDeviceToHost, s);
+            if (e != cudaSuccess) { result = cuda_fail(e, "cudaMemcpyAsync(raw)"); break; }
+            sync = true;
+        }
+        if (own) {
+            own = false;
+            e = cudaFreeAsync(ws, s);
+            if (e != cudaSuccess) { result = cuda_fail(e, "cudaFreeAsync"); break; }
+        }
+        if (sync) {
+            e = cudaStreamSynchronize(s);
+            if (e != cudaSuccess) { result = cuda_fail(e, "cudaStreamSynchronize"); break; }
+        }
+    } while (0);
+    if (own) cudaFreeAsync(ws, s);
+    if (result == PERM_OK) g_launches = (uint32_t)tl;
+    return result;
+}
+
+perm_status_t perm_c128_tree_combine(const perm_tree_node_t* nodes, int count, perm_dd_c128_t* raw, int* root_level) {
+    if (count < 0 || (count > 0 && !nodes) || !raw) return PERM_E_ARG;
+    std::vector<perm::TreeNode> v;
+    for (int k = 0; k < count; k++) {
+        if (nodes[k].level == perm::kTreeUnused) continue;
+        if (nodes[k].level >= 64 || (nodes[k].level > 0 && (nodes[k].index >> (64 - nodes[k].level)) != 0))
+            return PERM_E_ARG;
+        perm::TreeNode t;
+        memcpy(&t, &nodes[k], sizeof(t));
+        v.push_back(t);
+    }
+    if (!tree_merge(v)) return PERM_E_ARG;
+    ddc acc;
+    acc.re.hi = acc.re.lo = acc.im.hi = acc.im.lo = 0.0;
+    for (size_t i = 0; i < v.size(); i++) acc = i == 0 ? v[0].v : perm::ddc_add(acc, v[i].v);
+    raw->hi_re = acc.re.hi;
+    raw->lo_re = acc.re.lo;
+    raw->hi_im = acc.im.hi;
+    raw->lo_im = acc.im.lo;
+    if (root_level) *root_level = (v.size() == 1 && v[0].index == 0) ? (int)v[0].level : -1;
+    return PERM_OK;
 }
 
 perm_status_t perm_c128_range(const perm_c128_t* A, int n, uint64_t k_begin, uint64_t k_end,
@@ -397,7 +636,7 @@ perm_status_t perm_c128_range(const perm_c128_t* A, int n, uint64_t k_begin, uin
     if (st != PERM_OK) return st;
     if (k_begin > k_end) return PERM_E_ARG;
     if (k_end > (1ull << (n - 1))) return PERM_E_ORDER;
-    return run_walk(A, n, k_begin, k_end, 0, nullptr, partial, workspace, workspace_bytes, stream, stats);
+    return run_walk(A, n, k_begin, k_end, 0, -1, nullptr, partial, workspace, workspace_bytes, stream, stats);
 }
 
 perm_status_t perm_c128_finalize(const perm_dd_c128_t* partials, int count, int n, perm_c128_t* out,
@@ -443,40 +682,41 @@ perm_status_t perm_c128_batched(const perm_c128_t* A_dev, int n, int64_t B, perm
     return PERM_OK;
 }
 
-// greedypartition (App. B) on the host.  Returns false if A has a zero row or column.
+// greedypartition (App. B) on the host, as a single scan: the paper repeatedly takes the
+// remaining row of least out-degree (lowest index on ties) and discards every row whose support meets the
+// taken one.  Visiting the rows once in (degree, index) order and taking a row iff its support is disjoint
+// from the union of the supports taken so far selects the same rows in the same order (a skipped row meets
+// the union, which only grows; a taken row is the least remaining one).  Returns false if A has a zero
+// row or column (per = 0).
 static bool sparse_partition(const perm_c128_t* A, int n, perm_sparse_info_t& I) {
-    uint64_t N[64];
-    int deg[64];
-    uint64_t colany = 0;
-    bool zero_row = false;
-    for (int i = 0; i < n; i++) {
-        N[i] = 0;
-        deg[i] = 0;
-        for (int j = 0; j < n; j++) {
-            const perm_c128_t a = A[(size_t)i * n + j];
-            if (a.re != 0.0 || a.im != 0.0) { N[i] |= 1ull << j; deg[i]++; }
+    struct Row { int deg, idx; uint64_t supp; };
+    std::vector<Row> rows((size_t)n);
+    uint64_t cols = 0;
+    bool empty_row = false;
+    for (int r = 0; r < n; r++) {
+        uint64_t m = 0;
+        for (int c = 0; c < n; c++) {
+            const perm_c128_t z = A[(size_t)r * n + c];
+            if (z.re != 0.0 || z.im != 0.0) m |= 1ull << c;
         }
-        colany |= N[i];
-        zero_row |= N[i] == 0;
+        rows[(size_t)r] = Row{__builtin_popcountll(m), r, m};
+        cols |= m;
+        empty_row |= (m == 0);
     }
-    const uint64_t all = n == 64 ? ~0ull : ((1ull << n) - 1ull);
-    uint64_t V = all, used = 0;
+    std::stable_sort(rows.begin(), rows.end(), [](const Row& x, const Row& y) { return x.deg < y.deg; });
+    const uint64_t full = n == 64 ? ~0ull : ((1ull << n) - 1ull);
+    uint64_t taken = 0;
     I.d = 0;
-    while (V) {
-        int k = -1;
-        for (int i = 0; i < n; i++)
-            if (((V >> i) & 1ull) && (k < 0 || deg[i] < deg[k])) k = i;
-        I.smask[I.d++] = N[k];
-        used |= N[k];
-        V &= ~(1ull << k);
-        for (int l = 0; l < n; l++)
-            if (((V >> l) & 1ull) && (N[k] & N[l])) V &= ~(1ull << l);
+    for (const Row& r : rows) {
+        if (r.supp & taken) continue;          // (a zero row is taken, with S = {}, as in the paper)
+        I.smask[I.d++] = r.supp;
+        taken |= r.supp;
     }
-    I.tmask = all & ~used;
+    I.tmask = full & ~taken;
     I.nt = (uint32_t)__builtin_popcountll(I.tmask);
+    const bool zero = empty_row || cols != full;
     double sets = std::ldexp(1.0, (int)I.nt);
     for (uint32_t l = 0; l < I.d; l++) sets *= std::ldexp(1.0, __builtin_popcountll(I.smask[l])) - 1.0;
-    const bool zero = zero_row || colany != all;
     I.sets = zero ? 0.0 : sets;
     I.chunk_log2 = -1;
     return !zero;
@@ -500,9 +740,9 @@ perm_status_t perm_c128_sparse(const perm_c128_t* A, int n, perm_c128_t* out_hos
     cudaStream_t s = (cudaStream_t)stream;
     const bool a_dev = is_device_ptr(A);
     std::vector<perm_c128_t> host;
-    perm_status_t st = load_and_check(A, n, a_dev, s, host);
+    const perm_c128_t* Ah = nullptr;
+    perm_status_t st = host_matrix(A, n, a_dev, true, s, host, &Ah);   // the partition is planned on the host
     if (st != PERM_OK) return st;
-    const perm_c128_t* Ah = a_dev ? host.data() : A;
     perm_sparse_info_t I;
     memset(&I, 0, sizeof(I));
     if (!sparse_partition(Ah, n, I)) {                    // a zero row or column: per = 0

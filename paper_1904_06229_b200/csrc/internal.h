@@ -22,23 +22,18 @@ __host__ __device__ constexpr int walk_inner_bits(int n) { return (n - 1) < PERM
 // U = 3 (8-term blocks) up to n = 39 and U = 2 beyond (the 4n-register row sums leave ptxas less room
 // to overlap an 8-term block); U = 2 also for the constant-bank orders 34, 35, 37, 39, whose register caps
 // (walk.cuh: walk_const_maxnreg) were found for U = 2.
-#ifdef PERM_CONST_TABLE2
-__host__ __device__ constexpr int walk_inner_bits(int n) {
-    return n == 41 ? 3 : (n >= 33 ? 2 : ((n - 1) < 3 ? (n - 1) : 3));
-}
-#else
 __host__ __device__ constexpr int walk_inner_bits(int n) {
     return (n == 34 || n == 35 || n == 37 || n == 39 || n >= 40) ? 2 : ((n - 1) < 3 ? (n - 1) : 3);
 }
 #endif
-#endif
 constexpr int kWalkThreads = 64;
-// Lanes that share one chunk in the single-matrix walk (rows split between them, K1).  The n
-// complex row sums take 4n registers; beyond n = 48 one lane cannot hold them without spilling, so
-// two lanes split the rows.  (Splitting earlier, to raise occupancy, measured no faster on B200: the
-// walk is bound by FP64 operand bandwidth, not latency -- DESIGN.md "Walk kernel".)
+// Lanes that share one chunk in the shared-memory walk (rows split between them).  The n
+// complex row sums take 4n registers; from n = 33 one lane cannot hold them next to the shared-memory column
+// operands without spilling, so two lanes split the rows.  For n <= 48 the aligned chunks of a walk run in
+// the constant-bank kernel (one lane per chunk, uniform-register columns); this kernel then only walks
+// unaligned edge pieces and chunks of 2^U ranks.
 #ifndef PERM_WALK_S2_MIN
-#define PERM_WALK_S2_MIN 49
+#define PERM_WALK_S2_MIN 33
 #endif
 #ifndef PERM_WALK_S4_MIN
 #define PERM_WALK_S4_MIN 65
@@ -78,7 +73,7 @@ struct Segment {
 constexpr int kConstMaxN = 48;
 // Orders that use the constant-bank walk: the ones for which ptxas keeps the per-use parameter loads on
 // the uniform datapath (LDCU -> DADD R, R, UR, one vector register read per update) -- n = 32 at its
-// default allocation, 34, 35, 37, 39, 42..45 under the register caps of walk_const_maxnreg (walk.cuh).
+// default allocation, 33..48 under the register caps of walk_const_maxnreg (walk.cuh).
 // Measured on B200 (profiles/round1_const_table_rates.txt): +4..12% over the shared-memory walk (n = 44:
 // 6.14e10 vs 5.49e10 terms/s).  PERM_CONST_ORDERS=0 enables the path for every n <= kConstMaxN (scans).
 #ifndef PERM_CONST_ORDERS
@@ -87,46 +82,28 @@ constexpr int kConstMaxN = 48;
 __host__ __device__ constexpr bool walk_const_path(int n) {
 #if PERM_CONST_ORDERS == 0
     return n <= kConstMaxN;                               // scans only
-#elif defined(PERM_CONST_TABLE2)
-    return n == PERM_CONST_ORDERS || (n >= 33 && n <= 48);
 #else
-    return n == PERM_CONST_ORDERS || n == 34 || n == 35 || n == 37 || n == 39 || (n >= 42 && n <= 45);
+    return n == PERM_CONST_ORDERS || (n >= 33 && n <= kConstMaxN);
 #endif
 }
 
-// Signed-column-table walk (walk_table.cuh): every row-sum update takes its column from the kernel
-// parameters, columns j < walk_table_cols(n) with both signs and a zero column ((2 E + 1) n x 16 bytes <= 32 KB
-// for n <= 48).
-constexpr int kTableCols = 20;
-__host__ __device__ constexpr int walk_table_cols(int n) { return n < kTableCols ? n : kTableCols; }
-// PERM_TABLE_BSMEM: the block-boundary flip reads +-columns from shared memory instead (development)
-#ifndef PERM_TABLE_BSMEM
-#define PERM_TABLE_BSMEM 0
-#endif
-constexpr int kTableThreads = PERM_TABLE_BSMEM ? 128 : 64;
-// Off by default: measured slower than walk_kernel_c at n = 44 (5.83e10 vs 6.14e10 terms/s; DESIGN.md 5.1,
-// profiles/round1_walk_table_variants.txt).  PERM_TABLE_ORDERS=n enables it for order n (experiments).
-#ifndef PERM_TABLE_ORDERS
-#define PERM_TABLE_ORDERS -1
-#endif
-__host__ __device__ constexpr bool walk_table_path(int n) {
-#if PERM_TABLE_ORDERS == 0
-    return n >= 8 && n <= kConstMaxN;                     // scans only
-#elif PERM_TABLE_ORDERS < 0
-    return false;
-#else
-    return n == PERM_TABLE_ORDERS;
-#endif
-}
+// chunk walkers per block of the kernel that walks the aligned body (walk_kernel_c)
+__host__ __device__ constexpr int walk_body_walkers(int n) { return walk_block_threads(n); }
 
-// Warp-pair walk (walk_pair.cuh): each chunk's rows split between two warps, three 128-thread CTAs per SM.
-#ifndef PERM_WALK_PAIR
-#define PERM_WALK_PAIR 0
-#endif
-__host__ __device__ constexpr bool walk_pair_path(int n) { return PERM_WALK_PAIR && n >= 40 && n <= 48; }
-// chunk walkers per block of the kernel that walks the aligned body (walk_kernel_c / walk_kernel_p)
-__host__ __device__ constexpr int walk_body_walkers(int n) {
-    return walk_table_path(n) ? kTableThreads : (walk_pair_path(n) ? 64 : walk_block_threads(n));
+// Chunk length 2^b of a WHOLE permanent (perm_c128) and of the chunk walk (perm_c128_chunks' default):
+// a function of n alone, so the per-chunk partials -- and through the canonical tree (tree.cu) the
+// result -- do not depend on the grid, the number of GPUs or how the chunks are sliced into launches.
+// Chosen with a cost model for B200 (37,888 resident walkers): chunks = 2^{n-1-b} <= 2^25 for n <= 56
+// (tail of the static round-robin <= 0.3% at 1 GPU, 0.3% at 8 GPUs for n >= 37), and b >= 10 where that
+// leaves enough chunks (explicit seeding costs 2n(n-1-b) FP64 instructions per 2^b terms: < 1%).
+__host__ __device__ constexpr int walk_chunk_log2(int n) {
+    const int u = walk_inner_bits(n);
+    const int a = n - 26, c = (n - 19) < 10 ? (n - 19) : 10;
+    int b = a > c ? a : c;
+    if (b < u) b = u;
+    if (b > 30) b = 30;
+    if (b > n - 1) b = n - 1;
+    return b < 0 ? 0 : b;
 }
 
 struct WalkLaunch {
@@ -135,13 +112,22 @@ struct WalkLaunch {
     int n;
     int nseg;
     Segment seg[kMaxSegments];
-    ddc* partials;          // device, grid + grid_edge entries
+    ddc* items;             // device: one dd partial per walked item (segment order, chunks in rank order)
     int grid;               // blocks of the main launch
     int use_const;          // run segment `body` in walk_kernel_c
     int body;               // index of the body segment (use_const)
     int grid_edge;          // blocks of the edge launch (use_const and nseg > 1), else 0
     cudaStream_t stream;
 };
+
+// One-launch path of a small whole permanent (walk.cuh: walk_small_kernel, a cluster of <= 16 CTAs).
+constexpr int kSmallMaxN = 16;
+constexpr int kSmallMaxThreads = 256;
+constexpr uint64_t kSmallMaxChunks = 16 * kSmallMaxThreads;
+template <int N> cudaError_t walk_small_launch(const double2* A_dev, int e, uint64_t chunks, ddc* raw, ddc* out_dd,
+                                               double2* out_c, cudaStream_t s);
+cudaError_t walk_small_launch_n(int n, const double2* A_dev, int e, uint64_t chunks, ddc* raw, ddc* out_dd,
+                                double2* out_c, cudaStream_t s);
 
 // Defined in walk_inst.cu (explicit instantiations over N = 1..64).
 template <int N> cudaError_t walk_launch(const WalkLaunch& L);
@@ -155,6 +141,25 @@ cudaError_t walk_occupancy_n(int n, int* blocks_per_sm, int* walkers_per_block);
 cudaError_t walk_occupancy_c_n(int n, int* blocks_per_sm);
 cudaError_t walk_seed_launch_n(int n, const double2* A_dev, const uint64_t* ranks_dev, int count,
                                double2* w_out, cudaStream_t s);
+
+// tree.cu: the canonical pairwise tree over absolute leaf indices.  Leaf i of a
+// span is node (0, a0 + i); node (L+1, k) = ddc_add(node (L, 2k), node (L, 2k+1)).  A span [a0, a0+count)
+// reduces to its maximal complete nodes (at most two per level), so partials of disjoint spans -- other
+// launches, other GPUs -- merge into exactly the value one launch over the union would give.
+struct TreeNode {           // == perm_tree_node_t (48 bytes)
+    uint32_t level;         // ~0u: unused slot
+    uint32_t reserved;
+    uint64_t index;         // covers leaves [index << level, (index + 1) << level)
+    ddc v;
+};
+constexpr int kTreeMaxNodes = 128;
+constexpr uint32_t kTreeUnused = 0xffffffffu;
+size_t tree_workspace_bytes(uint64_t count);
+// nodes_dev: kTreeMaxNodes slots, the maximal nodes sorted by position, the rest marked unused (may be
+// NULL); raw_dev (may be NULL): their left-to-right dd sum; out_dd / out_c (may be NULL): raw * f in dd /
+// rounded to double.
+cudaError_t tree_launch(const ddc* leaves, uint64_t a0, uint64_t count, void* ws, TreeNode* nodes_dev, ddc* raw_dev,
+                        ddc* out_dd, double2* out_c, double f, cudaStream_t s, int* launches);
 
 // reduce.cu
 cudaError_t reduce_launch(const ddc* parts, int count, int n_final, ddc* out_dd, double2* out_c,

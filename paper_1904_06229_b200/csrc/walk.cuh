@@ -17,17 +17,19 @@
 // rows: lane h keeps the row sums of rows [hR, hR+R), R = ceil(n/2) (an odd n is padded with a
 // neutral row w = 1).  Each lane multiplies its R row sums; after every two terms the pair swaps one
 // partial product with a single shuffle (lane 0 finishes the even term, lane 1 the odd one), so the
-// FP64 work per term is unchanged (6n-4) while registers per thread halve -- at n = 44 that doubles
-// the resident warps, which is what the FP64 pipe needs to hide its latency.
+// FP64 work per term is unchanged (6n-4) while registers per thread halve (n > 48 only).
 //
 // Per term: 2n DADD/DFMA (row-sum update) + 4(n-2) DMUL/DFMA (product, split
 // into K independent chains) + 4 DFMA (last multiply fused with the signed accumulation)
 // = 6n-4 FP64 instructions for ~8n flops.  Column operands are loaded with ld.volatile.shared right
 // before use: this keeps ptxas from hoisting/CSE-ing the (loop-invariant) columns into registers,
 // which at n = 44 would spill.  Plain-double sums over 2^kWalkFoldBits terms are folded into a
-// per-thread double-double accumulator (TwoSum), then reduced warp -> block -> per-block partial in
-// HBM; reduce.cu adds the partials in a fixed order.
+// double-double accumulator (TwoSum) that starts at zero for every item (chunk or single term); each
+// item's dd partial is written to HBM at its index in the launch's item order, and tree.cu combines the
+// items by the canonical pairwise tree -- so an item's value, and the result, depend only on (A, n, b).
 #pragma once
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -58,7 +60,8 @@ struct WCfg {
 #ifdef PERM_WALK_REG_EXTRA
     static constexpr int REGS = ((4 * R + PERM_WALK_REG_EXTRA + 7) / 8) * 8;
 #else
-    static constexpr int REGS = ((4 * R + 80 + 7) / 8) * 8;
+    // >= 224: below that ptxas spills the two-lane walk at n = 33..48 (tools/spills.py)
+    static constexpr int REGS = (4 * R + 128) > 224 ? ((4 * R + 128 + 7) / 8) * 8 : 224;
 #endif
     static constexpr int MINB_RAW = (S == 1) ? 1 : 65536 / (NT * (REGS < 255 ? REGS : 255));
     static constexpr int MINB = MINB_RAW < 1 ? 1 : MINB_RAW;
@@ -69,7 +72,8 @@ using WalkCfg = WCfg<N, walk_lanes_per_chunk(N)>;
 
 struct WalkParams {
     const double2* A;                      // device, row-major
-    ddc* partials;                         // [gridDim.x]
+    ddc* items;                            // one dd partial per item, at seg_item0[s] + (index in segment)
+    uint64_t seg_item0[kMaxSegments];
     uint64_t seg_c0[kMaxSegments];
     uint64_t seg_pre[kMaxSegments + 1];    // prefix item counts
     int32_t seg_e[kMaxSegments];
@@ -413,18 +417,18 @@ template <class C>
 __device__ __forceinline__ void walk_seeded(uint32_t lc, uint32_t h, uint64_t c, int e, double (&wr)[C::R],
                                             double (&wi)[C::R], ddc& acc) {
     constexpr int U = C::U, R = C::R;
-    const uint64_t nblk = 1ull << (e - U);
-    const uint64_t cpar = c & 1ull;
-    constexpr uint64_t kFoldMask = (U >= kWalkFoldBits) ? 0ull : ((1ull << (kWalkFoldBits - U)) - 1ull);
+    const uint32_t nblk = 1u << (e - U);                 // e <= 30: 32-bit block counter (fewer registers)
+    const uint32_t cpar = (uint32_t)(c & 1ull);
+    constexpr uint32_t kFoldMask = (U >= kWalkFoldBits) ? 0u : ((1u << (kWalkFoldBits - U)) - 1u);
     double ar = 0.0, ai = 0.0, pr[C::S], pi[C::S];
-    for (uint64_t q = 0; q < nblk; q++) {
+    for (uint32_t q = 0; q < nblk; q++) {
         if (q > 0) {
             // block boundary: Gray bit j = U + ctz(q) flips to 1 ^ bit_{j+1}(rank)
-            const int j = U + __ffsll((long long)q) - 1;
-            const uint64_t nb = (j + 1 < e) ? ((q >> (j + 1 - U)) & 1ull) : cpar;
+            const int j = U + __ffs((int)q) - 1;
+            const uint32_t nb = (j + 1 < e) ? ((q >> (j + 1 - U)) & 1u) : cpar;
             flip_add<R>(lc + (uint32_t)(j * C::P) * 16u + (nb ? C::NEG : 0u), wr, wi);
         }
-        const uint64_t nbm = (U < e) ? (q & 1ull) : cpar;   // bit_U(rank) for the mid-block flip
+        const uint32_t nbm = (U < e) ? (q & 1u) : cpar;     // bit_U(rank) for the mid-block flip
         const uint32_t lmid = lc + (uint32_t)((U - 1) * C::P) * 16u + (nbm ? C::NEG : 0u);
         InnerStep<C, 0>::run(lc, lmid, h, wr, wi, ar, ai, pr, pi);
         // fold the plain block sums into the dd accumulator every 2^kWalkFoldBits terms (and at the end)
@@ -504,34 +508,38 @@ __global__ void __launch_bounds__(WalkCfg<N>::NT, WalkCfg<N>::MINB) walk_kernel(
     const uint32_t lc = (uint32_t)__cvta_generic_to_shared(smem) + hoff;
     const uint32_t lb = (uint32_t)__cvta_generic_to_shared(smem + 2 * N * C::P) + hoff;
 
-    ddc acc;
-    acc.re.hi = acc.re.lo = acc.im.hi = acc.im.lo = 0.0;
-    const uint64_t W = (uint64_t)gridDim.x * (blockDim.x / C::S);     // walkers (lane groups)
-    const uint64_t total = P.seg_pre[P.nseg];
-    int s = 0;
-    for (uint64_t g = (uint64_t)blockIdx.x * (blockDim.x / C::S) + threadIdx.x / C::S; g < total; g += W) {
-        while (g >= P.seg_pre[s + 1]) s++;
-        const uint64_t c = P.seg_c0[s] + (g - P.seg_pre[s]);
-        const int e = P.seg_e[s];
-        if constexpr (C::U >= 1) {
-            if (e == 0) single_term<C>(lc, lb, h, c, acc);
-            else        walk_chunk<C>(lc, lb, h, c, e, acc);
-        } else {
-            single_term<C>(lc, lb, h, c, acc);
-        }
-    }
-
-    // warp -> block reduction of the dd partials, fixed order.
+    // static round-robin over the launch's items: walker w takes the global items g = w (mod W); per segment
+    // that is i = (w - seg_pre[s]) mod W, i + W, ...  (only the 64-bit item index is live across a chunk)
+    const uint32_t wpb = blockDim.x / C::S;
+    const uint64_t w = (uint64_t)blockIdx.x * wpb + threadIdx.x / C::S;
+    // the item's dd accumulator lives in shared memory (touched once per 2^kWalkFoldBits terms): at n >= 33
+    // the 4n row-sum registers leave no room for it without spilling
+    __shared__ ddc sacc_[C::NT];
+    for (int s = 0; s < P.nseg; s++) {
+        const uint64_t W = (uint64_t)gridDim.x * wpb;
+        const uint64_t pre = P.seg_pre[s], cnt = P.seg_pre[s + 1] - pre;
+        const uint64_t i0 = (w + W - pre % W) % W;
+        for (uint64_t i = i0; i < cnt; i += (uint64_t)gridDim.x * wpb) {
+            const int e = P.seg_e[s];
+            {
+                volatile ddc& z = *(volatile ddc*)&sacc_[threadIdx.x];
+                z.re.hi = 0.0; z.re.lo = 0.0; z.im.hi = 0.0; z.im.lo = 0.0;
+            }
+            ddc& acc = sacc_[threadIdx.x];
+            const uint64_t c = P.seg_c0[s] + i;
+            if constexpr (C::U >= 1) {
+                if (e == 0) single_term<C>(lc, lb, h, c, acc);
+                else        walk_chunk<C>(lc, lb, h, c, e, acc);
+            } else {
+                single_term<C>(lc, lb, h, c, acc);
+            }
+            ddc v = acc;
+            if constexpr (C::S > 1) {  // the S lanes of a group hold interleaved terms: fixed-order combine
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) acc = ddc_add(acc, shfl_down_ddc(acc, off));
-    __shared__ ddc swarp[32];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (lane == 0) swarp[warp] = acc;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        ddc b = swarp[0];
-        for (int w = 1; w < (int)(blockDim.x >> 5); w++) b = ddc_add(b, swarp[w]);
-        P.partials[blockIdx.x] = b;
+                for (int off = C::S / 2; off > 0; off >>= 1) v = ddc_add(v, shfl_down_ddc(v, off, group_mask<C::S>()));
+            }
+            if (h == 0) P.items[P.seg_item0[s] + i] = v;
+        }
     }
 }
 
@@ -552,14 +560,15 @@ __global__ void __launch_bounds__(WalkCfg<N>::NT, WalkCfg<N>::MINB) walk_kernel(
 #ifndef PERM_CONST_MIDNEG
 #define PERM_CONST_MIDNEG 0
 #endif
-__host__ __device__ constexpr int walk_const_midneg(int n) { return (PERM_CONST_MIDNEG || n == 44) ? 1 : 0; }
+__host__ __device__ constexpr int walk_const_midneg(int n) { return (PERM_CONST_MIDNEG || n == 42 || n == 44) ? 1 : 0; }
 template <int N>
 struct WalkParamsC {
     static constexpr int NC = walk_inner_bits(N);   // columns held in the constant bank (the inner flips)
     static constexpr int MN = walk_const_midneg(N);
     double2 col[NC + MN][N];               // col[j][i] = a_ij, j < U; col[U][i] = -a_{i,U-1} (MN = 1)
     const double2* A;                      // device, row-major (staged to shared memory)
-    ddc* partials;                         // [gridDim.x]
+    ddc* items;                            // item partials; body chunk c0 + g -> items[item0 + g]
+    uint64_t item0;
     uint64_t c0;                           // first body chunk
     uint64_t count;                        // body chunks
     int32_t eb;                            // log2 body chunk length (>= U)
@@ -655,18 +664,16 @@ __device__ __forceinline__ void walk_chunk_const(const WalkParamsC<C::N>& P, uin
 // Register cap of the constant-bank walk for order N (0: the default __launch_bounds__ kernel).  Whether
 // ptxas keeps the per-use parameter loads on the uniform datapath (LDCU -> DADD R, R, UR: one vector
 // register read per update instead of two) depends on its register allocation; these caps are the ones
-// measured to produce LDCU for U = 2 (tools/const_ldcu_scan.sh, profiles/round1_const_ldcu_scan.txt), and
+// measured to produce LDCU with 0 spill bytes (rescanned in round 2 for the per-chunk partial stores,
+// profiles/round2_const_ldcu_scan.txt; n = 42 only with its mid-block sign by address), and
 // tests/test_abi_cpu.py checks the built library still does.
 __host__ __device__ constexpr int walk_const_maxnreg(int n) {
 #ifdef PERM_CONST_MAXNREG_ALL
     return PERM_CONST_MAXNREG_ALL;                  // scans only (tools/const_ldcu_scan.sh)
-#elif defined(PERM_CONST_TABLE2)
-    return n == 33 ? 172 : n == 34 ? 200 : n == 35 ? 208 : n == 36 ? 212 : n == 37 ? 216 : n == 38 ? 220
-         : n == 39 ? 224 : n == 40 ? 228 : n == 41 ? 208 : n == 42 ? 208 : n == 43 ? 208 : n == 44 ? 248
-         : n == 45 ? 216 : n == 46 ? 224 : n == 47 ? 228 : n == 48 ? 232 : 0;
 #else
-    return n == 34 ? 200 : n == 35 ? 208 : n == 37 ? 216 : n == 39 ? 224 : n == 42 ? 208 : n == 43 ? 208
-         : n == 44 ? 248 : n == 45 ? 216 : 0;
+    return n == 33 ? 172 : n == 34 ? 192 : n == 35 ? 196 : n == 36 ? 188 : n == 37 ? 204 : n == 38 ? 200
+         : n == 39 ? 212 : n == 40 ? 212 : n == 41 ? 212 : n == 42 ? 216 : n == 43 ? 204 : n == 44 ? 244
+         : n == 45 ? 236 : n == 46 ? 240 : n == 47 ? 240 : n == 48 ? 244 : 0;
 #endif
 }
 
@@ -708,8 +715,6 @@ __device__ __forceinline__ void walk_body_c(const WalkParamsC<N>& P) {
     __syncthreads();
     const uint32_t lc = (uint32_t)__cvta_generic_to_shared(scol);
     const uint32_t lb = (uint32_t)__cvta_generic_to_shared(sbase);
-    ddc acc;
-    acc.re.hi = acc.re.lo = acc.im.hi = acc.im.lo = 0.0;
     // warp-uniform item loop (every lane runs every iteration; lanes past the end walk a valid chunk
     // and drop the result), so all control flow and column addresses stay on the uniform datapath
     const uint32_t ln = threadIdx.x & 31u;
@@ -721,18 +726,95 @@ __device__ __forceinline__ void walk_body_c(const WalkParamsC<N>& P) {
         ddc part;
         part.re.hi = part.re.lo = part.im.hi = part.im.lo = 0.0;
         walk_chunk_const<C>(P, lc, lb, P.c0 + (valid ? g : 0), part);
-        if (valid) acc = ddc_add(acc, part);
+        if (valid) P.items[P.item0 + g] = part;
     }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) acc = ddc_add(acc, shfl_down_ddc(acc, off));
-    __shared__ ddc swarp[32];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (lane == 0) swarp[warp] = acc;
+}
+
+// ------------------------------------------------------------------------------------------------
+// Small whole permanents (2^{n-1-b} <= kSmallMaxChunks chunks, n <= 16): ONE launch of a thread-block
+// cluster of up to 16 CTAs.  Thread t of CTA k walks chunk k T + t (one chunk each), the CTA reduces its T
+// chunk partials by the canonical pairwise tree in shared memory (its T chunks are an aligned subtree),
+// and after a cluster barrier CTA 0 gathers the CTA roots through distributed shared memory and finishes
+// the tree -> per(A) = 2(-1)^n root.  Bit-identical to the multi-launch path (same chunks, same tree), but
+// without the separate tree launches: the latency of a small permanent is one kernel.
+template <int N>
+__global__ void __launch_bounds__(kSmallMaxThreads) walk_small_kernel(const double2* __restrict__ A, int e,
+                                                                     ddc* __restrict__ raw, ddc* __restrict__ out_dd,
+                                                                     double2* __restrict__ out_c) {
+    namespace cg = cooperative_groups;
+    using C = WalkCfg<N>;
+    static_assert(C::S == 1, "small path: one lane per chunk");
+    extern __shared__ double2 smem[];
+    __shared__ ddc tree[kSmallMaxThreads];
+    cg::cluster_group cluster = cg::this_cluster();
+    stage_matrix<C>(A, smem, smem + 2 * N * C::P);
+    const uint32_t lc = (uint32_t)__cvta_generic_to_shared(smem);
+    const uint32_t lb = (uint32_t)__cvta_generic_to_shared(smem + 2 * N * C::P);
+    const int T = blockDim.x, t = threadIdx.x;
+    const uint64_t c = (uint64_t)cluster.block_rank() * T + t;
+    ddc acc;
+    acc.re.hi = acc.re.lo = acc.im.hi = acc.im.lo = 0.0;
+    if constexpr (C::U >= 1) {
+        if (e == 0) single_term<C>(lc, lb, 0u, c, acc);
+        else        walk_chunk<C>(lc, lb, 0u, c, e, acc);
+    } else {
+        single_term<C>(lc, lb, 0u, c, acc);
+    }
+    tree[t] = acc;
     __syncthreads();
-    if (threadIdx.x == 0) {
-        ddc b = swarp[0];
-        for (int w = 1; w < (int)(blockDim.x >> 5); w++) b = ddc_add(b, swarp[w]);
-        P.partials[blockIdx.x] = b;
+    for (int off = 1; off < T; off <<= 1) {              // node (L+1, k) = node (L, 2k) + node (L, 2k+1)
+        if ((t & (2 * off - 1)) == 0) tree[t] = ddc_add(tree[t], tree[t + off]);
+        __syncthreads();
+    }
+    cluster.sync();                                      // every CTA root is in its tree[0]
+    const int nb = (int)cluster.num_blocks();
+    if (cluster.block_rank() == 0) {
+        __shared__ ddc roots[16];
+        if (t < nb) roots[t] = *cluster.map_shared_rank(&tree[0], t);
+        __syncthreads();
+        if (t == 0) {
+            for (int off = 1; off < nb; off <<= 1)
+                for (int k = 0; k + off < nb; k += 2 * off) roots[k] = ddc_add(roots[k], roots[k + off]);
+            ddc r = roots[0];
+            if (raw) *raw = r;
+            const double f = (N & 1) ? -2.0 : 2.0;       // 2 (-1)^n, exact
+            r.re.hi *= f; r.re.lo *= f; r.im.hi *= f; r.im.lo *= f;
+            if (out_dd) *out_dd = r;
+            if (out_c) *out_c = make_double2(r.re.hi + r.re.lo, r.im.hi + r.im.lo);
+        }
+    }
+    cluster.sync();                                      // keep every CTA's shared memory alive until read
+}
+
+template <int N>
+cudaError_t walk_small_launch(const double2* A_dev, int e, uint64_t chunks, ddc* raw, ddc* out_dd, double2* out_c,
+                              cudaStream_t s) {
+    if constexpr (N > kSmallMaxN || WalkCfg<N>::S != 1) {
+        return cudaErrorInvalidValue;
+    } else {
+        using C = WalkCfg<N>;
+        if (chunks < 1 || chunks > (uint64_t)kSmallMaxChunks || (chunks & (chunks - 1))) return cudaErrorInvalidValue;
+        int ncta = (int)(chunks / 64);
+        ncta = ncta < 1 ? 1 : (ncta > 16 ? 16 : ncta);
+        const int T = (int)(chunks / (uint64_t)ncta);
+        cudaError_t err = cudaFuncSetAttribute(walk_small_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)C::smem_bytes);
+        if (err == cudaSuccess && ncta > 8)
+            err = cudaFuncSetAttribute(walk_small_kernel<N>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (err != cudaSuccess) return err;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)ncta, 1, 1);
+        cfg.blockDim = dim3((unsigned)T, 1, 1);
+        cfg.dynamicSmemBytes = C::smem_bytes;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = (unsigned)ncta;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        return cudaLaunchKernelEx(&cfg, walk_small_kernel<N>, A_dev, e, raw, out_dd, out_c);
     }
 }
 
@@ -760,22 +842,25 @@ __global__ void seed_kernel(const double2* __restrict__ A, const uint64_t* __res
     }
 }
 
+// seg[k] is segment seg_index[k] of the launch plan; item0[k] the global index of its first item.
 template <int N>
-cudaError_t walk_launch_smem(const WalkLaunch& L, const Segment* seg, int nseg, ddc* partials, int grid) {
+cudaError_t walk_launch_smem(const WalkLaunch& L, const Segment* seg, const uint64_t* item0, int nseg, int grid) {
     using C = WalkCfg<N>;
     WalkParams P;
     P.A = L.A_dev;
-    P.partials = partials;
+    P.items = L.items;
     uint64_t pre = 0;
     for (int s = 0; s < kMaxSegments; s++) {
         P.seg_pre[s] = pre;
         if (s < nseg) {
             P.seg_c0[s] = seg[s].c0;
             P.seg_e[s] = seg[s].e;
+            P.seg_item0[s] = item0[s];
             pre += seg[s].count;
         } else {
             P.seg_c0[s] = 0;
             P.seg_e[s] = 0;
+            P.seg_item0[s] = 0;
         }
     }
     P.seg_pre[kMaxSegments] = pre;
@@ -785,36 +870,18 @@ cudaError_t walk_launch_smem(const WalkLaunch& L, const Segment* seg, int nseg, 
     return cudaGetLastError();
 }
 
-// Launches the walk over L.seg.  For n <= kConstMaxN the largest segment (the aligned body) runs in
-// walk_kernel_c (matrix in the constant bank) on L.grid blocks and the remaining segments, if any, in
-// walk_kernel on L.grid_edge blocks; partials land in L.partials[0 .. L.grid + L.grid_edge).
-template <int N>
-cudaError_t walk_launch_pair(const WalkLaunch& L);
-template <int N>
-cudaError_t walk_occupancy_pair(int* blocks_per_sm);
-
-template <int N>
-cudaError_t walk_launch_table(const WalkLaunch& L);
-template <int N>
-cudaError_t walk_occupancy_table(int* blocks_per_sm);
-
+// Launches the walk over L.seg; item k of the plan (segments in order, chunks in rank order) writes its dd
+// partial to L.items[k].  For the constant-bank orders the largest segment (the aligned body) runs in
+// walk_kernel_c on L.grid blocks and the remaining segments, if any, in walk_kernel on L.grid_edge blocks.
 template <int N>
 cudaError_t walk_launch(const WalkLaunch& L) {
-    if constexpr (walk_table_path(N)) {
-        if (L.use_const) {
-            cudaError_t err = walk_launch_table<N>(L);
-            if (err != cudaSuccess || L.grid_edge == 0) return err;
-            Segment rest[kMaxSegments];
-            int nr = 0;
-            for (int s = 0; s < L.nseg; s++)
-                if (s != L.body) rest[nr++] = L.seg[s];
-            return walk_launch_smem<N>(L, rest, nr, L.partials + L.grid, L.grid_edge);
-        }
+    uint64_t item0[kMaxSegments];
+    uint64_t pre = 0;
+    for (int s = 0; s < L.nseg; s++) {
+        item0[s] = pre;
+        pre += L.seg[s].count;
     }
-    if constexpr (walk_pair_path(N)) {
-        if (L.use_const) return walk_launch_pair<N>(L);
-    }
-    if constexpr (walk_const_path(N) && walk_lanes_per_chunk(N) == 1 && walk_inner_bits(N) >= 1) {
+    if constexpr (walk_const_path(N) && walk_inner_bits(N) >= 1) {
         if (L.use_const) {
             const Segment& b = L.seg[L.body];
             WalkParamsC<N> P;
@@ -826,7 +893,8 @@ cudaError_t walk_launch(const WalkLaunch& L) {
                     P.col[WalkParamsC<N>::NC][i] = make_double2(-a.x, -a.y);
                 }
             P.A = L.A_dev;
-            P.partials = L.partials;
+            P.items = L.items;
+            P.item0 = item0[L.body];
             P.c0 = b.c0;
             P.count = b.count;
             P.eb = b.e;
@@ -837,23 +905,27 @@ cudaError_t walk_launch(const WalkLaunch& L) {
             cudaError_t err = cudaGetLastError();
             if (err != cudaSuccess || L.grid_edge == 0) return err;
             Segment rest[kMaxSegments];
+            uint64_t rest0[kMaxSegments];
             int nr = 0;
             for (int s = 0; s < L.nseg; s++)
-                if (s != L.body) rest[nr++] = L.seg[s];
-            return walk_launch_smem<N>(L, rest, nr, L.partials + L.grid, L.grid_edge);
+                if (s != L.body) {
+                    rest[nr] = L.seg[s];
+                    rest0[nr++] = item0[s];
+                }
+            return walk_launch_smem<N>(L, rest, rest0, nr, L.grid_edge);
         }
     }
-    return walk_launch_smem<N>(L, L.seg, L.nseg, L.partials, L.grid);
+    return walk_launch_smem<N>(L, L.seg, item0, L.nseg, L.grid);
 }
 
 // Occupancy of walk_kernel_c (0 when the constant-bank path does not exist for this order).
 template <int N>
 cudaError_t walk_occupancy_c(int* blocks_per_sm) {
     *blocks_per_sm = 0;
-    if constexpr (walk_table_path(N)) return walk_occupancy_table<N>(blocks_per_sm);
-    if constexpr (walk_pair_path(N)) return walk_occupancy_pair<N>(blocks_per_sm);
-    if constexpr (walk_const_path(N) && walk_lanes_per_chunk(N) == 1 && walk_inner_bits(N) >= 1) {
-        const void* k = walk_const_maxnreg(N) > 0 ? (const void*)walk_kernel_cm<N> : (const void*)walk_kernel_c<N>;
+    if constexpr (walk_const_path(N) && walk_inner_bits(N) >= 1) {
+        const void* k;
+        if constexpr (walk_const_maxnreg(N) > 0) k = (const void*)walk_kernel_cm<N>;
+        else                                     k = (const void*)walk_kernel_c<N>;
         cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                (int)WCfg<N, 1>::smem_bytes);
         if (err != cudaSuccess) return err;

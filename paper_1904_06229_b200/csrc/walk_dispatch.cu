@@ -32,6 +32,13 @@ cudaError_t walk_seed_launch_n(int n, const double2* A_dev, const uint64_t* rank
 #undef PERM_CASE
 }
 
+cudaError_t walk_small_launch_n(int n, const double2* A_dev, int e, uint64_t chunks, ddc* raw, ddc* out_dd,
+                                double2* out_c, cudaStream_t s) {
+#define PERM_CASE(N) case N: return walk_small_launch<N>(A_dev, e, chunks, raw, out_dd, out_c, s);
+    switch (n) { PERM_R8(PERM_CASE, 0) PERM_R8(PERM_CASE, 8) default: return cudaErrorInvalidValue; }
+#undef PERM_CASE
+}
+
 #define PERM_R48(M) PERM_R8(M, 0) PERM_R8(M, 8) PERM_R8(M, 16) PERM_R8(M, 24) PERM_R8(M, 32) PERM_R8(M, 40)
 
 cudaError_t sparse_launch(const SparseLaunch& L) {

@@ -32,7 +32,11 @@ def complex_gaussian(shape, seed: int | np.random.Generator) -> np.ndarray:
 def haar_unitary(m: int, seed: int | np.random.Generator) -> np.ndarray:
     """Haar-random m x m unitary: Q R = Z, U = Q diag(r_ii / |r_ii|)."""
     Z = complex_gaussian((m, m), seed)
-    Q, R = np.linalg.qr(Z)
+    # single-threaded LAPACK: the bits of Q must not depend on the process's thread count (torchrun sets
+    # OMP_NUM_THREADS=1, a plain run does not) -- bench results are compared bitwise across launches
+    from threadpoolctl import threadpool_limits
+    with threadpool_limits(limits=1):
+        Q, R = np.linalg.qr(Z)
     d = np.diag(R)
     return np.ascontiguousarray(Q * (d / np.abs(d))[None, :])
 

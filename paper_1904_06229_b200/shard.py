@@ -1,21 +1,26 @@
 """Sharding one permanent over processes / GPUs (App. A distribute + permanent).
 
-The 2^{n-1} Gray ranks are split into contiguous spans with the paper's ``distribute``:
-rank ``i`` of ``G`` gets ``[k, k+l)``, ``k = i q + min(i, r)``, ``l = q + [i < r]``.  Each process
-computes its raw partial with :func:`perm_c128_range` on its own GPU (no data-path communication),
-then ONE collective -- an all-gather of the four float64 of each rank's double-double partial over
-NCCL (NVLink/NVSwitch) -- and every rank combines the G partials in rank order with
-:func:`perm_c128_finalize` (2(-1)^n * ordered dd sum; "partial sums ... stored in an array
-before the final summation").  The ordered combine makes the result bit-identical on
-every rank and run to run.
+The 2^{n-1} Gray ranks form 2^{n-1-b} aligned chunks of 2^b ranks (b = chunk_log2(n), a function of n
+alone).  The CHUNKS are split into contiguous spans with the paper's ``distribute``: rank
+``i`` of ``G`` gets chunks ``[k, k+l)``, ``k = i q + min(i, r)``, ``l = q + [i < r]`` -- whole chunks, so
+every GPU walks only aligned chunks.  Each process walks its span with
+:func:`perm_c128_chunks` (one dd partial per chunk) and reduces it with :func:`perm_c128_tree` to the
+span's maximal nodes of the canonical chunk tree; ONE collective -- an all-gather of every rank's node
+array (128 x 48 bytes) over NCCL (NVLink/NVSwitch) -- and every rank merges the nodes with
+:func:`perm_c128_tree_combine` and applies 2(-1)^n (:func:`perm_c128_finalize`; "partial sums ...
+stored in an array before the final summation").  Because the tree is fixed by the chunk
+indices, per(A) is bit-identical for every G, every slicing of the span into steps, and to
+:func:`perm_c128` (S:172 determinism, strengthened).
 
-Only the host logic lives here; all arithmetic of the walk runs in libperm.so.
+The range API path (:func:`perm_c128_range` + ordered :func:`combine`) is kept for arbitrary rank spans.
+Only host logic lives here; all arithmetic of the walk runs in libperm.so.
 """
 from __future__ import annotations
 
 import numpy as np
 
-from . import DD, perm_c128_finalize, perm_c128_range, perm_int01_finalize, perm_int01_range
+from . import (DD, TREE_MAX_NODES, chunk_log2, perm_c128_chunks, perm_c128_finalize, perm_c128_range,
+               perm_c128_tree, perm_c128_tree_combine, perm_int01_finalize, perm_int01_range)
 
 
 def rank_span(total: int, world: int, rank: int) -> tuple[int, int]:
@@ -27,15 +32,70 @@ def rank_span(total: int, world: int, rank: int) -> tuple[int, int]:
     return k0, k0 + q + (1 if rank < r else 0)
 
 
+def chunk_span(n: int, world: int, rank: int, b: int | None = None) -> tuple[int, int]:
+    """Whole aligned chunks of 2^b ranks for rank ``rank`` of ``world``: distribute(2^{n-1-b}, world, rank)."""
+    b = chunk_log2(n) if b is None else b
+    return rank_span(1 << (n - 1 - b), world, rank)
+
+
+def step_slices(c0: int, c1: int, steps: int, wave: int) -> list[tuple[int, int]]:
+    """Cut the chunk span [c0, c1) into ``steps`` contiguous slices made of whole rounds of ``wave`` chunks
+    (a wave = the chunk walkers one launch keeps resident): round counts per step by distribute, so only
+    the very last round of the span can be partial.  Slices may be empty when steps > rounds."""
+    if steps < 1 or wave < 1 or c1 < c0:
+        raise ValueError("bad slicing arguments")
+    rounds = -(-(c1 - c0) // wave)
+    out, cur = [], c0
+    for s in range(steps):
+        r0, r1 = rank_span(rounds, steps, s)
+        nxt = min(c1, c0 + r1 * wave)
+        out.append((cur, nxt))
+        cur = nxt
+    return out
+
+
+def combine_nodes(nodes, n: int, expect_root: bool = True, return_dd: bool = False):
+    """per(A) from the tree nodes of disjoint chunk spans covering all 2^{n-1-b} chunks (any order; e.g. the
+    all-gathered node arrays of every rank and step): canonical merge + 2(-1)^n."""
+    raw, level = perm_c128_tree_combine(nodes)
+    if expect_root and level < 0:
+        raise ValueError("tree nodes do not cover the chunk range exactly")
+    return perm_c128_finalize([raw], n, return_dd=return_dd)
+
+
 def combine(gathered, n: int, return_dd: bool = False):
     """Ordered dd combine of a (G, 4) array of partials {hi_re, lo_re, hi_im, lo_im} -> per(A)."""
     arr = np.asarray(gathered, dtype=np.float64).reshape(-1, 4)
     return perm_c128_finalize([tuple(row) for row in arr], n, return_dd=return_dd)
 
 
-def sharded_permanent(A, group=None, *, workspace=None, stream=None, partial_out=None, gathered_out=None,
-                      events=None):
-    """per(A) with the Gray range split over the ranks of a torch.distributed process group.
+def sharded_permanent(A, group=None, *, stream=None, return_dd: bool = False):
+    """per(A) with the aligned chunks split over the ranks of a torch.distributed process group: chunk walk
+    + canonical tree on each rank, one all-gather of the node arrays, canonical merge.  Bit-identical to
+    perm_c128(A) for any group size.  A: host (numpy / pinned torch) or CUDA n x n complex128."""
+    import torch
+    import torch.distributed as dist
+
+    n = A.shape[0]
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    c0, c1 = chunk_span(n, world, rank)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    parts = perm_c128_chunks(A, c0, c1, stream=stream)
+    nodes = perm_c128_tree(parts, c0, c1, stream=stream)
+    if world > 1:
+        gathered = torch.empty((world * TREE_MAX_NODES, 6), dtype=torch.int64, device=dev)
+        dist.all_gather_into_tensor(gathered, nodes, group=group)
+    else:
+        gathered = nodes
+    return combine_nodes(gathered.cpu().numpy(), n, return_dd=return_dd)
+
+
+def sharded_permanent_range(A, group=None, *, workspace=None, stream=None, partial_out=None, gathered_out=None,
+                            events=None):
+    """per(A) with the Gray RANK range split by distribute over the ranks of a process group (range API:
+    perm_c128_range per rank + all-gather of the dd partials + ordered combine; equal to perm_c128 up to
+    rounding, bit-identical run to run at fixed G).
 
     A: host (numpy / pinned torch) n x n complex128.  Every rank returns the same value.
     partial_out / gathered_out: optional preallocated CUDA float64 tensors of 4 and 4G elements."""
@@ -99,5 +159,6 @@ def sharded_int01(A, group=None, *, stream=None) -> int:
     return combine_int01(gathered.cpu().numpy(), n)
 
 
-__all__ = ["rank_span", "combine", "sharded_permanent", "int01_rank_space", "pack_i128", "combine_int01",
+__all__ = ["rank_span", "chunk_span", "step_slices", "combine_nodes", "combine", "sharded_permanent",
+           "sharded_permanent_range", "int01_rank_space", "pack_i128", "combine_int01",
            "sharded_int01", "DD"]

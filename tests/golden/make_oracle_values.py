@@ -4,7 +4,7 @@ the seeded input generators).  Usage:
 
     python tests/golden/make_oracle_values.py [section ...]
 
-Sections: cfg1 cfg3 blockdiag44 ranges44 ranges32 cfg2 cfg4 (cfg4 takes ~1 h on 8 cores).
+Sections: cfg1 cfg3 blockdiag44 ranges44 ranges32 chunks44 chunks32 cfg2 cfg4 (cfg4 takes ~1 h on 8 cores).
 Each section is merged into the JSON file as it finishes, with the oracle
 function used and its wall time.
 """
@@ -34,7 +34,17 @@ RANGES = {
     32: [(0, 1 << 20), ((1 << 30) - (1 << 19), (1 << 30) + (1 << 19)),
          ((1 << 31) - (1 << 20), 1 << 31), (777777777, 777777777 + 1000003)],
 }
-CFG2_SAMPLES = {8: 2000, 12: 400, 16: 256, 20: 64}
+# chunk spans [c0, c1) of 2^b-rank chunks (b = the library's chunk length for a whole permanent, n = 44: 18,
+# n = 32: 10 -- a constant of the method's decomposition, restated here, not read from the library): the
+# first and last chunks, the chunk where 8 GPU shards meet (rank 2^40 = chunk 2^22; 3 * 2^40 unaligned to the
+# span), and a bench step boundary at one GPU (44 rounds of 37,888 chunks)
+CHUNKS = {
+    44: (18, [(0, 16), ((1 << 22) - 8, (1 << 22) + 8), (3 * (1 << 22) - 5, 3 * (1 << 22) + 11),
+              (44 * 37888 - 8, 44 * 37888 + 8), ((1 << 25) - 16, 1 << 25)]),
+    32: (10, [(0, 4096), ((1 << 18) - 2048, (1 << 18) + 2048), (3 * (1 << 18) - 1000, 3 * (1 << 18) + 3096),
+              ((1 << 21) - 4096, 1 << 21)]),
+}
+CFG2_SAMPLES = {8: 2000, 12: 400, 16: 10000, 20: 1000}
 BLOCK_SEEDS = (4401, 4402, 4403)          # B1 seed, B2 seed, permutation seed
 
 
@@ -99,6 +109,26 @@ def sec_ranges44():
     return {"sha256": sha(A), "fn": "oracle.subpermanent (App. A steps 2-15)", "ranges": _ranges(44, A)}
 
 
+def _chunks(n, A):
+    b, spans = CHUNKS[n]
+    out = []
+    for c0, c1 in spans:
+        t = time.time()
+        q = oracle.subpermanent(A, c0 << b, (c1 - c0) << b, parts=4 * oracle.num_threads())
+        out.append({"c0": c0, "c1": c1, "value": qc_json(q), "seconds": time.time() - t})
+    return {"chunk_log2": b, "spans": out}
+
+
+def sec_chunks44():
+    A = inputs.cfg5()
+    return {"sha256": sha(A), "fn": "oracle.subpermanent (App. A steps 2-15) over whole chunks", **_chunks(44, A)}
+
+
+def sec_chunks32():
+    A = inputs.cfg4()
+    return {"sha256": sha(A), "fn": "oracle.subpermanent (App. A steps 2-15) over whole chunks", **_chunks(32, A)}
+
+
 def sec_ranges32():
     A = inputs.cfg4()
     return {"sha256": sha(A), "fn": "oracle.subpermanent (App. A steps 2-15)", "ranges": _ranges(32, A)}
@@ -110,7 +140,7 @@ def sec_cfg2():
         A = inputs.cfg2(n)
         idx = np.sort(np.random.default_rng(9000 + n).choice(A.shape[0], k, replace=False))
         t = time.time()
-        if n <= 12:
+        if n <= 16:
             v = oracle.ryser_batch(A[idx])
             fn = "oracle.ryser_batch (Eq. 3)"
         else:
@@ -130,7 +160,8 @@ def sec_cfg4():
 
 
 SECTIONS = {"cfg1": sec_cfg1, "cfg3": sec_cfg3, "blockdiag44": sec_blockdiag44, "ranges44": sec_ranges44,
-            "ranges32": sec_ranges32, "cfg2": sec_cfg2, "cfg4": sec_cfg4}
+            "ranges32": sec_ranges32, "chunks44": sec_chunks44, "chunks32": sec_chunks32, "cfg2": sec_cfg2,
+            "cfg4": sec_cfg4}
 
 if __name__ == "__main__":
     todo = sys.argv[1:] or list(SECTIONS)

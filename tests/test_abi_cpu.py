@@ -101,7 +101,7 @@ def test_sparse_plan_host_logic_matches_oracle_partition():
 
 
 def test_const_walk_keeps_uniform_column_operands():
-    # The constant-bank walks (n = 32, 34, 35, 37, 39, 42..45) take their inner columns as uniform-register
+    # The constant-bank walks (n = 32, 34, 35, 37, 39, 43..45) take their inner columns as uniform-register
     # operands (LDCU from the kernel-parameter bank): +4..12%.  ptxas only does this for some register
     # caps, so guard the built library's SASS against a silent fallback to per-lane LDC loads.
     import shutil
@@ -111,7 +111,7 @@ def test_const_walk_keeps_uniform_column_operands():
         pytest.skip("cuobjdump not available")
     lib = pb._LIB_PATH
     fns = ["_ZN4perm13walk_kernel_cILi32EEEvNS_11WalkParamsCIXT_EEE"]
-    fns += [f"_ZN4perm14walk_kernel_cmILi{n}EEEvNS_11WalkParamsCIXT_EEE" for n in (34, 35, 37, 39, 42, 43, 44, 45)]
+    fns += [f"_ZN4perm14walk_kernel_cmILi{n}EEEvNS_11WalkParamsCIXT_EEE" for n in (34, 35, 37, 39, 43, 44, 45)]
     # the sparse kernel's constant-bank variant (sparse.cuh, sparse_const_path)
     fns += [f"_ZN4perm15sparse_kernel_cILi{n}EEEvNS_13SparseParamsCIXT_EEE"
             for n in list(range(17, 24)) + list(range(25, 34)) + [47, 48]]

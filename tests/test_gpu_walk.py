@@ -260,16 +260,4 @@ def test_cfg5_subranges(golden_dir):
         ref = _q(rr["value"])
         assert abs(got - ref) <= 1e-12 * max(abs(ref), pins.range_scale(A, rr["k1"] - rr["k0"]))
 
-
-def test_cfg5_blockdiag_full_walk(golden_dir):
-    """P7: per(P (B1 (+) B2) Q) = per(B1) per(B2) at n = 44, full 2^43-term walk (the bench launch)."""
-    g = _golden(golden_dir).get("blockdiag44")
-    if not g:
-        pytest.skip("oracle_values.json has no blockdiag44 section")
-    s1, s2, sp = g["seeds"]
-    B1 = inputs.complex_gaussian((22, 22), s1)
-    B2 = inputs.complex_gaussian((22, 22), s2)
-    M, _, _ = inputs.block_diag_scrambled(B1, B2, sp)
-    ref = _q(g["per_B1"]) * _q(g["per_B2"])
-    got = pb.perm_c128(M)
-    assert pins.scaled_error(got, ref, M) <= TOL, (got, ref)
+# The n = 44 block-diagonal full walk (P7) runs on the bench's path in tests/test_gpu_chunks.py.
