@@ -17,6 +17,8 @@ Workloads (BASELINE.json configs; synthetic inputs from paper_1904_06229_b200/in
   cfgbd: 10^4 band matrices, n = 100, k = 5, App. C transfer method (NEXT-4); perms/s.
   cfgsp: one sparse 48x48 complex matrix (4% + a matching), App. B restricted enumeration (NEXT-3); sets/s.
   cfgpm: 1024 Bernoulli +-1 matrices of order 24 (Sec. V ensemble); exact; perms/s.
+  cfgens: 10^4 Ginibre + 10^4 circular matrices of order 24 (Secs. III-IV ensembles; NEXT-2), X = |per|/sqrt(n!)
+          streamed per matrix; perms/s and the sample moments of X.
   cfgw: 10^4 Boson-sampling output patterns with collisions (20 photons, 20 modes), weighted Ryser
         Eq. (4) (not a BASELINE config); perms/s.
 
@@ -234,6 +236,16 @@ def oracle_rate_cfg(cfg: str, seconds: float = 12.0) -> dict:
         per_step = sum(r * 100000 for r in rates)      # seconds for 4 x 10^5 permanents
         return {"value": 400000 / per_step, "unit": "perms/s", "cores": cores, "kind": "oracle",
                 "sample": "Eq. (3)/App. A binary128 oracle on the first config-2 submatrices; " + "; ".join(parts)}
+    if cfg == "cfgens":
+        Gm, Cm = inputs.cfgens(count=64)
+        t0 = time.perf_counter()
+        k = 0
+        while time.perf_counter() - t0 < seconds and k < 64:
+            oracle.ryser_batch(np.stack([Gm[k], Cm[k]]))
+            k += 1
+        dt = time.perf_counter() - t0
+        return {"value": 2 * k / dt, "unit": "perms/s", "cores": cores, "kind": "oracle",
+                "sample": f"Eq. (3) binary128 oracle on the first {k} Ginibre + {k} circular cfgens matrices, {dt:.1f} s"}
     if cfg == "cfg3":
         A = inputs.cfg3()
         t0 = time.perf_counter()
@@ -496,6 +508,51 @@ def run_ours(args):
         scaling = "weak" if world > 1 else "strong"
         if world > 1:
             units_per_step = count * len(ns)   # every rank does its share of the same global batch
+    elif cfg == "cfgens":
+        # NEXT-2: the Sec. III-IV ensembles streamed through the batched kernel with the X = |per|/sqrt(n!) output
+        Gm, Cm = inputs.cfgens()
+        B, n = Gm.shape[0], Gm.shape[1]
+        b0, b1 = shard.rank_span(B, world, rank)
+        hosts = [torch.from_numpy(np.ascontiguousarray(M[b0:b1])).pin_memory() for M in (Gm, Cm)]
+        devs = [h.to(device) for h in hosts]
+        xs = [torch.empty(b1 - b0, dtype=torch.float64, device=device) for _ in hosts]
+        xs_host = [torch.empty(b1 - b0, dtype=torch.float64).pin_memory() for _ in hosts]
+        e0, e1 = ev(), ev()
+        h2d = sum(h.numel() * 16 for h in hosts)
+        d2h = sum(x.numel() * 8 for x in xs_host)
+        walk_launches_per_step = 2
+        ens_stats = {}
+
+        def step():
+            e0.record(stream)
+            for dv, x in zip(devs, xs):
+                pb.perm_c128_batched_x(dv, x=x, stream=stream)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            es = torch.cuda.Event(enable_timing=True)
+            ee = torch.cuda.Event(enable_timing=True)
+            es.record(stream)
+            for h, dv, x, xh in zip(hosts, devs, xs, xs_host):
+                dv.copy_(h, non_blocking=True)
+                pb.perm_c128_batched_x(dv, x=x, stream=stream)
+                xh.copy_(x, non_blocking=True)
+            ee.record(stream)
+            torch.cuda.synchronize()
+            for name, xh in zip(("ginibre", "circular"), xs_host):
+                X = xh.numpy()
+                ens_stats[name] = {"mean_X": float(X.mean()), "mean_X2": float((X ** 2).mean()),
+                                   "mean_X4": float((X ** 4).mean()), "count": int(X.size)}
+            return {"dev": e0.elapsed_time(e1), "e2e": es.elapsed_time(ee), "walk": e0.elapsed_time(e1),
+                    "result": ens_stats["circular"]["mean_X2"]}
+
+        units_per_step = 2 * B
+        unit = "perms/s"
+        gpu_launches_per_step = 2 * 2
+        config = {"workload": f"Sec. III-IV ensembles: {B} Ginibre + {B} circular (exp(i theta)) matrices of order {n} "
+                              f"(seeds {inputs.SEEDS['cfgens_g']}, {inputs.SEEDS['cfgens_c']}), X = |per|/sqrt(n!) "
+                              "streamed per matrix", "batch": 2 * B, "n": n, "parallelism": f"batch x{world}",
+                  "l2": "inputs 184 MB > L2"}
+        scaling = "weak" if world > 1 else "strong"
     elif cfg in ("cfg3", "cfgpm"):
         pm1 = cfg == "cfgpm"
         A_np = inputs.bernoulli_pm1((1024, 24, 24), inputs.SEEDS["cfgpm"]) if pm1 else inputs.cfg3()
@@ -783,6 +840,15 @@ def run_ours(args):
                                "kernel": "weighted_kernel<20> (FP64 vector pipe)",
                                "algorithmic": "8n flops per Eq. (4) term x prod_k (m_k+1) terms per pattern",
                                "peak_measured_probe": peak_meas}
+        elif cfg == "cfgens":
+            fl = 2 * (b1 - b0) * (1 << (n - 1)) * 8 * n
+            achieved = fl / (dev_ms / K * 1e-3) / 1e12
+            out["roofline"] = {"bound": "alu", "achieved": achieved, "peak": nominal, "unit": "TFLOP/s",
+                               "frac": achieved / nominal, "traffic": ncu_traffic(cfg),
+                               "kernel": f"batched_kernel<{n}> x2 (FP64 vector pipe)",
+                               "algorithmic": "8n flops per Gray term x 2^(n-1) terms x matrices",
+                               "peak_measured_probe": peak_meas}
+            out["ensemble"] = ens_stats
         elif cfg == "cfg2":
             fl = sum(100000 / world * (1 << (n - 1)) * 8 * n for n in (8, 12, 16, 20))
             achieved = fl / (dev_ms / K * 1e-3) / 1e12
@@ -827,7 +893,7 @@ def run_reference(args):
     if rank != 0:
         return          # the reference arm runs on rank 0 only
     cfg = args.config
-    unit = "perms/s" if cfg in ("cfg2", "cfg3", "cfgw", "cfgpm", "cfgbd") else "terms/s"
+    unit = "perms/s" if cfg in ("cfg2", "cfg3", "cfgw", "cfgpm", "cfgbd", "cfgens") else "terms/s"
     for _ in range(max(0, args.warmup)):
         oracle_rate_cfg(cfg, seconds=1.0)
     rates, samples = [], []
@@ -856,7 +922,7 @@ def main():
     ap.add_argument("--steps", type=int, default=1)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="cfg5", choices=["cfg1", "cfg2", "cfg3", "cfg3s", "cfg4", "cfg5", "cfgw", "cfgpm",
-                                                          "cfgsp", "cfgbd"])
+                                                          "cfgsp", "cfgbd", "cfgens"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)

@@ -195,6 +195,13 @@ perm_status_t perm_c128_finalize(const perm_dd_c128_t* partials, int count, int 
 perm_status_t perm_c128_batched(const perm_c128_t* A_dev, int n, int64_t B, perm_c128_t* per_dev,
                                 double* abs2_dev, void* stream);
 
+/* The same, plus the ensemble statistic of Secs. IV-V, X_b = |per(A_b)| / sqrt(n!), for
+ * streaming random-matrix ensembles (Ginibre, circular, Haar minors: E[X^2] = 1 for Ginibre and circular):
+ *   x_dev      device, B doubles X_b = sqrt(|per_b|^2 / n!) (n! rounded to binary64), or NULL.
+ * At least one of per_dev, abs2_dev, x_dev must be non-NULL.  Otherwise as perm_c128_batched. */
+perm_status_t perm_c128_batched_x(const perm_c128_t* A_dev, int n, int64_t B, perm_c128_t* per_dev,
+                                  double* abs2_dev, double* x_dev, void* stream);
+
 /* ------------------------------------------------------------------------------------------
  * Sparse matrices: restricted enumeration (App. B; Sec. II-D; NEXT-3).
  * ------------------------------------------------------------------------------------------ */

@@ -140,6 +140,7 @@ def lib() -> ctypes.CDLL:
         "perm_c128_range": [P, i32, u64, u64, P, P, sz, P, P],
         "perm_c128_finalize": [P, i32, i32, P, P],
         "perm_c128_batched": [P, i32, i64, P, P, P],
+        "perm_c128_batched_x": [P, i32, i64, P, P, P, P],
         "perm_c128_weighted_batched": [P, P, i32, i32, i64, P, P, P],
         "perm_sparse_plan": [P, i32, P],
         "perm_c128_band_batched": [P, i32, i32, i64, P, P, P],
@@ -485,6 +486,29 @@ def perm_c128_batched(A, *, per=None, abs2=None, want_per: bool = True, want_abs
     return per, abs2
 
 
+def perm_c128_batched_x(A, *, per=None, abs2=None, x=None, want_per: bool = False, want_abs2: bool = False,
+                        want_x: bool = True, stream=None):
+    """per, |per|^2 and the ensemble statistic X = |per|/sqrt(n!) of a (B, n, n) complex128 CUDA
+    tensor, 1 <= n <= 32.  Stream-ordered.  Returns (per, abs2, x) CUDA tensors (None where not requested)."""
+    torch = _torch()
+    if not (_is_torch(A) and A.is_cuda and A.dtype == torch.complex128):
+        raise ValueError("perm_c128_batched_x expects a CUDA complex128 tensor (B, n, n)")
+    A = A.contiguous()
+    B, n, n2 = A.shape
+    if n != n2:
+        raise ValueError("matrices must be square")
+    if per is None and want_per:
+        per = torch.empty(B, dtype=torch.complex128, device=A.device)
+    if abs2 is None and want_abs2:
+        abs2 = torch.empty(B, dtype=torch.float64, device=A.device)
+    if x is None and want_x:
+        x = torch.empty(B, dtype=torch.float64, device=A.device)
+    ptr = lambda t: ctypes.c_void_p(t.data_ptr() if t is not None else 0)
+    _check(lib().perm_c128_batched_x(ctypes.c_void_p(A.data_ptr()), n, B, ptr(per), ptr(abs2), ptr(x),
+                                     _stream_ptr(stream)))
+    return per, abs2, x
+
+
 def perm_c128_weighted_batched(C, mult, *, per=None, abs2=None, want_per: bool = True, want_abs2: bool = True,
                                stream=None):
     """per and |per|^2 of B matrices with repeated columns (Eq. (4)): C is a (B, n, R)
@@ -610,7 +634,7 @@ def perm_fp64_probe(blocks: int, threads: int, iters: int, sink, stream=None):
 
 
 __all__ = ["perm_c128", "perm_c128_range", "perm_c128_finalize", "perm_c128_chunks", "perm_c128_tree",
-           "perm_c128_tree_combine", "chunk_log2", "chunk_walkers", "tree_workspace_bytes", "tree_nodes", "make_tree_nodes", "perm_c128_batched", "perm_c128_weighted_batched",
+           "perm_c128_tree_combine", "chunk_log2", "chunk_walkers", "tree_workspace_bytes", "tree_nodes", "make_tree_nodes", "perm_c128_batched", "perm_c128_batched_x", "perm_c128_weighted_batched",
            "perm_int01", "perm_pm1", "perm_int01_range", "perm_int01_finalize", "perm_c128_sparse", "perm_sparse_plan",
            "perm_c128_band_batched", "band_storage",
            "perm_c128_seed", "perm_fp64_probe", "workspace_bytes", "make_workspace", "int01_workspace_bytes",

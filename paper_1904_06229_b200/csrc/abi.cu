@@ -667,19 +667,24 @@ perm_status_t perm_c128_finalize(const perm_dd_c128_t* partials, int count, int 
     return PERM_OK;
 }
 
-perm_status_t perm_c128_batched(const perm_c128_t* A_dev, int n, int64_t B, perm_c128_t* per_dev,
-                                double* abs2_dev, void* stream) {
+perm_status_t perm_c128_batched_x(const perm_c128_t* A_dev, int n, int64_t B, perm_c128_t* per_dev, double* abs2_dev,
+                                  double* x_dev, void* stream) {
     g_launches = 0;
     if (B < 0) return PERM_E_ARG;
     if (n < 1 || n > perm::kMaxBatchedN) return PERM_E_ORDER;
     if (B == 0) return PERM_OK;
-    if (!A_dev || (!per_dev && !abs2_dev)) return PERM_E_ARG;
+    if (!A_dev || (!per_dev && !abs2_dev && !x_dev)) return PERM_E_ARG;
     int launches = 0;
-    cudaError_t e = perm::batched_launch((const double2*)A_dev, n, B, (double2*)per_dev, abs2_dev,
+    cudaError_t e = perm::batched_launch((const double2*)A_dev, n, B, (double2*)per_dev, abs2_dev, x_dev,
                                          (cudaStream_t)stream, &launches);
     if (e != cudaSuccess) return cuda_fail(e, "batched kernel launch");
     g_launches = (uint32_t)launches;
     return PERM_OK;
+}
+
+perm_status_t perm_c128_batched(const perm_c128_t* A_dev, int n, int64_t B, perm_c128_t* per_dev,
+                                double* abs2_dev, void* stream) {
+    return perm_c128_batched_x(A_dev, n, B, per_dev, abs2_dev, nullptr, stream);
 }
 
 // greedypartition (App. B) on the host, as a single scan: the paper repeatedly takes the

@@ -93,6 +93,24 @@ __global__ void __launch_bounds__(32 * kBandWarps) band_kernel(const double2* __
     constexpr int SPL = (S + 31) / 32;                                     // states per lane
     extern __shared__ __align__(16) unsigned char bsm[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if constexpr (K == 0) {
+        // bandwidth 0: one state (the empty window), the transfer step multiplies by a_ii -- per = prod a_ii;
+        // one lane per matrix
+        for (int64_t b = ((int64_t)blockIdx.x * kBandWarps + warp) * 32 + lane; b < B;
+             b += (int64_t)gridDim.x * kBandWarps * 32) {
+            double vr = 1.0, vi = 0.0;
+            for (int i = 0; i < n; i++) {
+                const double2 a = A[b * (int64_t)n + i];
+                const double t = vr * a.y;
+                vr = fma(vr, a.x, -vi * a.y);
+                vi = fma(vi, a.x, t);
+            }
+            if (per) per[b] = make_double2(vr, vi);
+            if (abs2) abs2[b] = __dadd_rn(__dmul_rn(vr, vr), __dmul_rn(vi, vi));
+        }
+        (void)bsm;
+        return;
+    } else {
     double2* cur = (double2*)bsm + (size_t)warp * (2 * NS + W);
     double2* nxt = cur + NS;
     double2* row = cur + 2 * NS;
@@ -179,6 +197,7 @@ __global__ void __launch_bounds__(32 * kBandWarps) band_kernel(const double2* __
             if (per) per[b] = r;
             if (abs2) abs2[b] = __dadd_rn(__dmul_rn(r.x, r.x), __dmul_rn(r.y, r.y));
         }
+    }
     }
 }
 

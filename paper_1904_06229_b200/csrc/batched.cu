@@ -8,7 +8,8 @@
 // small n (few terms per matrix) several matrices share a warp.  Each warp stages its matrices
 // (coalesced global reads) column-major, with a negated copy, into its own shared-memory slice.  The group's dd partials
 // are combined with a fixed shuffle tree; lane 0 applies 2(-1)^n (App. A permanent step 4)
-// and writes per (rounded from dd) and |per|^2 = re^2 + im^2 of that rounded value.
+// and writes per (rounded from dd), |per|^2 = re^2 + im^2 of that rounded value and, if asked, the
+// ensemble statistic X = |per| / sqrt(n!) of Secs. IV-V: X = sqrt(|per|^2 / n!).
 #include "walk.cuh"
 
 namespace perm {
@@ -29,7 +30,8 @@ struct BatCfg {
 template <int N>
 __global__ void __launch_bounds__(BatCfg<N>::NT) batched_kernel(const double2* __restrict__ A, int64_t B,
                                                                 double2* __restrict__ per,
-                                                                double* __restrict__ abs2) {
+                                                                double* __restrict__ abs2,
+                                                                double* __restrict__ xs, double nfact) {
     using C = BatCfg<N>;
     extern __shared__ double2 smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -83,12 +85,14 @@ __global__ void __launch_bounds__(BatCfg<N>::NT) batched_kernel(const double2* _
         const double im = (acc.im.hi + acc.im.lo) * f;
         const int64_t m = m0 + g;
         if (per) per[m] = make_double2(re, im);
-        if (abs2) abs2[m] = __dadd_rn(__dmul_rn(re, re), __dmul_rn(im, im));   // no FMA: fl(fl(re^2) + fl(im^2))
+        const double a2 = __dadd_rn(__dmul_rn(re, re), __dmul_rn(im, im));   // no FMA: fl(fl(re^2) + fl(im^2))
+        if (abs2) abs2[m] = a2;
+        if (xs) xs[m] = __dsqrt_rn(__ddiv_rn(a2, nfact));
     }
 }
 
 template <int N>
-cudaError_t batched_launch_t(const double2* A, int64_t B, double2* per, double* abs2, cudaStream_t s) {
+cudaError_t batched_launch_t(const double2* A, int64_t B, double2* per, double* abs2, double* xs, cudaStream_t s) {
     using C = BatCfg<N>;
     static_assert(C::E >= WCfg<N, 1>::U || C::E == 0, "lane chunk shorter than the unrolled block");
     cudaError_t err = cudaFuncSetAttribute(batched_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -97,18 +101,20 @@ cudaError_t batched_launch_t(const double2* A, int64_t B, double2* per, double* 
     const int64_t per_block = (int64_t)C::WARPS * C::G;
     const int64_t grid = (B + per_block - 1) / per_block;
     if (grid > 0x7fffffffLL) return cudaErrorInvalidValue;
-    batched_kernel<N><<<(unsigned)grid, C::NT, C::smem_bytes, s>>>(A, B, per, abs2);
+    double nfact = 1.0;                                   // n! rounded to binary64 (exact for n <= 22)
+    for (int k = 2; k <= N; k++) nfact *= (double)k;
+    batched_kernel<N><<<(unsigned)grid, C::NT, C::smem_bytes, s>>>(A, B, per, abs2, xs, nfact);
     return cudaGetLastError();
 }
 
 #define PERM_R8(M, b) M(b + 1) M(b + 2) M(b + 3) M(b + 4) M(b + 5) M(b + 6) M(b + 7) M(b + 8)
 
-cudaError_t batched_launch(const double2* A, int n, int64_t B, double2* per, double* abs2, cudaStream_t s,
-                           int* launches) {
+cudaError_t batched_launch(const double2* A, int n, int64_t B, double2* per, double* abs2, double* xs,
+                           cudaStream_t s, int* launches) {
     *launches = 0;
     if (B == 0) return cudaSuccess;
     *launches = 1;
-#define PERM_CASE(N) case N: return batched_launch_t<N>(A, B, per, abs2, s);
+#define PERM_CASE(N) case N: return batched_launch_t<N>(A, B, per, abs2, xs, s);
     switch (n) { PERM_R8(PERM_CASE, 0) PERM_R8(PERM_CASE, 8) PERM_R8(PERM_CASE, 16) PERM_R8(PERM_CASE, 24)
                  default: return cudaErrorInvalidValue; }
 #undef PERM_CASE

@@ -167,7 +167,7 @@ cudaError_t reduce_launch(const ddc* parts, int count, int n_final, ddc* out_dd,
 cudaError_t fp64_probe_launch(int blocks, int threads, int iters, double* sink, cudaStream_t s);
 
 // batched.cu
-cudaError_t batched_launch(const double2* A, int n, int64_t B, double2* per, double* abs2, cudaStream_t s,
+cudaError_t batched_launch(const double2* A, int n, int64_t B, double2* per, double* abs2, double* xs, cudaStream_t s,
                            int* launches);
 
 // sparse.cuh / sparse_inst.cu (App. B restricted enumeration), n <= kMaxSparseN

@@ -145,9 +145,13 @@ __global__ void __launch_bounds__(walk_block_threads(N)) sparse_kernel_c(const _
     }
 }
 
+// Shared-memory sparse walk.  Lanes per item S = walk_lanes_per_chunk(N) (two from n = 33, rows split
+// between the lanes exactly as in walk_kernel): the 4n row-sum registers of one lane would not fit next to
+// the shared-memory column operands without spilling.  The S lanes of a group walk the same item.
 template <int N>
-__global__ void __launch_bounds__(walk_block_threads(N)) sparse_kernel(const __grid_constant__ SparseParams P) {
-    using C = WCfg<N, 1>;
+__global__ void __launch_bounds__(WalkCfg<N>::NT, WalkCfg<N>::MINB) sparse_kernel(const __grid_constant__ SparseParams P) {
+    using C = WalkCfg<N>;
+    constexpr int R = C::R, S = C::S;
     extern __shared__ double2 smem[];
     // stage the permuted columns (slot k = column P.col[k]) and their negations, walk layout
     for (int k = threadIdx.x; k < N * C::P; k += blockDim.x) {
@@ -157,17 +161,23 @@ __global__ void __launch_bounds__(walk_block_threads(N)) sparse_kernel(const __g
         smem[N * C::P + k] = make_double2(-a.x, -a.y);
     }
     __syncthreads();
-    const uint32_t lc = (uint32_t)__cvta_generic_to_shared(smem);
+    const uint32_t h = threadIdx.x % S;
+    const uint32_t lc = (uint32_t)__cvta_generic_to_shared(smem) + h * (uint32_t)R * 16u;
+    // the item's dd partial lives in shared memory (touched once per 2^kWalkFoldBits terms)
+    __shared__ ddc spart_[C::NT];
     ddc acc;
     acc.re.hi = acc.re.lo = acc.im.hi = acc.im.lo = 0.0;
     const uint64_t total = P.outer * P.chunks;
-    const uint64_t W = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < total; g += W) {
+    const uint64_t W = (uint64_t)gridDim.x * (blockDim.x / S);
+    for (uint64_t g = (uint64_t)blockIdx.x * (blockDim.x / S) + threadIdx.x / S; g < total; g += W) {
         uint64_t o = g / P.chunks;
         const uint64_t c = g - o * P.chunks;
-        double wr[N], wi[N];
+        double wr[R], wi[R];
 #pragma unroll
-        for (int i = 0; i < N; i++) { wr[i] = 0.0; wi[i] = 0.0; }
+        for (int i = 0; i < R; i++) {                      // padding rows (odd n, S = 2) are a neutral factor 1
+            wr[i] = ((int)h * R + i < N) ? 0.0 : 1.0;
+            wi[i] = 0.0;
+        }
         // outer combination o -> non-empty s_l: mixed radix 2^{|S_l|} - 1, digit v -> sub-mask v + 1
         int ssum = 0;
         for (int l = 0; l < P.d; l++) {
@@ -176,35 +186,58 @@ __global__ void __launch_bounds__(walk_block_threads(N)) sparse_kernel(const __g
             o /= r;
             for (int q = 0; q < P.ssz[l]; q++) {
                 const double f = (double)((m >> q) & 1ull);
-                flip_dyn<N>(lc + (uint32_t)((P.soff[l] + q) * C::P) * 16u, f, wr, wi);
+                flip_dyn<R>(lc + (uint32_t)((P.soff[l] + q) * C::P) * 16u, f, wr, wi);
             }
             ssum += __popcll(m);
         }
-        ddc part;
-        part.re.hi = part.re.lo = part.im.hi = part.im.lo = 0.0;
+        {
+            volatile ddc& z = *(volatile ddc*)&spart_[threadIdx.x];
+            z.re.hi = 0.0; z.re.lo = 0.0; z.im.hi = 0.0; z.im.lo = 0.0;
+        }
+        ddc& part = spart_[threadIdx.x];
         if (P.e == 0) {
             // a single rank r = c of the T walk (|T| < U, or no T at all)
             const uint64_t x = c ^ (c >> 1);
             for (int q = 0; q < P.nt; q++)
-                flip_dyn<N>(lc + (uint32_t)(q * C::P) * 16u, (double)((x >> q) & 1ull), wr, wi);
+                flip_dyn<R>(lc + (uint32_t)(q * C::P) * 16u, (double)((x >> q) & 1ull), wr, wi);
             double ar = 0.0, ai = 0.0;
-            if (c & 1ull) term_acc<N, C::K, +1>(wr, wi, ar, ai);
-            else          term_acc<N, C::K, -1>(wr, wi, ar, ai);
+            if constexpr (S == 1) {
+                if (c & 1ull) term_acc<R, C::K, +1>(wr, wi, ar, ai);
+                else          term_acc<R, C::K, -1>(wr, wi, ar, ai);
+            } else {
+                double pr, pi;
+                lane_product<R, C::K>(wr, wi, pr, pi);
+#pragma unroll
+                for (int k = 1; k < S; k <<= 1) {           // butterfly: every lane ends with the full product
+                    const double qr = __shfl_xor_sync(group_mask<S>(), pr, k);
+                    const double qi = __shfl_xor_sync(group_mask<S>(), pi, k);
+                    cmul2(pr, pi, qr, qi);
+                }
+                if (h == 0) {
+                    if (c & 1ull) { ar += pr; ai += pi; }
+                    else          { ar -= pr; ai -= pi; }
+                }
+            }
             part.re = dd_add_d(part.re, ar);
             part.im = dd_add_d(part.im, ai);
         } else {
             const int e = P.e;
             const uint64_t x = ((c ^ (c >> 1)) << e) | ((c & 1ull) << (e - 1));
             for (int q = e - 1; q < P.nt; q++)
-                flip_dyn<N>(lc + (uint32_t)(q * C::P) * 16u, (double)((x >> q) & 1ull), wr, wi);
-            walk_seeded<C>(lc, 0u, c, e, wr, wi, part);
+                flip_dyn<R>(lc + (uint32_t)(q * C::P) * 16u, (double)((x >> q) & 1ull), wr, wi);
+            walk_seeded<C>(lc, h, c, e, wr, wi, part);
+        }
+        ddc pv = part;
+        if constexpr (S > 1) {          // the S lanes of a group hold interleaved terms: fixed-order combine
+#pragma unroll
+            for (int off = S / 2; off > 0; off >>= 1) pv = ddc_add(pv, shfl_down_ddc(pv, off, group_mask<S>()));
         }
         // contribution -(-1)^{|s|} * part
         if ((ssum & 1) == 0) {
-            part.re.hi = -part.re.hi; part.re.lo = -part.re.lo;
-            part.im.hi = -part.im.hi; part.im.lo = -part.im.lo;
+            pv.re.hi = -pv.re.hi; pv.re.lo = -pv.re.lo;
+            pv.im.hi = -pv.im.hi; pv.im.lo = -pv.im.lo;
         }
-        acc = ddc_add(acc, part);
+        if (h == 0) acc = ddc_add(acc, pv);
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) acc = ddc_add(acc, shfl_down_ddc(acc, off));
@@ -250,20 +283,19 @@ cudaError_t sparse_launch_t(const SparseLaunch& L) {
         }
     }
     cudaError_t err = cudaFuncSetAttribute(sparse_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)C::smem_bytes);
+                                           (int)WalkCfg<N>::smem_bytes);
     if (err != cudaSuccess) return err;
-    sparse_kernel<N><<<L.grid, walk_block_threads(N), C::smem_bytes, L.stream>>>(P);
+    sparse_kernel<N><<<L.grid, WalkCfg<N>::NT, WalkCfg<N>::smem_bytes, L.stream>>>(P);
     return cudaGetLastError();
 }
 
 template <int N>
 cudaError_t sparse_occupancy_t(int* blocks_per_sm) {
-    using C = WCfg<N, 1>;
+    using C = WalkCfg<N>;
     cudaError_t err = cudaFuncSetAttribute(sparse_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)C::smem_bytes);
     if (err != cudaSuccess) return err;
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, sparse_kernel<N>, walk_block_threads(N),
-                                                         C::smem_bytes);
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, sparse_kernel<N>, C::NT, C::smem_bytes);
 }
 
 }  // namespace perm

@@ -43,7 +43,7 @@ template <int N>
 struct WgtCfg {
     static constexpr int NT = 32;                    // one warp (one problem at a time) per block
 #ifndef PERM_WGT_REG_EXTRA
-#define PERM_WGT_REG_EXTRA 96
+#define PERM_WGT_REG_EXTRA 128
 #endif
     static constexpr int REGS = ((4 * N + PERM_WGT_REG_EXTRA + 7) / 8) * 8;
     static constexpr int MINB_RAW = 65536 / (NT * (REGS < 255 ? REGS : 255));

@@ -18,7 +18,8 @@ from __future__ import annotations
 
 import numpy as np
 
-SEEDS = {"cfg1": 16, "cfg2_u": 2000, "cfg2_idx": 3000, "cfg3": 24, "cfg4": 1024, "cfg5": 44, "cfgw": 2424, "cfgpm": 2425, "cfgsp": 4848, "cfgbd": 1005}
+SEEDS = {"cfg1": 16, "cfg2_u": 2000, "cfg2_idx": 3000, "cfg3": 24, "cfg4": 1024, "cfg5": 44, "cfgw": 2424, "cfgpm": 2425, "cfgsp": 4848, "cfgbd": 1005,
+         "cfgens_g": 2024, "cfgens_c": 3024}
 
 
 def complex_gaussian(shape, seed: int | np.random.Generator) -> np.ndarray:
@@ -145,6 +146,19 @@ def bernoulli_pm1(shape, seed: int) -> np.ndarray:
     """Bernoulli +-1 entries, Pr(+1) = Pr(-1) = 1/2 (Sec. V), as int8."""
     rng = np.random.default_rng(seed)
     return np.ascontiguousarray((2 * rng.integers(0, 2, size=shape) - 1).astype(np.int8))
+
+
+def circular(shape, seed: int | np.random.Generator) -> np.ndarray:
+    """Complex circular entries exp(i theta), theta uniform on [0, 2 pi) (Sec. IV)."""
+    rng = np.random.default_rng(seed)
+    theta = rng.uniform(0.0, 2.0 * np.pi, size=shape)
+    return np.ascontiguousarray(np.exp(1j * theta))
+
+
+def cfgens(count: int = 10_000, n: int = 24) -> tuple[np.ndarray, np.ndarray]:
+    """The ensemble workload: `count` Ginibre matrices and `count` circular matrices of
+    order n (Secs. III-IV collect 10^7 of each for n <= 30; this is a bounded batch of the same shape)."""
+    return (complex_gaussian((count, n, n), SEEDS["cfgens_g"]), circular((count, n, n), SEEDS["cfgens_c"]))
 
 
 def haar_minors(n: int, a: float, count: int, seed: int) -> np.ndarray:

@@ -100,6 +100,32 @@ def test_sparse_plan_host_logic_matches_oracle_partition():
     assert L.perm_c128_sparse(A.ctypes.data_as(ctypes.c_void_p), 49, ctypes.byref(out), None, None) == 2
 
 
+def test_sparse_plan_properties():
+    """App. B greedypartition by its defining properties, independent of any implementation:
+    every S_l is the support of a row; the S_l are pairwise disjoint; S_l is the support of the least-degree
+    (lowest index on ties) row among the rows that miss S_1 .. S_{l-1}; no row misses all of them at the end;
+    T is the rest; sets = 2^|T| prod_l (2^|S_l| - 1)."""
+    rng = np.random.default_rng(31)
+    for n, dens in ((6, 0.3), (12, 0.15), (20, 0.1), (33, 0.06), (48, 0.04), (64, 0.03)):
+        for _ in range(3):
+            M = (rng.random((n, n)) < dens) * (1.0 + rng.random((n, n)))
+            M[np.arange(n), rng.permutation(n)] += 1.0
+            supp = [sum(1 << j for j in range(n) if M[i, j] != 0) for i in range(n)]
+            p = pb.perm_sparse_plan(M.astype(np.complex128))
+            S = p["S"]
+            used = 0
+            for s in S:
+                assert s in supp and s & used == 0
+                cand = [i for i in range(n) if supp[i] & used == 0]
+                k = min(cand, key=lambda i: (bin(supp[i]).count("1"), i))
+                assert s == supp[k]
+                used |= s
+            assert all(supp[i] & used for i in range(n))
+            full = (1 << n) - 1
+            assert p["T"] == full & ~used
+            assert p["sets"] == 2.0 ** bin(p["T"]).count("1") * math.prod(2.0 ** bin(s).count("1") - 1 for s in S)
+
+
 def test_const_walk_keeps_uniform_column_operands():
     # The constant-bank walks (n = 32, 34, 35, 37, 39, 43..45) take their inner columns as uniform-register
     # operands (LDCU from the kernel-parameter bank, DESIGN.md 5.1): +4..12%.  ptxas only does this for some register
@@ -120,3 +146,17 @@ def test_const_walk_keeps_uniform_column_operands():
         uniform = sum(1 for l in sass.splitlines() if "LDCU.64" in l and "c[0x0][UR" in l)
         lane = sum(1 for l in sass.splitlines() if " LDC.64 R" in l and "c[0x0][R" in l)
         assert uniform > 100 and lane == 0, (fn, uniform, lane)
+
+
+def test_no_register_spills_in_library_kernels():
+    """Every kernel libperm.so dispatches compiles without spill stores (ptxas -v logs of the last build,
+    paper_1904_06229_b200/build/*.o.log; tools/spills.py): a spill puts local-memory traffic into loops
+    that are meant to run from registers."""
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+    from spills import spills
+    d = spills()
+    if not d:
+        pytest.skip("no ptxas logs (library not built in this tree)")
+    bad = {k: v for k, v in d.items() if v[0] > 0}
+    assert not bad, bad

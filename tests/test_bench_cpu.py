@@ -37,3 +37,15 @@ def test_collision_patterns_are_valid_multisets():
         # each stored column is a column of U's first n rows (unit-norm rows of a unitary restricted)
         for j in range(k):
             assert np.min(np.abs(U[:8, :] - C[b, :, j:j + 1]).sum(axis=0)) < 1e-12
+
+
+def test_circular_generator():
+    # entries exp(i theta), theta ~ U[0, 2 pi): modulus 1, E a = 0, E a^2 = 0 (5 sigma)
+    import numpy as np
+    from paper_1904_06229_b200 import inputs
+    a = inputs.circular((200_000,), 5)
+    assert np.allclose(np.abs(a), 1.0, rtol=0, atol=1e-15)
+    for k in (1, 2):
+        m = np.mean(a ** k)
+        assert abs(m) <= 5 / np.sqrt(a.size), (k, m)
+    assert np.array_equal(inputs.circular((4, 4), 9), inputs.circular((4, 4), 9))

@@ -184,6 +184,34 @@ def test_app_a_trace(golden_dir):
             assert oracle.subpermanent(A, k0, k1 - k0).value == float(ref)
 
 
+def test_subpermanent_par_pins(golden_dir):
+    """oracle_subpermanent_par -- App. A's permanent loop restricted to a sub-range [r, r+l):
+    the span cut by distribute into `parts` pieces walked on host threads, partials added in order.  Pinned
+    (1) exactly on the dyadic n = 3 hand trace for every split of every span, (2) on random spans against
+    range_sum, whose terms are re-derived from the definition per rank (no walk, no split), and the serial
+    walk, for part counts that leave empty, single-rank and unaligned pieces."""
+    g = json.load(open(os.path.join(golden_dir, "app_a_trace_n3.json")))
+    A = np.array(g["A"], dtype=np.complex128)
+    for parts in (1, 2, 3, 4, 7):
+        for k0 in range(5):
+            for k1 in range(k0, 5):
+                ref = sum(Fraction(*g["terms_num_den"][r]) for r in range(k0, k1))
+                assert oracle.subpermanent(A, k0, k1 - k0, parts=parts).value == float(ref), (parts, k0, k1)
+    rng = np.random.default_rng(77)
+    for n in (9, 20, 33):
+        A = inputs.complex_gaussian((n, n), 700 + n)
+        N = 1 << (n - 1)
+        for _ in range(2):
+            k0 = int(rng.integers(0, max(1, N - 2500)))
+            k1 = min(N, k0 + int(rng.integers(1, 2500)))
+            ref = oracle.range_sum(A, k0, k1).value
+            ser = oracle.subpermanent(A, k0, k1 - k0).value
+            for parts in (2, 3, 5, 16, 64, 4096):
+                par = oracle.subpermanent(A, k0, k1 - k0, parts=parts).value
+                assert _close(par, ref, 1e-20, scale=max(abs(ref), 1.0) * 1e3), (n, k0, k1, parts)
+                assert _close(par, ser, 1e-20, scale=max(abs(ser), 1.0) * 1e3), (n, k0, k1, parts)
+
+
 def test_n2_closed_form():
     # App. A at n = 2: S = (ad + bc)/2, per = ad + bc (SURVEY App. S-1)
     a, b, c, d = 1 + 2j, 3 - 1j, -2 + 0.5j, 0.25 + 4j
