@@ -514,7 +514,7 @@ def run_ours(args):
         B, n = Gm.shape[0], Gm.shape[1]
         b0, b1 = shard.rank_span(B, world, rank)
         hosts = [torch.from_numpy(np.ascontiguousarray(M[b0:b1])).pin_memory() for M in (Gm, Cm)]
-        devs = [h.to(device) for h in hosts]
+        ens_dev = [h.to(device) for h in hosts]
         xs = [torch.empty(b1 - b0, dtype=torch.float64, device=device) for _ in hosts]
         xs_host = [torch.empty(b1 - b0, dtype=torch.float64).pin_memory() for _ in hosts]
         e0, e1 = ev(), ev()
@@ -525,14 +525,14 @@ def run_ours(args):
 
         def step():
             e0.record(stream)
-            for dv, x in zip(devs, xs):
+            for dv, x in zip(ens_dev, xs):
                 pb.perm_c128_batched_x(dv, x=x, stream=stream)
             e1.record(stream)
             torch.cuda.synchronize()
             es = torch.cuda.Event(enable_timing=True)
             ee = torch.cuda.Event(enable_timing=True)
             es.record(stream)
-            for h, dv, x, xh in zip(hosts, devs, xs, xs_host):
+            for h, dv, x, xh in zip(hosts, ens_dev, xs, xs_host):
                 dv.copy_(h, non_blocking=True)
                 pb.perm_c128_batched_x(dv, x=x, stream=stream)
                 xh.copy_(x, non_blocking=True)

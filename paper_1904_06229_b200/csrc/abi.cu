@@ -315,6 +315,8 @@ perm_status_t run_walk(const perm_c128_t* A, int n, uint64_t k0, uint64_t k1, in
     perm_status_t result = PERM_OK;
     uint32_t launches = 0;
     ResBlock* res = (ResBlock*)(ws + L.res_off);
+    double2* small_c = nullptr;                           // device outputs the small kernel writes directly
+    ddc* small_dd = nullptr;
     do {
         cudaError_t e = cudaSuccess;
         if (small) {
@@ -329,8 +331,12 @@ perm_status_t run_walk(const perm_c128_t* A, int n, uint64_t k0, uint64_t k1, in
                 if (e != cudaSuccess) { result = cuda_fail(e, "cudaMemcpyAsync(A H2D)"); break; }
                 A_dev = (const double2*)(ws + L.a_off);
             }
+            // device outputs are written by the kernel itself (no extra copy node on the latency path)
+            if (out_c && is_device_ptr(out_c)) { small_c = (double2*)out_c; }
+            if (out_dd && is_device_ptr(out_dd)) { small_dd = (ddc*)out_dd; }
             if (stats && stats->ev_walk_begin) cudaEventRecord((cudaEvent_t)stats->ev_walk_begin, s);
-            e = perm::walk_small_launch_n(n, A_dev, p.seg[0].e, p.items, &res->raw, &res->out_dd, &res->out_c, s);
+            e = perm::walk_small_launch_n(n, A_dev, p.seg[0].e, p.items, &res->raw, small_dd ? small_dd : &res->out_dd,
+                                          small_c ? small_c : &res->out_c, s);
             if (e != cudaSuccess) { result = cuda_fail(e, "small walk launch"); break; }
             if (stats && stats->ev_walk_end) cudaEventRecord((cudaEvent_t)stats->ev_walk_end, s);
             launches = 1;
@@ -354,13 +360,13 @@ perm_status_t run_walk(const perm_c128_t* A, int n, uint64_t k0, uint64_t k1, in
         }
         const void* src_c = &res->out_c;
         const void* src_dd = n_final > 0 ? (const void*)&res->out_dd : (const void*)&res->raw;
-        const bool c_dev = out_c && is_device_ptr(out_c);
-        const bool dd_dev = out_dd && is_device_ptr(out_dd);
-        if (c_dev) {
+        const bool c_dev = small_c != nullptr || (out_c && is_device_ptr(out_c));
+        const bool dd_dev = small_dd != nullptr || (out_dd && is_device_ptr(out_dd));
+        if (c_dev && !small_c) {
             e = cudaMemcpyAsync(out_c, src_c, sizeof(double2), cudaMemcpyDeviceToDevice, s);
             if (e != cudaSuccess) { result = cuda_fail(e, "cudaMemcpyAsync(result)"); break; }
         }
-        if (dd_dev) {
+        if (dd_dev && !small_dd) {
             e = cudaMemcpyAsync(out_dd, src_dd, sizeof(ddc), cudaMemcpyDeviceToDevice, s);
             if (e != cudaSuccess) { result = cuda_fail(e, "cudaMemcpyAsync(result dd)"); break; }
         }

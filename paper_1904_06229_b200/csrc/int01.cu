@@ -16,6 +16,8 @@
 // unrolled inner block of 2^U steps (compile-time columns and signs, warp-uniform broadcast loads).
 // Per-block partial sums (exact, order-free) go to the workspace; a final kernel adds them per
 // matrix, checks divisibility and writes per as int128.
+#include <mutex>
+
 #include "internal.h"
 
 namespace perm {
@@ -256,24 +258,54 @@ struct I01Plan {
     uint64_t chunks;
 };
 
+// Resident blocks of int01_kernel<n> on the current device (SMs x occupancy), computed once per device.
+// Sizing the grid to it matters: a grid of 2.3 waves leaves the last wave 70% idle.
+#define PERM_R8I(M, b) M(b + 1) M(b + 2) M(b + 3) M(b + 4) M(b + 5) M(b + 6) M(b + 7) M(b + 8)
+static int int01_resident_blocks(int n) {
+    static std::once_flag once[64][kMaxInt01N + 1];
+    static int res[64][kMaxInt01N + 1];
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64 || n < 1 || n > kMaxInt01N) return 148 * 4;
+    std::call_once(once[dev][n], [&] {
+        int sms = 148, bps = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaError_t e = cudaErrorInvalidValue;
+        switch (n) {
+#define PERM_CASE(N) case N: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, int01_kernel<N, false>, \
+                                                                                 I01Cfg<N>::NT, 0); break;
+            PERM_R8I(PERM_CASE, 0) PERM_R8I(PERM_CASE, 8) PERM_R8I(PERM_CASE, 16) PERM_R8I(PERM_CASE, 24)
+            PERM_CASE(33)
+#undef PERM_CASE
+            default: break;
+        }
+        if (e != cudaSuccess || bps < 1) bps = 4;
+        res[dev][n] = sms * bps;
+    });
+    return res[dev][n];
+}
+
+// B matrices: floor(R / B) blocks per matrix when the batch is smaller than the R resident blocks (one
+// wave), else one block per matrix; the chunk length makes every thread walk 16 chunks (seeding 16 chunks'
+// high columns is < 2% of the walk at n = 24), exactly when the block count is a power of two.
 static I01Plan int01_plan(int n, int64_t B) {
-    // threads per matrix ~ max(128, 148*16*128 / B) (a few waves of the whole chip), chunk >= 2^U
     const int U = walk_inner_bits(n);
     const int nb = n > kMaxGlynnInt01N ? n : n - 1;           // Gray bits
-    const uint64_t total = 1ull << nb;
-    int64_t want_threads = (int64_t)148 * 16 * 128 / (B > 0 ? B : 1);
-    if (want_threads < 128) want_threads = 128;
-    int e = nb;
-    while (e > U && (total >> e) < (uint64_t)want_threads * 4) e--;
+    const int64_t R = int01_resident_blocks(n);
+    int64_t nblk = (B > 0 && B < R) ? R / B : 1;
+    const uint64_t want = (uint64_t)nblk * 128u * 16u;         // chunks per matrix
+    int lg = 0;
+    while ((1ull << lg) < want) lg++;
+    int e = nb - lg;
+    if (e < U) e = U;
+    if (e > nb) e = nb;
     if (n == 1) e = 0;
     I01Plan p;
     p.e = e;
-    p.chunks = total >> e;
-    uint64_t blocks = (p.chunks + 127) / 128;
-    const uint64_t cap = (uint64_t)((want_threads + 127) / 128);
-    if (blocks > cap) blocks = cap;
-    if (blocks < 1) blocks = 1;
-    p.nblk = (int)blocks;
+    p.chunks = 1ull << (nb - e);
+    const uint64_t need = (p.chunks + 127) / 128;
+    if ((uint64_t)nblk > need) nblk = (int64_t)need;
+    if (nblk < 1) nblk = 1;
+    p.nblk = (int)nblk;
     return p;
 }
 
@@ -354,14 +386,15 @@ cudaError_t int01_range_launch(const uint8_t* A, int n, uint64_t k0, uint64_t k1
     raw_host[0] = raw_host[1] = 0;
     if (k1 <= k0) return cudaSuccess;
     const int U = walk_inner_bits(n);
-    const int nblk = kInt01RangeBlocks;
+    const int R = int01_resident_blocks(n);                     // one wave of resident blocks
+    const int nblk = R < kInt01RangeBlocks ? R : kInt01RangeBlocks;
     int* flag = (int*)ws;
     u128* out = (u128*)((char*)ws + 16);
     u128* partials = (u128*)((char*)ws + 32);
     // chunk length 2^b: ~8 chunks per thread of the nblk x 128 grid (>= 2^U, <= 2^30)
     const uint64_t T = (uint64_t)nblk * 128u;
     int b = 0;
-    while (b < 30 && ((k1 - k0) >> (b + 1)) >= T * 8u) b++;
+    while (b < 30 && ((k1 - k0) >> (b + 1)) >= T * 16u) b++;
     if (b < U) b = U;
     cudaError_t err = cudaMemsetAsync(flag, 0, sizeof(int), s);
     int accum = 0;

@@ -79,11 +79,14 @@ constexpr int kConstMaxN = 48;
 #ifndef PERM_CONST_ORDERS
 #define PERM_CONST_ORDERS 32
 #endif
+#ifndef PERM_CONST_MIN
+#define PERM_CONST_MIN 33                                 // (development: 99 = shared-memory walk above n = 32)
+#endif
 __host__ __device__ constexpr bool walk_const_path(int n) {
 #if PERM_CONST_ORDERS == 0
     return n <= kConstMaxN;                               // scans only
 #else
-    return n == PERM_CONST_ORDERS || (n >= 33 && n <= kConstMaxN);
+    return n == PERM_CONST_ORDERS || (n >= PERM_CONST_MIN && n <= kConstMaxN);
 #endif
 }
 

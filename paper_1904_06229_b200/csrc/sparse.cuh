@@ -289,8 +289,20 @@ cudaError_t sparse_launch_t(const SparseLaunch& L) {
     return cudaGetLastError();
 }
 
+// Occupancy of the kernel the launch normally uses: the constant-bank kernel on its orders (the planner sizes
+// the grid and the T-walk chunk length from it), else the shared-memory kernel.
 template <int N>
 cudaError_t sparse_occupancy_t(int* blocks_per_sm) {
+    if constexpr (sparse_const_path(N) && WCfg<N, 1>::U >= 1 && WalkParamsC<N>::MN == 0) {
+        cudaError_t err = cudaFuncSetAttribute(sparse_kernel_c<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)WCfg<N, 1>::smem_bytes);
+        if (err != cudaSuccess) return err;
+        err = cudaFuncSetAttribute(sparse_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)WalkCfg<N>::smem_bytes);
+        if (err != cudaSuccess) return err;
+        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, sparse_kernel_c<N>, walk_block_threads(N),
+                                                             WCfg<N, 1>::smem_bytes);
+    }
     using C = WalkCfg<N>;
     cudaError_t err = cudaFuncSetAttribute(sparse_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)C::smem_bytes);

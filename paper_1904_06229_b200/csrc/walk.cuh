@@ -29,6 +29,7 @@
 // items by the canonical pairwise tree -- so an item's value, and the result, depend only on (A, n, b).
 #pragma once
 #include <cooperative_groups.h>
+#include <mutex>
 
 #include "common.cuh"
 #include "internal.h"
@@ -760,22 +761,34 @@ __global__ void __launch_bounds__(kSmallMaxThreads) walk_small_kernel(const doub
     } else {
         single_term<C>(lc, lb, 0u, c, acc);
     }
-    tree[t] = acc;
+    // node (L+1, k) = node (L, 2k) + node (L, 2k+1): the first levels inside each warp by shuffles (lane l
+    // combines with l + off when l is a multiple of 2 off), then the warp roots in shared memory
+    const int wl = T < 32 ? T : 32;
+    const unsigned wmask = T < 32 ? ((1u << T) - 1u) : 0xffffffffu;     // T is a power of two
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const ddc o = shfl_down_ddc(acc, off, wmask);
+        if (off < wl && (t & (2 * off - 1)) == 0) acc = ddc_add(acc, o);
+    }
+    if ((t & 31) == 0) tree[t >> 5] = acc;
     __syncthreads();
-    for (int off = 1; off < T; off <<= 1) {              // node (L+1, k) = node (L, 2k) + node (L, 2k+1)
-        if ((t & (2 * off - 1)) == 0) tree[t] = ddc_add(tree[t], tree[t + off]);
+    const int nw = (T + 31) >> 5;
+    for (int off = 1; off < nw; off <<= 1) {
+        if (t < nw && (t & (2 * off - 1)) == 0) tree[t] = ddc_add(tree[t], tree[t + off]);
         __syncthreads();
     }
     cluster.sync();                                      // every CTA root is in its tree[0]
     const int nb = (int)cluster.num_blocks();
-    if (cluster.block_rank() == 0) {
-        __shared__ ddc roots[16];
-        if (t < nb) roots[t] = *cluster.map_shared_rank(&tree[0], t);
-        __syncthreads();
+    if (cluster.block_rank() == 0 && t < 32) {
+        ddc r;
+        r.re.hi = r.re.lo = r.im.hi = r.im.lo = 0.0;
+        if (t < nb) r = *cluster.map_shared_rank(&tree[0], t);
+#pragma unroll
+        for (int off = 1; off < 16; off <<= 1) {
+            const ddc o = shfl_down_ddc(r, off, wmask);
+            if (off < nb && (t & (2 * off - 1)) == 0) r = ddc_add(r, o);
+        }
         if (t == 0) {
-            for (int off = 1; off < nb; off <<= 1)
-                for (int k = 0; k + off < nb; k += 2 * off) roots[k] = ddc_add(roots[k], roots[k + off]);
-            ddc r = roots[0];
             if (raw) *raw = r;
             const double f = (N & 1) ? -2.0 : 2.0;       // 2 (-1)^n, exact
             r.re.hi *= f; r.re.lo *= f; r.im.hi *= f; r.im.lo *= f;
@@ -797,11 +810,21 @@ cudaError_t walk_small_launch(const double2* A_dev, int e, uint64_t chunks, ddc*
         int ncta = (int)(chunks / 64);
         ncta = ncta < 1 ? 1 : (ncta > 16 ? 16 : ncta);
         const int T = (int)(chunks / (uint64_t)ncta);
-        cudaError_t err = cudaFuncSetAttribute(walk_small_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               (int)C::smem_bytes);
-        if (err == cudaSuccess && ncta > 8)
-            err = cudaFuncSetAttribute(walk_small_kernel<N>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        // function attributes once per device (host latency matters here: this path is one small launch)
+        int dev = 0;
+        cudaError_t err = cudaGetDevice(&dev);
         if (err != cudaSuccess) return err;
+        static std::once_flag once[64];
+        static cudaError_t attr_err[64];
+        if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+        std::call_once(once[dev], [] (int d) {
+            cudaError_t e2 = cudaFuncSetAttribute(walk_small_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  (int)C::smem_bytes);
+            if (e2 == cudaSuccess)
+                e2 = cudaFuncSetAttribute(walk_small_kernel<N>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+            attr_err[d] = e2;
+        }, dev);
+        if (attr_err[dev] != cudaSuccess) return attr_err[dev];
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3((unsigned)ncta, 1, 1);
         cfg.blockDim = dim3((unsigned)T, 1, 1);

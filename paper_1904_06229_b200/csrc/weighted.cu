@@ -43,9 +43,14 @@ template <int N>
 struct WgtCfg {
     static constexpr int NT = 32;                    // one warp (one problem at a time) per block
 #ifndef PERM_WGT_REG_EXTRA
-#define PERM_WGT_REG_EXTRA 128
+    // working-set registers beyond the 4n row sums: 96, or 128 for the orders that spill at 96 / 112
+    // (tools/spills.py; the extra budget costs occupancy, so only where needed -- n = 20 keeps 96)
+    static constexpr int EXTRA = (N == 12 || N == 14 || N == 15 || N == 16 || N == 18 || N == 23 || N == 25 ||
+                                  N >= 26) ? 128 : 96;
+#else
+    static constexpr int EXTRA = PERM_WGT_REG_EXTRA;
 #endif
-    static constexpr int REGS = ((4 * N + PERM_WGT_REG_EXTRA + 7) / 8) * 8;
+    static constexpr int REGS = ((4 * N + EXTRA + 7) / 8) * 8;
     static constexpr int MINB_RAW = 65536 / (NT * (REGS < 255 ? REGS : 255));
     static constexpr int MINB = MINB_RAW > 32 ? 32 : (MINB_RAW < 1 ? 1 : MINB_RAW);
 };
