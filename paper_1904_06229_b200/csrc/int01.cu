@@ -16,6 +16,7 @@
 // unrolled inner block of 2^U steps (compile-time columns and signs, warp-uniform broadcast loads).
 // Per-block partial sums (exact, order-free) go to the workspace; a final kernel adds them per
 // matrix, checks divisibility and writes per as int128.
+#include <cstdlib>
 #include <mutex>
 
 #include "internal.h"
@@ -290,9 +291,14 @@ static int int01_resident_blocks(int n) {
 static I01Plan int01_plan(int n, int64_t B) {
     const int U = walk_inner_bits(n);
     const int nb = n > kMaxGlynnInt01N ? n : n - 1;           // Gray bits
-    const int64_t R = int01_resident_blocks(n);
+    int64_t R = int01_resident_blocks(n);
+    uint64_t rounds = 16;
+    // development overrides (plan scans): PERM_INT01_WAVES = resident-block waves, PERM_INT01_ROUNDS = chunks
+    // per thread
+    if (const char* w = getenv("PERM_INT01_WAVES")) R = (int64_t)(R * atof(w));
+    if (const char* r = getenv("PERM_INT01_ROUNDS")) rounds = (uint64_t)atoi(r);
     int64_t nblk = (B > 0 && B < R) ? R / B : 1;
-    const uint64_t want = (uint64_t)nblk * 128u * 16u;         // chunks per matrix
+    const uint64_t want = (uint64_t)nblk * 128u * rounds;      // chunks per matrix
     int lg = 0;
     while ((1ull << lg) < want) lg++;
     int e = nb - lg;

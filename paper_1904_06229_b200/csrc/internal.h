@@ -22,8 +22,12 @@ __host__ __device__ constexpr int walk_inner_bits(int n) { return (n - 1) < PERM
 // U = 3 (8-term blocks) up to n = 39 and U = 2 beyond (the 4n-register row sums leave ptxas less room
 // to overlap an 8-term block); U = 2 also for the constant-bank orders 34, 35, 37, 39, whose register caps
 // (walk.cuh: walk_const_maxnreg) were found for U = 2.
+#ifndef PERM_U2_FROM33
+#define PERM_U2_FROM33 0                                  // (development: U = 2 for every n >= 33)
+#endif
 __host__ __device__ constexpr int walk_inner_bits(int n) {
-    return (n == 34 || n == 35 || n == 37 || n == 39 || n >= 40) ? 2 : ((n - 1) < 3 ? (n - 1) : 3);
+    return (n == 34 || n == 35 || n == 37 || n == 39 || n >= 40 || (PERM_U2_FROM33 && n >= 33)) ? 2
+                                                                                 : ((n - 1) < 3 ? (n - 1) : 3);
 }
 #endif
 constexpr int kWalkThreads = 64;

@@ -672,7 +672,8 @@ __host__ __device__ constexpr int walk_const_maxnreg(int n) {
 #ifdef PERM_CONST_MAXNREG_ALL
     return PERM_CONST_MAXNREG_ALL;                  // scans only (tools/const_ldcu_scan.sh)
 #else
-    return n == 33 ? 172 : n == 34 ? 192 : n == 35 ? 196 : n == 36 ? 188 : n == 37 ? 204 : n == 38 ? 200
+    return n == 33 ? (PERM_U2_FROM33 ? 176 : 172) : n == 34 ? 192 : n == 35 ? 196
+         : n == 36 ? (PERM_U2_FROM33 ? 196 : 188) : n == 37 ? 204 : n == 38 ? (PERM_U2_FROM33 ? 204 : 200)
          : n == 39 ? 212 : n == 40 ? 212 : n == 41 ? 212 : n == 42 ? 216 : n == 43 ? 204 : n == 44 ? 244
          : n == 45 ? 236 : n == 46 ? 240 : n == 47 ? 240 : n == 48 ? 244 : 0;
 #endif
