@@ -267,6 +267,7 @@ perm_status_t launch_walk(const perm_c128_t* A, int n, const WalkPlan& p, ddc* i
     WL.nseg = p.nseg;
     for (int i = 0; i < p.nseg; i++) WL.seg[i] = p.seg[i];
     WL.items = items;
+    WL.nitems = p.items;
     WL.grid = p.grid;
     WL.use_const = p.use_const;
     WL.body = p.body;

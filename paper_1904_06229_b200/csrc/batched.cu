@@ -84,6 +84,7 @@ __global__ void __launch_bounds__(BatCfg<N>::NT) batched_kernel(const double2* _
         const double re = (acc.re.hi + acc.re.lo) * f;
         const double im = (acc.im.hi + acc.im.lo) * f;
         const int64_t m = m0 + g;
+        PERM_DCHECK(m < B);
         if (per) per[m] = make_double2(re, im);
         const double a2 = __dadd_rn(__dmul_rn(re, re), __dmul_rn(im, im));   // no FMA: fl(fl(re^2) + fl(im^2))
         if (abs2) abs2[m] = a2;

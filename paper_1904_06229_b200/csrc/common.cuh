@@ -6,7 +6,26 @@
 // App. A -- also recovers the sentinel {1e16, 1, -1e16} (reading R7).
 #pragma once
 #include <cstdint>
+#include <cstdio>
 #include <cuda_runtime.h>
+
+// Device-side bounds checks of the debug build (PERM_VARIANT=dbg PERM_EXTRA_FLAGS=-DPERM_DEBUG_CHECKS):
+// compute-sanitizer is not available on the GPU pool, so index invariants are asserted in the kernels
+// themselves and the GPU tests run once against the checking build.
+#ifdef PERM_DEBUG_CHECKS
+#define PERM_DCHECK(cond)                                                                        \
+    do {                                                                                         \
+        if (!(cond)) {                                                                           \
+            printf("PERM_DCHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, __LINE__, \
+                   (int)blockIdx.x, (int)threadIdx.x);                                           \
+            __trap();                                                                            \
+        }                                                                                        \
+    } while (0)
+#else
+#define PERM_DCHECK(cond) \
+    do {                  \
+    } while (0)
+#endif
 
 namespace perm {
 

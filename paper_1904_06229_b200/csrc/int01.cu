@@ -285,14 +285,15 @@ static int int01_resident_blocks(int n) {
     return res[dev][n];
 }
 
-// B matrices: floor(R / B) blocks per matrix when the batch is smaller than the R resident blocks (one
-// wave), else one block per matrix; the chunk length makes every thread walk 16 chunks (seeding 16 chunks'
-// high columns is < 2% of the walk at n = 24), exactly when the block count is a power of two.
+// B matrices: floor(R / B) blocks per matrix when the batch is smaller than R (two waves of resident blocks),
+// else one block per matrix; the chunk length makes every thread walk ~4 chunks.
 static I01Plan int01_plan(int n, int64_t B) {
     const int U = walk_inner_bits(n);
     const int nb = n > kMaxGlynnInt01N ? n : n - 1;           // Gray bits
-    int64_t R = int01_resident_blocks(n);
-    uint64_t rounds = 16;
+    // measured on B200 (tools/int01_scan.py, profiles/round2_int01_plan_scan.txt): two waves of resident blocks,
+    // four chunks per thread -- more rounds mean shorter chunks and more seeding
+    int64_t R = 2 * int01_resident_blocks(n);
+    uint64_t rounds = 4;
     // development overrides (plan scans): PERM_INT01_WAVES = resident-block waves, PERM_INT01_ROUNDS = chunks
     // per thread
     if (const char* w = getenv("PERM_INT01_WAVES")) R = (int64_t)(R * atof(w));

@@ -23,7 +23,7 @@ __host__ __device__ constexpr int walk_inner_bits(int n) { return (n - 1) < PERM
 // to overlap an 8-term block); U = 2 also for the constant-bank orders 34, 35, 37, 39, whose register caps
 // (walk.cuh: walk_const_maxnreg) were found for U = 2.
 #ifndef PERM_U2_FROM33
-#define PERM_U2_FROM33 0                                  // (development: U = 2 for every n >= 33)
+#define PERM_U2_FROM33 1                                  // U = 2 for every n >= 33 (n = 33, 36, 38: +6..13%)
 #endif
 __host__ __device__ constexpr int walk_inner_bits(int n) {
     return (n == 34 || n == 35 || n == 37 || n == 39 || n >= 40 || (PERM_U2_FROM33 && n >= 33)) ? 2
@@ -120,6 +120,7 @@ struct WalkLaunch {
     int nseg;
     Segment seg[kMaxSegments];
     ddc* items;             // device: one dd partial per walked item (segment order, chunks in rank order)
+    uint64_t nitems;        // items of the plan (the length of `items`)
     int grid;               // blocks of the main launch
     int use_const;          // run segment `body` in walk_kernel_c
     int body;               // index of the body segment (use_const)

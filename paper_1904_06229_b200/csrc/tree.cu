@@ -28,6 +28,7 @@ struct TreeWs {
 
 __device__ __forceinline__ void export_node(TreeWs* w, uint32_t level, uint64_t index, const ddc& v) {
     const unsigned k = atomicAdd(&w->count, 1u);
+    PERM_DCHECK(k < (unsigned)kTreeMaxNodes);
     if (k < (unsigned)kTreeMaxNodes) {
         w->exp[k].level = level;
         w->exp[k].reserved = 0;
@@ -48,6 +49,7 @@ __global__ void __launch_bounds__(kGroup) tree_pass_kernel(const ddc* __restrict
     const int lo = a0 > gb ? (int)(a0 - gb) : 0;
     const int hi = end < gb + kGroup ? (int)(end - gb) : kGroup;
     const int t = threadIdx.x;
+    PERM_DCHECK(lo >= 0 && lo < hi && hi <= kGroup && gb + (uint64_t)hi - a0 <= cnt);
     if (t >= lo && t < hi) s[t] = in[gb + t - a0];
     __syncthreads();
 #pragma unroll 1
@@ -70,6 +72,7 @@ __global__ void __launch_bounds__(kGroup) tree_pass_kernel(const ddc* __restrict
         if (comp) s[t] = v;
         __syncthreads();
     }
+    PERM_DCHECK(!(t == 0 && lo == 0 && hi == kGroup) || g >= out_a0);
     if (t == 0 && lo == 0 && hi == kGroup) out[g - out_a0] = s[0];
 }
 
@@ -78,6 +81,7 @@ __global__ void tree_finish_kernel(TreeWs* w, TreeNode* __restrict__ nodes, ddc*
                                    ddc* __restrict__ out_dd, double2* __restrict__ out_c, double f) {
     if (threadIdx.x != 0) return;
     unsigned m = w->count;
+    PERM_DCHECK(m <= (unsigned)kTreeMaxNodes);
     if (m > (unsigned)kTreeMaxNodes) m = kTreeMaxNodes;   // cannot happen: <= 2 per level
     TreeNode* e = w->exp;
     for (unsigned i = 1; i < m; i++) {                    // insertion sort by first leaf

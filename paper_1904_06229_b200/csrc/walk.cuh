@@ -74,6 +74,7 @@ using WalkCfg = WCfg<N, walk_lanes_per_chunk(N)>;
 struct WalkParams {
     const double2* A;                      // device, row-major
     ddc* items;                            // one dd partial per item, at seg_item0[s] + (index in segment)
+    uint64_t nitems;                       // items of the whole launch plan (bounds of `items`)
     uint64_t seg_item0[kMaxSegments];
     uint64_t seg_c0[kMaxSegments];
     uint64_t seg_pre[kMaxSegments + 1];    // prefix item counts
@@ -539,6 +540,7 @@ __global__ void __launch_bounds__(WalkCfg<N>::NT, WalkCfg<N>::MINB) walk_kernel(
 #pragma unroll
                 for (int off = C::S / 2; off > 0; off >>= 1) v = ddc_add(v, shfl_down_ddc(v, off, group_mask<C::S>()));
             }
+            PERM_DCHECK(P.seg_item0[s] + i < P.nitems);
             if (h == 0) P.items[P.seg_item0[s] + i] = v;
         }
     }
@@ -570,6 +572,9 @@ struct WalkParamsC {
     const double2* A;                      // device, row-major (staged to shared memory)
     ddc* items;                            // item partials; body chunk c0 + g -> items[item0 + g]
     uint64_t item0;
+#ifdef PERM_DEBUG_CHECKS
+    uint64_t nitems;                       // (debug build: bounds of `items`)
+#endif
     uint64_t c0;                           // first body chunk
     uint64_t count;                        // body chunks
     int32_t eb;                            // log2 body chunk length (>= U)
@@ -728,6 +733,9 @@ __device__ __forceinline__ void walk_body_c(const WalkParamsC<N>& P) {
         ddc part;
         part.re.hi = part.re.lo = part.im.hi = part.im.lo = 0.0;
         walk_chunk_const<C>(P, lc, lb, P.c0 + (valid ? g : 0), part);
+#ifdef PERM_DEBUG_CHECKS
+        PERM_DCHECK(!valid || P.item0 + g < P.nitems);
+#endif
         if (valid) P.items[P.item0 + g] = part;
     }
 }
@@ -873,6 +881,7 @@ cudaError_t walk_launch_smem(const WalkLaunch& L, const Segment* seg, const uint
     WalkParams P;
     P.A = L.A_dev;
     P.items = L.items;
+    P.nitems = L.nitems;
     uint64_t pre = 0;
     for (int s = 0; s < kMaxSegments; s++) {
         P.seg_pre[s] = pre;
@@ -919,6 +928,9 @@ cudaError_t walk_launch(const WalkLaunch& L) {
             P.A = L.A_dev;
             P.items = L.items;
             P.item0 = item0[L.body];
+#ifdef PERM_DEBUG_CHECKS
+            P.nitems = L.nitems;
+#endif
             P.c0 = b.c0;
             P.count = b.count;
             P.eb = b.e;
