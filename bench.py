@@ -257,7 +257,6 @@ def oracle_rate_cfg(cfg: str, seconds: float = 12.0) -> dict:
         return {"value": k / dt, "unit": "perms/s", "cores": cores, "kind": "oracle",
                 "sample": f"Eq. (3) int128 oracle on {k} of the 64 config-3 matrices, {dt:.1f} s"}
     if cfg == "cfg3s":
-        import numpy as np
         A = inputs.bernoulli01((1, 33, 33), 33)[0]
         B = np.ascontiguousarray(A[:24, :24])
         t0 = time.perf_counter()
