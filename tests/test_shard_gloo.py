@@ -143,3 +143,86 @@ def test_int01_finalize_host_logic():
     assert perm_int01_finalize(parts[::-1], n) == oracle.ryser_i01_batch(A[None])[0]   # order-free
     with pytest.raises(PermError):
         perm_int01_finalize(parts[:2], n)          # an incomplete cover is not divisible by 2^{n-1}
+
+
+def _span_nodes(leaves, a, b):
+    """Maximal canonical tree nodes of the chunk span [a, b) as a node buffer: each node's value is the
+    canonical merge of its leaves (the library's host merge, which is what the device tree computes)."""
+    import paper_1904_06229_b200 as pb
+    entries = []
+    while a < b:
+        lv = 0
+        while a % (1 << (lv + 1)) == 0 and a + (1 << (lv + 1)) <= b:
+            lv += 1
+        k = a >> lv
+        sub = [(0, c, leaves[c]) for c in range(k << lv, (k + 1) << lv)]
+        raw, _ = pb.perm_c128_tree_combine(pb.make_tree_nodes(sub))
+        entries.append((lv, k, raw.astuple()))
+        a += 1 << lv
+    buf = np.zeros((pb.TREE_MAX_NODES, 6), dtype=np.int64)
+    raw = pb.make_tree_nodes(entries + [(pb.TREE_UNUSED, 0, (0, 0, 0, 0))] * (pb.TREE_MAX_NODES - len(entries)))
+    buf.view(np.uint8).reshape(-1)[:] = raw
+    return buf
+
+
+def _chunk_leaves(n, b):
+    """Oracle dd partials of every chunk of 2^b ranks (App. A subpermanent per chunk) -- stand-ins for
+    perm_c128_chunks' output in this CPU test."""
+    import oracle
+    from paper_1904_06229_b200 import inputs
+    A = inputs.complex_gaussian((n, n), 91)
+    out = []
+    for c in range(1 << (n - 1 - b)):
+        q = oracle.subpermanent(A, c << b, 1 << b)
+        out.append((float(q.re_hi), float(q.re_lo), float(q.im_hi), float(q.im_lo)))
+    return A, out
+
+
+def _tree_worker(rank, world, port, n, b, steps, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1904_06229_b200 import shard
+        _, leaves = _chunk_leaves(n, b)
+        c0, c1 = shard.chunk_span(n, world, rank, b)
+        collected = []
+        for s0, s1 in shard.step_slices(c0, c1, steps, 3):        # a "wave" of 3 chunks
+            nodes = torch.from_numpy(_span_nodes(leaves, s0, s1))
+            gathered = torch.empty((world * nodes.shape[0], 6), dtype=torch.int64)
+            dist.all_gather_into_tensor(gathered, nodes)
+            collected.append(gathered.numpy().copy())
+        v, d = shard.combine_nodes(np.concatenate(collected), n, return_dd=True)
+        q.put((rank, d.astuple(), c0, c1))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,steps", [(2, 1), (3, 2), (4, 3)])
+def test_chunk_tree_sharding_is_bit_identical(world, steps):
+    """The chunk path's host logic over gloo: whole-chunk spans per rank (distribute over chunks), each
+    rank's span sliced into steps, one all-gather of the tree-node arrays per step, canonical merge --
+    every rank gets the same double-double, bitwise equal to merging all chunk partials in one process,
+    and equal to the oracle's permanent within the north-star bound."""
+    import paper_1904_06229_b200 as pb
+    from tests import pins
+    import oracle
+    n, b = 10, 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_tree_worker, args=(r, world, port, n, b, steps, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    A, leaves = _chunk_leaves(n, b)
+    raw, root = pb.perm_c128_tree_combine(pb.make_tree_nodes([(0, c, v) for c, v in enumerate(leaves)]))
+    assert root == n - 1 - b
+    _, ref_dd = pb.perm_c128_finalize([raw], n, return_dd=True)
+    assert all(d == ref_dd.astuple() for _, d, _, _ in res), res
+    spans = sorted((c0, c1) for _, _, c0, c1 in res)
+    assert spans[0][0] == 0 and spans[-1][1] == 1 << (n - 1 - b)
+    assert pins.scaled_error(ref_dd.value, oracle.ryser(A).value, A) <= 1e-12
