@@ -302,8 +302,9 @@ perm_status_t run_walk(const perm_c128_t* A, int n, uint64_t k0, uint64_t k1, in
     WalkPlan p;
     perm_status_t st = plan_walk(n, k0, k1, b_req, p);
     if (st != PERM_OK) return st;
-    const bool small = n_final > 0 && n <= perm::kSmallMaxN && p.items <= perm::kSmallMaxChunks && p.nseg == 1 &&
-                       k0 == 0 && (p.items & (p.items - 1)) == 0;
+    static const bool small_enabled = !(getenv("PERM_SMALL_PATH") && atoi(getenv("PERM_SMALL_PATH")) == 0);
+    const bool small = small_enabled && n_final > 0 && n <= perm::kSmallMaxN && p.items <= perm::kSmallMaxChunks &&
+                       p.nseg == 1 && k0 == 0 && (p.items & (p.items - 1)) == 0;   // (PERM_SMALL_PATH=0: development)
     const WsLayout L = ws_layout(n, small ? 0 : p.items);
     char* ws = (char*)workspace;
     bool own_ws = false;

@@ -393,7 +393,9 @@ __device__ __forceinline__ void seed_rows(uint32_t lc, uint32_t lb, uint64_t x, 
         wr[i] = b.x;
         wi[i] = b.y;
     }
-    for (int j = j0; j < N - 1; j++) {
+    // columns in DESCENDING order (every walk seeds this way): for lanes walking consecutive chunks the high
+    // columns come first and are warp-uniform, so the small-permanent kernel can share that prefix exactly
+    for (int j = N - 2; j >= j0; j--) {
         const double f = (double)((x >> j) & 1ull);
         flip_dyn<R>(lc + (uint32_t)(j * P) * 16u, f, wr, wi);
     }
@@ -638,7 +640,7 @@ __device__ __forceinline__ void walk_chunk_const(const WalkParamsC<C::N>& P, uin
         wi[i] = b.y;
     }
     const uint64_t x = ((c ^ (c >> 1)) << e) | ((c & 1ull) << (e - 1));
-    for (int j = e - 1; j < N - 1; j++) {                 // seed, App. A steps 5-8 (shared memory)
+    for (int j = N - 2; j >= e - 1; j--) {                // seed, App. A steps 5-8 (shared memory), descending
         const double f = (double)((x >> j) & 1ull);
         flip_dyn<N>(lc + (uint32_t)(j * N) * 16u, f, wr, wi);
     }
@@ -764,9 +766,46 @@ __global__ void __launch_bounds__(kSmallMaxThreads) walk_small_kernel(const doub
     const uint64_t c = (uint64_t)cluster.block_rank() * T + t;
     ddc acc;
     acc.re.hi = acc.re.lo = acc.im.hi = acc.im.lo = 0.0;
-    if constexpr (C::U >= 1) {
-        if (e == 0) single_term<C>(lc, lb, 0u, c, acc);
-        else        walk_chunk<C>(lc, lb, 0u, c, e, acc);
+    // the chunk length of a whole permanent is a compile-time function of n: with it as a constant the
+    // seeding loop and the block loop unroll (same operations in the same order as the generic walk)
+    constexpr int E = walk_chunk_log2(N);
+    (void)e;
+    if constexpr (C::U >= 1 && E > 0) {
+        // seed w(gray(c 2^E)) -- the same operations in the same order as seed_rows -- sharing the warp-uniform
+        // high columns: with T a multiple of 32 the lanes' chunks differ only in their low 5 bits, so Gray bits
+        // >= 5 of c, i.e. columns >= E + 5, are the same for the whole warp.  Lane i (< N) folds those columns
+        // into row i once; the rows are broadcast; each lane adds its own low columns.
+        constexpr int R = C::R;
+        double wr[R], wi[R];
+        const uint64_t x = ((c ^ (c >> 1)) << E) | ((c & 1ull) << (E - 1));
+        int jlo = E - 1;                                 // lowest column folded by this lane alone
+        if (T >= 32) {
+            const int lane = t & 31;
+            double pr = 0.0, pi = 0.0;
+            if (lane < N) {
+                const double2 b = lds_c(lb + (uint32_t)lane * 16u);
+                pr = b.x;
+                pi = b.y;
+                for (int j = N - 2; j >= E + 5; j--) {
+                    const double f = (double)((x >> j) & 1ull);
+                    const double2 a = lds_c(lc + (uint32_t)(j * C::P + lane) * 16u);
+                    pr = fma(f, a.x, pr);
+                    pi = fma(f, a.y, pi);
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < R; i++) {
+                wr[i] = __shfl_sync(0xffffffffu, pr, i);
+                wi[i] = __shfl_sync(0xffffffffu, pi, i);
+            }
+            for (int j = (E + 4 < N - 2 ? E + 4 : N - 2); j >= jlo; j--) {
+                const double f = (double)((x >> j) & 1ull);
+                flip_dyn<R>(lc + (uint32_t)(j * C::P) * 16u, f, wr, wi);
+            }
+        } else {
+            seed_rows<C>(lc, lb, x, jlo, wr, wi);
+        }
+        walk_seeded<C>(lc, 0u, c, E, wr, wi, acc);
     } else {
         single_term<C>(lc, lb, 0u, c, acc);
     }
@@ -781,17 +820,29 @@ __global__ void __launch_bounds__(kSmallMaxThreads) walk_small_kernel(const doub
     }
     if ((t & 31) == 0) tree[t >> 5] = acc;
     __syncthreads();
-    const int nw = (T + 31) >> 5;
-    for (int off = 1; off < nw; off <<= 1) {
-        if (t < nw && (t & (2 * off - 1)) == 0) tree[t] = ddc_add(tree[t], tree[t + off]);
-        __syncthreads();
+    const int nw = (T + 31) >> 5;                        // warp roots: finished by warp 0 in shuffles
+    if (nw > 1 && t < 32) {
+        ddc r;
+        r.re.hi = r.re.lo = r.im.hi = r.im.lo = 0.0;
+        if (t < nw) r = tree[t];
+#pragma unroll
+        for (int off = 1; off < 8; off <<= 1) {          // nw <= kSmallMaxThreads / 32 = 8
+            const ddc o = shfl_down_ddc(r, off);
+            if (off < nw && (t & (2 * off - 1)) == 0) r = ddc_add(r, o);
+        }
+        if (t == 0) tree[0] = r;
     }
-    cluster.sync();                                      // every CTA root is in its tree[0]
+    // every CTA pushes its root into CTA 0's shared memory (distributed shared memory store), then ONE cluster
+    // barrier (release/acquire): after it only CTA 0 reads, from its own shared memory, so the others may exit
+    __shared__ ddc roots[16];
+    __syncthreads();
+    if (t == 0) *cluster.map_shared_rank(&roots[cluster.block_rank()], 0) = tree[0];
+    cluster.sync();
     const int nb = (int)cluster.num_blocks();
     if (cluster.block_rank() == 0 && t < 32) {
         ddc r;
         r.re.hi = r.re.lo = r.im.hi = r.im.lo = 0.0;
-        if (t < nb) r = *cluster.map_shared_rank(&tree[0], t);
+        if (t < nb) r = roots[t];
 #pragma unroll
         for (int off = 1; off < 16; off <<= 1) {
             const ddc o = shfl_down_ddc(r, off, wmask);
@@ -805,7 +856,6 @@ __global__ void __launch_bounds__(kSmallMaxThreads) walk_small_kernel(const doub
             if (out_c) *out_c = make_double2(r.re.hi + r.re.lo, r.im.hi + r.im.lo);
         }
     }
-    cluster.sync();                                      // keep every CTA's shared memory alive until read
 }
 
 template <int N>
@@ -816,6 +866,7 @@ cudaError_t walk_small_launch(const double2* A_dev, int e, uint64_t chunks, ddc*
     } else {
         using C = WalkCfg<N>;
         if (chunks < 1 || chunks > (uint64_t)kSmallMaxChunks || (chunks & (chunks - 1))) return cudaErrorInvalidValue;
+        if (e != walk_chunk_log2(N)) return cudaErrorInvalidValue;    // the kernel walks chunks of 2^b(n)
         int ncta = (int)(chunks / 64);
         ncta = ncta < 1 ? 1 : (ncta > 16 ? 16 : ncta);
         const int T = (int)(chunks / (uint64_t)ncta);
