@@ -43,10 +43,9 @@ template <int N>
 struct WgtCfg {
     static constexpr int NT = 32;                    // one warp (one problem at a time) per block
 #ifndef PERM_WGT_REG_EXTRA
-    // working-set registers beyond the 4n row sums: 96, or 128 for the orders that spill at 96 / 112
-    // (tools/spills.py; the extra budget costs occupancy, so only where needed -- n = 20 keeps 96)
-    static constexpr int EXTRA = (N == 12 || N == 14 || N == 15 || N == 16 || N == 18 || N == 23 || N == 25 ||
-                                  N >= 26) ? 128 : 96;
+    // working-set registers beyond the 4n row sums (0 spill bytes at every order, tools/spills.py, with the
+    // unrolled sweeps of m_s <= kWgtSpecMax)
+    static constexpr int EXTRA = (N == 23 || N == 24) ? 160 : 128;
 #else
     static constexpr int EXTRA = PERM_WGT_REG_EXTRA;
 #endif
@@ -69,6 +68,36 @@ __host__ __device__ constexpr size_t wgt_slot_bytes(int N, int R) {
     // (3 R ints), the lanes' outer digits and directions (2 R x 32 bytes)
     return ((size_t)(R + 2) * N * 16 + (size_t)(R + 2) * (N + 1) * 8 + (size_t)3 * R * 4 + (size_t)2 * R * 32 + 15) &
            ~(size_t)15;
+}
+
+// One sweep of the fastest digit f_s over its m_s + 1 values (terms j = 0..m_s): weight, product, signed sum,
+// then the step to the next value (+-cbar_s by address).  MS >= 0: m_s known at compile time (unrolled).
+#ifndef PERM_WGT_SPECIALISE
+#define PERM_WGT_SPECIALISE 1
+#endif
+constexpr bool kWgtSpecialise = PERM_WGT_SPECIALISE != 0;
+#ifndef PERM_WGT_SPEC_MAX
+#define PERM_WGT_SPEC_MAX 2
+#endif
+constexpr int kWgtSpecMax = PERM_WGT_SPEC_MAX;   // largest m_s with an unrolled sweep
+template <int N, int MS>
+__device__ __forceinline__ void wgt_sweep(int ms, double sc2, const double* tsw, int& f1, int d1, uint32_t step,
+                                          double (&wr)[N], double (&wi)[N], double& ar, double& ai) {
+    const int m = MS >= 0 ? MS : ms;
+#pragma unroll (MS >= 0 ? MS + 1 : kWgtUnroll)
+    for (int j = 0; j <= m; j++) {
+        const double wt = sc2 * tsw[f1];
+        double xr, xi, yr, yi;
+        two_factors<N, kWgtChains<N>>(wr, wi, xr, xi, yr, yi);
+        if constexpr (N == 1) { yr = 1.0; yi = 0.0; }
+        xr *= wt;
+        xi *= wt;
+        fused_acc<+1>(xr, xi, yr, yi, ar, ai);
+        if (j < m) {
+            flip_add<N>(step, wr, wi);
+            f1 += d1;
+        }
+    }
 }
 
 template <int N>
@@ -196,19 +225,13 @@ __global__ void __launch_bounds__(WgtCfg<N>::NT, WgtCfg<N>::MINB)
                     const double sc2 = scale * tsw2[f2];
                     const uint32_t step = fwd1 ? cs : nbase;
                     const int d1 = fwd1 ? 1 : -1;
-#pragma unroll (kWgtUnroll)
-                    for (int j = 0; j <= ms; j++) {
-                        const double wt = sc2 * tsw[f1];
-                        double xr, xi, yr, yi;
-                        two_factors<N, kWgtChains<N>>(wr, wi, xr, xi, yr, yi);
-                        if constexpr (N == 1) { yr = 1.0; yi = 0.0; }
-                        xr *= wt;
-                        xi *= wt;
-                        fused_acc<+1>(xr, xi, yr, yi, ar, ai);
-                        if (j < ms) {
-                            flip_add<N>(step, wr, wi);
-                            f1 += d1;
-                        }
+                    // the fast sweep, unrolled for the common small multiplicities (warp-uniform switch)
+                    switch (kWgtSpecialise && N <= 24 && ms <= kWgtSpecMax ? ms : -1) {
+                        case 1: wgt_sweep<N, 1>(ms, sc2, tsw, f1, d1, step, wr, wi, ar, ai); break;
+                        case 2: wgt_sweep<N, 2>(ms, sc2, tsw, f1, d1, step, wr, wi, ar, ai); break;
+                        case 3: wgt_sweep<N, (kWgtSpecMax >= 3 ? 3 : -1)>(ms, sc2, tsw, f1, d1, step, wr, wi, ar, ai); break;
+                        case 4: wgt_sweep<N, (kWgtSpecMax >= 4 ? 4 : -1)>(ms, sc2, tsw, f1, d1, step, wr, wi, ar, ai); break;
+                        default: wgt_sweep<N, -1>(ms, sc2, tsw, f1, d1, step, wr, wi, ar, ai); break;
                     }
                     fwd1 = !fwd1;
                     if (r < ms2) {
