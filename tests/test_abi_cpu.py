@@ -160,3 +160,31 @@ def test_no_register_spills_in_library_kernels():
         pytest.skip("no ptxas logs (library not built in this tree)")
     bad = {k: v for k, v in d.items() if v[0] > 0}
     assert not bad, bad
+
+
+def test_chunk_and_tree_argument_validation_without_gpu():
+    """perm_c128_chunks / perm_c128_tree / perm_chunk_walkers reject bad arguments before any device work."""
+    L = pb.lib()
+    A = np.eye(10, dtype=np.complex128)
+    p = A.ctypes.data_as(ctypes.c_void_p)
+    dummy = ctypes.c_void_p(1)
+    C = L.perm_c128_chunks
+    assert C(None, 10, 3, 0, 1, dummy, None, 0, None, None) == 1                 # null A
+    assert C(p, 0, 3, 0, 1, dummy, None, 0, None, None) == 2                     # n < 1
+    assert C(p, 65, 3, 0, 1, dummy, None, 0, None, None) == 2                    # n > 64
+    assert C(p, 10, 1, 0, 1, dummy, None, 0, None, None) == 1                    # 0 < b < U(10) = 3
+    assert C(p, 10, 10, 0, 1, dummy, None, 0, None, None) == 1                   # b > n - 1
+    assert C(p, 10, 3, 2, 1, dummy, None, 0, None, None) == 1                    # c_begin > c_end
+    assert C(p, 10, 3, 0, 65, dummy, None, 0, None, None) == 2                   # c_end > 2^{n-1-b}
+    assert C(p, 10, 3, 5, 5, None, None, 0, None, None) == 0                     # empty span: no-op
+    T = L.perm_c128_tree
+    assert T(dummy, 3, 2, dummy, None, None, 0, None) == 1                       # c_begin > c_end
+    assert T(dummy, 0, 4, None, None, None, 0, None) == 1                        # no output at all
+    assert T(None, 0, 4, dummy, None, None, 0, None) == 1                        # partials missing
+    w = ctypes.c_uint64()
+    assert L.perm_chunk_walkers(0, 3, ctypes.byref(w)) == 2
+    assert L.perm_chunk_walkers(10, 3, None) == 1
+    b = ctypes.c_size_t()
+    assert L.perm_tree_workspace_bytes(1 << 25, ctypes.byref(b)) == 0 and b.value > (1 << 25) * 32 // 255
+    assert L.perm_c128_batched_x(None, 8, 0, None, None, None, None) == 0         # B == 0: no-op
+    assert L.perm_c128_batched_x(None, 8, 4, None, None, None, None) == 1         # nothing requested
