@@ -862,7 +862,10 @@ def run_ours(args):
         achieved = roofline_units / (walk_ms * 1e-3) / 1e12
         out["roofline"] = {"bound": "alu", "achieved": achieved, "peak": nominal, "unit": "TFLOP/s",
                            "frac": achieved / nominal, "traffic": ncu_traffic(cfg),
-                           "kernel": "walk_kernel<n> (FP64 vector pipe)",
+                           "kernel": ((f"walk_small_kernel<{n}> (one cluster launch: walk + tree)" if n <= 16
+                                       else f"walk_kernel_c<{n}>" if n == 32
+                                       else f"walk_kernel_cm<{n}>" if 33 <= n <= 48 else f"walk_kernel<{n}>")
+                                      + " (FP64 vector pipe)"),
                            "algorithmic": "8n flops per Gray term x terms per launch (rank 0)",
                            "peak_note": "derived: 148 SMs x 64 FP64 FMA/clk x 2 x 1965 MHz",
                            "peak_measured_probe": peak_meas, "frac_of_measured": achieved / peak_meas,
