@@ -12,6 +12,28 @@
 #include "../../include/perm.h"
 #include "internal.h"
 
+namespace perm {
+
+cudaError_t malloc_async(void** p, size_t bytes, cudaStream_t s) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    static std::once_flag once[64];
+    if (dev >= 0 && dev < 64) {
+        std::call_once(once[dev], [](int d) {
+            cudaMemPool_t pool;
+            if (cudaDeviceGetDefaultMemPool(&pool, d) == cudaSuccess) {
+                uint64_t thr = UINT64_MAX;
+                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+            }
+            cudaGetLastError();
+        }, dev);
+    }
+    return cudaMallocAsync(p, bytes, s);
+}
+
+}  // namespace perm
+
 namespace {
 
 using perm::ddc;
@@ -309,7 +331,7 @@ perm_status_t run_walk(const perm_c128_t* A, int n, uint64_t k0, uint64_t k1, in
     char* ws = (char*)workspace;
     bool own_ws = false;
     if (ws == nullptr) {
-        PERM_CUDA(cudaMallocAsync((void**)&ws, L.total, s), "cudaMallocAsync(workspace)");
+        PERM_CUDA(perm::malloc_async((void**)&ws, L.total, s), "cudaMallocAsync(workspace)");
         own_ws = true;
     } else if (workspace_bytes < L.total) {
         return PERM_E_WORKSPACE;
@@ -529,7 +551,7 @@ perm_status_t perm_c128_chunks(const perm_c128_t* A, int n, int chunk_log2, uint
     bool own = false;
     if (!a_dev) {
         if (!ws) {
-            PERM_CUDA(cudaMallocAsync((void**)&ws, a_bytes, s), "cudaMallocAsync(A)");
+            PERM_CUDA(perm::malloc_async((void**)&ws, a_bytes, s), "cudaMallocAsync(A)");
             own = true;
         } else if (workspace_bytes < a_bytes) {
             return PERM_E_WORKSPACE;
@@ -569,7 +591,7 @@ perm_status_t perm_c128_tree(const perm_dd_c128_t* partials_dev, uint64_t c_begi
     char* ws = (char*)workspace;
     bool own = false;
     if (!ws) {
-        PERM_CUDA(cudaMallocAsync((void**)&ws, need, s), "cudaMallocAsync(tree workspace)");
+        PERM_CUDA(perm::malloc_async((void**)&ws, need, s), "cudaMallocAsync(tree workspace)");
         own = true;
     } else if (workspace_bytes < need) {
         return PERM_E_WORKSPACE;
@@ -810,7 +832,7 @@ perm_status_t perm_c128_sparse(const perm_c128_t* A, int n, perm_c128_t* out_hos
     char* ws = nullptr;
     const size_t part_bytes = (size_t)L.grid * sizeof(ddc);
     const size_t total = part_bytes + sizeof(ddc) + (a_dev ? 0 : (size_t)n * n * sizeof(double2));
-    PERM_CUDA(cudaMallocAsync((void**)&ws, total, s), "cudaMallocAsync(sparse workspace)");
+    PERM_CUDA(perm::malloc_async((void**)&ws, total, s), "cudaMallocAsync(sparse workspace)");
     perm_status_t result = PERM_OK;
     do {
         const double2* A_dev = (const double2*)A;
@@ -893,7 +915,7 @@ static perm_status_t run_int(const uint8_t* A_dev, bool pm1, int n, int64_t B, p
     char* ws = (char*)workspace;
     bool own = false;
     if (!ws) {
-        PERM_CUDA(cudaMallocAsync((void**)&ws, need, s), "cudaMallocAsync(workspace)");
+        PERM_CUDA(perm::malloc_async((void**)&ws, need, s), "cudaMallocAsync(workspace)");
         own = true;
     } else if (workspace_bytes < need) {
         return PERM_E_WORKSPACE;
@@ -936,7 +958,7 @@ perm_status_t perm_int01_range(const uint8_t* A_dev, int n, uint64_t k_begin, ui
     if (k_begin == k_end) return PERM_OK;
     cudaStream_t s = (cudaStream_t)stream;
     char* ws = nullptr;
-    PERM_CUDA(cudaMallocAsync((void**)&ws, perm::int01_range_workspace_bytes(), s), "cudaMallocAsync(workspace)");
+    PERM_CUDA(perm::malloc_async((void**)&ws, perm::int01_range_workspace_bytes(), s), "cudaMallocAsync(workspace)");
     unsigned long long raw[2] = {0, 0};
     int flag = 0, l = 0;
     const cudaError_t e = perm::int01_range_launch(A_dev, n, k_begin, k_end, ws, s, raw, &flag, &l);
@@ -984,7 +1006,7 @@ perm_status_t perm_c128_seed(const perm_c128_t* A, int n, const uint64_t* ranks,
     const size_t r_bytes = (size_t)count * sizeof(uint64_t);
     const size_t w_bytes = (size_t)count * n * sizeof(double2);
     char* ws = nullptr;
-    PERM_CUDA(cudaMallocAsync((void**)&ws, align256(a_bytes) + align256(r_bytes) + w_bytes, s), "cudaMallocAsync");
+    PERM_CUDA(perm::malloc_async((void**)&ws, align256(a_bytes) + align256(r_bytes) + w_bytes, s), "cudaMallocAsync");
     char* a_d = ws;
     char* r_d = ws + align256(a_bytes);
     char* w_d = r_d + align256(r_bytes);

@@ -169,6 +169,11 @@ size_t tree_workspace_bytes(uint64_t count);
 cudaError_t tree_launch(const ddc* leaves, uint64_t a0, uint64_t count, void* ws, TreeNode* nodes_dev, ddc* raw_dev,
                         ddc* out_dd, double2* out_c, double f, cudaStream_t s, int* launches);
 
+// abi.cu: stream-ordered scratch allocation.  The first call per device raises the release threshold of the
+// device's default memory pool so that freed scratch stays cached (otherwise every synchronisation hands it
+// back to the driver and the next call pays a real allocation on its latency path).
+cudaError_t malloc_async(void** p, size_t bytes, cudaStream_t s);
+
 // reduce.cu
 cudaError_t reduce_launch(const ddc* parts, int count, int n_final, ddc* out_dd, double2* out_c,
                           cudaStream_t s);

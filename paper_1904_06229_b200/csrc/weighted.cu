@@ -288,7 +288,7 @@ cudaError_t weighted_launch_t(const double2* C, const int32_t* mult, int R, int6
     const int64_t cap = (int64_t)sms * bps;
     const int64_t grid = B < cap ? B : cap;
     unsigned long long* next = nullptr;                     // the work-queue counter, stream-ordered
-    err = cudaMallocAsync((void**)&next, sizeof(unsigned long long), st);
+    err = malloc_async((void**)&next, sizeof(unsigned long long), st);
     if (err != cudaSuccess) return err;
     err = cudaMemsetAsync(next, 0, sizeof(unsigned long long), st);
     if (err == cudaSuccess) {
