@@ -89,33 +89,14 @@ __device__ __forceinline__ double2 lds_c(uint32_t addr) {
     return v;
 }
 
-// (xr + i xi) *= (yr + i yi): 4 FP64 instructions.  With PERM_CMUL_FMA0 the two products are
-// written as fma(a, b, +0.0) (bit-identical to a*b except for the sign of an exact zero), so all four
-// are DFMA and ptxas can serve a repeated operand from the operand-reuse cache across consecutive
-// DFMAs (DMUL -> DFMA pairs do not share it); three-vector-operand DFMAs issue at ~0.7 of the FP64
-// pipe rate on B200 (tools/micro/fp64_banks2.cu), so reuse is what keeps the chain at pipe speed.
+// (xr + i xi) *= (yr + i yi): 4 FP64 instructions (2 DMUL + 2 DFMA).  Measured and not kept (round 1-2):
+// products as fma(a, b, +0.0) so all four are DFMA, and alternating the roles of xr and xi along a chain.
 __device__ __forceinline__ void cmul2(double& xr, double& xi, double yr, double yi) {
-#ifdef PERM_CMUL_FMA0
-    const double t = fma(xi, yi, 0.0);
-    const double u = fma(xi, yr, 0.0);
-#else
     const double t = xi * yi;
     const double u = xi * yr;
-#endif
     const double nr = fma(xr, yr, -t);
     xi = fma(xr, yi, u);
     xr = nr;
-}
-
-// The same product with the roles of xr and xi swapped: the two DMULs read xr (the first result of
-// the previous cmul2), the DFMAs xi.  Alternating the two forms along a chain lets each multiply
-// start on the half of the previous result that is ready first.
-__device__ __forceinline__ void cmul2_alt(double& xr, double& xi, double yr, double yi) {
-    const double t = xr * yi;
-    const double u = xr * yr;
-    const double ni = fma(xi, yr, t);
-    xr = fma(-xi, yi, u);
-    xi = ni;
 }
 
 // Product of rows [B, E) into (pr, pi).
@@ -124,14 +105,7 @@ __device__ __forceinline__ void chain(const double (&wr)[R], const double (&wi)[
     pr = wr[B];
     pi = wi[B];
 #pragma unroll
-    for (int i = B + 1; i < E; i++) {
-#ifdef PERM_CMUL_ALT
-        if ((i - B) & 1) cmul2(pr, pi, wr[i], wi[i]);
-        else             cmul2_alt(pr, pi, wr[i], wi[i]);
-#else
-        cmul2(pr, pi, wr[i], wi[i]);
-#endif
-    }
+    for (int i = B + 1; i < E; i++) cmul2(pr, pi, wr[i], wi[i]);
 }
 
 // Split prod_i w_i into two factors X * Y (K chains).
@@ -143,20 +117,8 @@ __device__ __forceinline__ void two_factors(const double (&wr)[R], const double 
         yr = wr[R - 1];
         yi = wi[R - 1];
     } else if constexpr (K == 2) {
-#ifdef PERM_CHAIN_STRIDE2
-        // rows interleaved between the chains (even rows / odd rows): both chains can start as soon as the
-        // first rows of a flip are updated
-        xr = wr[0]; xi = wi[0];
-        yr = wr[1]; yi = wi[1];
-#pragma unroll
-        for (int i = 2; i < R; i++) {
-            if (i & 1) cmul2(yr, yi, wr[i], wi[i]);
-            else       cmul2(xr, xi, wr[i], wi[i]);
-        }
-#else
         chain<0, R / 2, R>(wr, wi, xr, xi);
         chain<R / 2, R, R>(wr, wi, yr, yi);
-#endif
     } else if constexpr (K == 3) {
         constexpr int t = R / 3;
         double zr, zi;
@@ -204,11 +166,9 @@ __device__ __forceinline__ void two_factors(const double (&wr)[R], const double 
         xr = cr[0]; xi = ci[0];
         yr = cr[1]; yi = ci[1];
     } else {
-        constexpr int q = R / 4;
-        double r0, i0, r1, i1, r2, i2, r3, i3;
-#ifndef PERM_CHAIN_BLOCK4
         // rows dealt round-robin to the four chains (chain c: rows c, c+4, ...); the two products then
         // multiply each other in the fused accumulation
+        double r0, i0, r1, i1, r2, i2, r3, i3;
         r0 = wr[0]; i0 = wi[0]; r1 = wr[1]; i1 = wi[1]; r2 = wr[2]; i2 = wi[2]; r3 = wr[3]; i3 = wi[3];
 #pragma unroll
         for (int i = 4; i < R; i++) {
@@ -217,13 +177,6 @@ __device__ __forceinline__ void two_factors(const double (&wr)[R], const double 
             else if ((i & 3) == 2) cmul2(r2, i2, wr[i], wi[i]);
             else cmul2(r3, i3, wr[i], wi[i]);
         }
-        (void)q;
-#else
-        chain<0, q, R>(wr, wi, r0, i0);
-        chain<q, 2 * q, R>(wr, wi, r1, i1);
-        chain<2 * q, 3 * q, R>(wr, wi, r2, i2);
-        chain<3 * q, R, R>(wr, wi, r3, i3);
-#endif
         cmul2(r0, i0, r1, i1);
         cmul2(r2, i2, r3, i3);
         xr = r0; xi = i0; yr = r2; yi = i2;
@@ -649,11 +602,7 @@ __device__ __forceinline__ void walk_chunk_const(const WalkParamsC<C::N>& P, uin
     constexpr int kFoldMask = (U >= walk_fold_bits_const(N)) ? 0 : ((1 << (walk_fold_bits_const(N) - U)) - 1);
     double ar = 0.0, ai = 0.0;
     for (int q = 0; q < nblk; q++) {
-#ifdef PERM_CONST_SHFL_Z
-        const int z = __shfl_sync(0xffffffffu, q >> 30, 0);   // 0; explicitly warp-uniform, loop-variant
-#else
         const int z = q >> 30;                            // 0 (nblk <= 2^27); uniform, loop-variant
-#endif
         if (q > 0) {
             const int j = U + __ffs(q) - 1;
             const uint64_t nb = (j + 1 < e) ? (uint64_t)((q >> (j + 1 - U)) & 1) : cpar;
