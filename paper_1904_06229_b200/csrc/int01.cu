@@ -122,9 +122,70 @@ __device__ __forceinline__ void int_term(const int (&g)[N], u128& acc) {
     if (SIGN > 0) acc += p; else acc -= p;
 }
 
+// n <= 24 (at most four int32 groups): the 128-bit product and the 128-bit accumulate are replaced by 28-bit
+// limbs.  With u = p0 p1 = u1 2^28 + u0 and w = p2 p3 = w1 2^28 + w0 (0 <= u0, w0 < 2^28, |u1|, |w1| <=
+// n^12 / 2^28 < 2^27.1), the term is u0 w0 + 2^28 (u0 w1 + u1 w0) + 2^56 u1 w1; each limb sum grows by
+// < 2^56.1 per term and is kept in int64 (one IMAD.WIDE with accumulate per partial product), separately for
+// the + and - terms, and folded into the exact int128 total every 64 terms (64 x 2^56.1 < 2^63).  Three
+// groups: u0 p2 + 2^28 u1 p2; two: p0 p1 (< n^12 < 2^56); one: p0.
+template <int N>
+constexpr bool kLimb = ((N + 5) / 6) <= 4;
+constexpr int kLimbFoldBlocks = 8;                // inner blocks of 2^U <= 8 terms between folds
+
+struct Limbs {
+    long long p0, p1, p2, m0, m1, m2;
+};
+
+// s += a b, signed 32 x 32 -> 64 with a 64-bit addend: one IMAD.WIDE (plain C makes ptxas widen first and
+// multiply 64 x 64)
+__device__ __forceinline__ void mad_wide(long long& s, int a, int b) {
+    asm("mad.wide.s32 %0, %1, %2, %0;" : "+l"(s) : "r"(a), "r"(b));
+}
+
+template <int N, int SIGN>
+__device__ __forceinline__ void int_term(const int (&g)[N], Limbs& L) {
+    constexpr int NG = (N + 5) / 6;
+    int p[NG];
+#pragma unroll
+    for (int k = 0; k < NG; k++) {
+        p[k] = g[6 * k];
+#pragma unroll
+        for (int i = 6 * k + 1; i < 6 * k + 6 && i < N; i++) p[k] *= g[i];
+    }
+    long long& s0 = SIGN > 0 ? L.p0 : L.m0;
+    long long& s1 = SIGN > 0 ? L.p1 : L.m1;
+    long long& s2 = SIGN > 0 ? L.p2 : L.m2;
+    if constexpr (NG == 1) {
+        s0 += p[0];
+    } else if constexpr (NG == 2) {
+        mad_wide(s0, p[0], p[1]);
+    } else {
+        const long long u = (long long)p[0] * p[1];
+        const int u0 = (int)((unsigned)u & 0x0FFFFFFFu), u1 = (int)(u >> 28);
+        if constexpr (NG == 3) {
+            mad_wide(s0, u0, p[2]);
+            mad_wide(s1, u1, p[2]);
+        } else {
+            const long long w = (long long)p[2] * p[3];
+            const int w0 = (int)((unsigned)w & 0x0FFFFFFFu), w1 = (int)(w >> 28);
+            mad_wide(s0, u0, w0);
+            mad_wide(s1, u0, w1);
+            mad_wide(s1, u1, w0);
+            mad_wide(s2, u1, w1);
+        }
+    }
+}
+
+__device__ __forceinline__ void limb_fold(Limbs& L, u128& acc) {
+    const __int128 d0 = (__int128)(L.p0 - L.m0), d1 = (__int128)(L.p1 - L.m1), d2 = (__int128)(L.p2 - L.m2);
+    acc += (u128)d0 + ((u128)d1 << 28) + ((u128)d2 << 56);
+    L = Limbs{0, 0, 0, 0, 0, 0};
+}
+
 template <int N, int U, int T>
 struct IntInner {
-    static __device__ __forceinline__ void run(uint32_t sc, int (&g)[N], int zmid, u128& acc) {
+    template <class Acc>
+    static __device__ __forceinline__ void run(uint32_t sc, int (&g)[N], int zmid, Acc& acc) {
         if constexpr (T > 0) {
             constexpr int J = ctz_c((unsigned)T);
             constexpr int NP = I01Cfg<N>::NP;
@@ -165,6 +226,7 @@ __device__ __forceinline__ void int_chunk(uint32_t sc, uint32_t sbase, uint64_t 
         int_seed<N>(sc, sbase, x, e - 1, g);
         const uint64_t nblk = 1ull << (e - U);
         const uint64_t cpar = c & 1ull;
+        [[maybe_unused]] Limbs L{0, 0, 0, 0, 0, 0};
         for (uint64_t q = 0; q < nblk; q++) {
             if (q > 0) {
                 const int j = U + __ffsll((long long)q) - 1;
@@ -172,7 +234,13 @@ __device__ __forceinline__ void int_chunk(uint32_t sc, uint32_t sbase, uint64_t 
                 int_flip<N>(sc + 4u * (uint32_t)(j * I01Cfg<N>::NP), nb ? -1 : 1, g);
             }
             const uint64_t nbm = (U < e) ? (q & 1ull) : cpar;
-            IntInner<N, U, 0>::run(sc, g, nbm ? -1 : 1, acc);
+            if constexpr (kLimb<N>) {
+                static_assert((kLimbFoldBlocks << U) <= 64, "limb sums must stay below 2^63");
+                IntInner<N, U, 0>::run(sc, g, nbm ? -1 : 1, L);
+                if ((q & (kLimbFoldBlocks - 1)) == kLimbFoldBlocks - 1 || q + 1 == nblk) limb_fold(L, acc);
+            } else {
+                IntInner<N, U, 0>::run(sc, g, nbm ? -1 : 1, acc);
+            }
         }
     }
 }
