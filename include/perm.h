@@ -277,6 +277,9 @@ perm_status_t perm_int01_workspace_bytes(int n, int64_t B, size_t* bytes);
  * walked in Gray order; products and the signed sum are exact mod 2^128, per = (-1)^n Sum / 2^{n-1} is
  * exact (n! 2^{n-1} < 2^127), and the low n-1 bits of Sum are checked to be zero.  29 <= n <= 33: the
  * same walk over all 2^n subsets of Eq. (3), Sum = (-1)^{n+1} per, exact while n! < 2^127.
+ * 20 <= n <= 24: each matrix is walked with the Gray column holding the most zeros first and its zero rows
+ * first (per is invariant under row/column permutations), consecutive term pairs factored over those rows
+ * (DESIGN.md 5.3); the result is the same exact integer.
  *   A_dev     device, B*n*n bytes, each 0 or 1, row-major.
  *   out_dev   device, B perm_i128_t.
  * Synchronizes `stream` (to report PERM_E_NOT01 / PERM_E_CHECK).
@@ -294,7 +297,8 @@ perm_status_t perm_pm1(const int8_t* A_dev, int n, int64_t B, perm_i128_t* out_d
                        void* workspace, size_t workspace_bytes, void* stream);
 
 /* Sharding ONE exact 0-1 permanent (App. A partition): the
- * raw signed integer Gray sum over the ranks [k_begin, k_end) of the walk perm_int01 runs,
+ * raw signed integer Gray sum over the ranks [k_begin, k_end) of the Gray walk of A AS GIVEN (Gray bit j =
+ * column j; perm_int01 itself may walk a row- and column-permuted copy, DESIGN.md 5.3 -- same total),
  *     n <= 28:       P = sum_{r} (-1)^{r+1} prod_i g_i(gray r)   (half range, ranks < 2^{n-1})
  *     29 <= n <= 33: P = sum_{r} (-1)^{|gray r|} prod_i r_i(gray r)   (Eq. (3), ranks < 2^n)
  * modulo 2^128 (the exact value's two's-complement bits).  Partials of disjoint spans add exactly (mod

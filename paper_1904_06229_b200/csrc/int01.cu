@@ -16,6 +16,8 @@
 // unrolled inner block of 2^U steps (compile-time columns and signs, warp-uniform broadcast loads).
 // Per-block partial sums (exact, order-free) go to the workspace; a final kernel adds them per
 // matrix, checks divisibility and writes per as int128.
+// n = 20..24 and (0-1 entries) n = 29..33 walk a row/column-permuted copy with consecutive term pairs factored
+// over the rows a bit-0 flip leaves unchanged (see "pair-factored walk" below).
 #include <cstdlib>
 #include <mutex>
 
@@ -35,6 +37,20 @@ struct I01Cfg {
     static constexpr bool FULL = N > kMaxGlynnInt01N;
     static constexpr int NB = FULL ? N : N - 1;      // Gray bits (columns walked)
 };
+
+// Flips whose sign is known only at run time (mid-block bit U-1, block boundary) can read +CM a or -CM a by address
+// (IADD3, alu pipe) instead of computing z * CM a (IMAD, fma pipe): kZNeg for both in the pair-factored walk,
+// kPNeg = 0 / 1 (mid-block) / 2 (both) in the plain walk -- a pipe-balance choice, bit-identical results.
+#ifndef PERM_INT01_ZNEG
+#define PERM_INT01_ZNEG 1
+#endif
+#ifndef PERM_INT01_PNEG
+#define PERM_INT01_PNEG 2
+#endif
+constexpr bool kZNeg = PERM_INT01_ZNEG;
+constexpr int kPNeg = PERM_INT01_PNEG;
+template <int N>
+constexpr uint32_t kZNegOff = 4u * (uint32_t)(N * ((N + 3) & ~3));   // byte offset of the negated columns
 
 __device__ __forceinline__ int lds_i(uint32_t addr) {
     int v;
@@ -182,6 +198,193 @@ __device__ __forceinline__ void limb_fold(Limbs& L, u128& acc) {
     L = Limbs{0, 0, 0, 0, 0, 0};
 }
 
+// ---- pair-factored walk (perm_int01 / perm_pm1, 20 <= n <= 24) ------------------------------------------------
+// Consecutive ranks 2q, 2q+1 of an aligned block differ in Gray bit 0 only and carry opposite signs
+// ((-1)^{r+1}, App. A), so their two terms sum to  prod_{i<Z} g_i * (prod_{i>=Z} g'_i - prod_{i>=Z} g_i)  when the
+// Z rows i < Z have a_{i,0} = 0 (unchanged by the bit-0 flip).  The block stages A with the Gray column holding the
+// most zeros moved to position 0 and those zero rows moved first (per(A) is invariant under row and column
+// permutations, and the walk still visits every sign vector once), then walks with a compile-time Z from a short
+// menu (the largest entry <= the zero count; Z < 12 keeps the plain walk).  Per pair of terms: rows [0, 12) form
+// u = p0 p1 (two int32 groups of 6, |u| <= n^12 < 2^55.1); rows [12, n) form W = vB vA with vB over [12, n-6) and
+// vA over [n-6, n) (int32 each, the constant rows' part computed once per pair); F = W' - W (|F| <= 2 n^{n-12} <
+// 2^56.1) and the pair adds u F, exactly, in three int64 28-bit-limb sums (u0 F0, u0 F1 + u1 F0, u1 F1: < 2^56.6
+// per pair) folded into the int128 total every kZFoldPairs pairs.  Against the plain walk this drops the
+// unchanged rows' updates at every bit-0 flip and their products at every second term.
+template <int N>
+constexpr bool kZSplit = N >= 20 && N <= 24;
+#ifndef PERM_INT01_ZU
+#define PERM_INT01_ZU 4
+#endif
+constexpr int kZU = PERM_INT01_ZU;                 // inner Gray bits of the pair-factored walk (2^{U-1} pairs per block)
+constexpr int kZFoldPairs = 64;                    // 64 x 2^56.6 < 2^63
+
+// minimum resident blocks per SM asked of ptxas (register cap); 1 = no cap
+#ifndef PERM_INT01_MINB
+#define PERM_INT01_MINB 1
+#endif
+constexpr int kInt01MinBlocks = PERM_INT01_MINB;
+
+template <int N>
+constexpr bool kZSplitFull = N > kMaxGlynnInt01N && N <= kMaxInt01N;   // 0-1 only (row sums >= 0)
+
+// full-range orders: Z = n - M for M = 12 (exact u64 W), 15, 18 varying rows
+__device__ __forceinline__ int zsplit_menu_full(int z, int n) {
+    return z >= n - 12 ? n - 12 : z >= n - 15 ? n - 15 : z >= n - 18 ? n - 18 : 0;
+}
+
+// largest menu entry <= z (and <= n - 2), 0 = plain walk
+__device__ __forceinline__ int zsplit_menu(int z, int n) {
+    const int zm = z < n - 2 ? z : n - 2;
+    return zm >= 18 ? 18 : zm >= 16 ? 16 : zm >= 14 ? 14 : zm >= 12 ? 12 : 0;
+}
+
+// g += column (PLUS) or g -= column for rows [LO, N) only (the rows a bit-0 flip can change).
+template <int N, int LO, bool PLUS>
+__device__ __forceinline__ void int_flip_rows(uint32_t col, int (&g)[N]) {
+#pragma unroll
+    for (int i = LO & ~3; i < N; i += 4) {
+        const int4 a = lds_i4(col + 4u * (uint32_t)i);
+        const int v[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+        for (int k = 0; k < 4; k++)
+            if (i + k >= LO && i + k < N) g[i + k] = PLUS ? g[i + k] + v[k] : g[i + k] - v[k];
+    }
+}
+
+template <int N, int LO, int HI>
+__device__ __forceinline__ int int_rowprod(const int (&g)[N], int init) {
+    int p = init;
+#pragma unroll
+    for (int i = LO; i < HI; i++) p *= g[i];
+    return p;
+}
+
+__device__ __forceinline__ long long mul_wide(int a, int b) {
+    long long r;
+    asm("mul.wide.s32 %0, %1, %2;" : "=l"(r) : "r"(a), "r"(b));
+    return r;
+}
+
+struct ZLimbs {
+    long long s0, s1, s2;
+};
+
+// W = vB vA for the current row sums; cB / cA = the constant rows' part of each group (computed once per pair)
+template <int N, int Z>
+__device__ __forceinline__ long long zsplit_w(const int (&g)[N], int cB, int cA) {
+    constexpr int BV = Z > 12 ? Z : 12;            // B = [12, N-6): constant [12, min(Z, N-6)), varying after
+    constexpr int AV = Z > N - 6 ? Z : N - 6;      // A = [N-6, N):  constant [N-6, max(Z, N-6)), varying after
+    const int vB = int_rowprod<N, (BV < N - 6 ? BV : N - 6), N - 6>(g, cB);
+    const int vA = int_rowprod<N, AV, N>(g, cA);
+    return mul_wide(vA, vB);
+}
+
+template <int N, int Z, int U, int T>
+struct IntInnerZ {
+    static __device__ __forceinline__ void run(uint32_t sc, int (&g)[N], int zmid, ZLimbs& L) {
+        constexpr int NP = I01Cfg<N>::NP;
+        if constexpr (T > 0) {                       // flip of Gray bit J >= 1 (all rows)
+            constexpr int J = ctz_c((unsigned)T);
+            if constexpr (J == U - 1) {
+                if constexpr (kZNeg) int_flip_static<N, true>(sc + (zmid < 0 ? kZNegOff<N> : 0u) + 4u * (uint32_t)(J * NP), g);
+                else int_flip<N>(sc + 4u * (uint32_t)(J * NP), zmid, g);
+            } else {
+                constexpr bool PLUS = ((T >> (J + 1)) & 1) == 0;
+                int_flip_static<N, PLUS>(sc + 4u * (uint32_t)(J * NP), g);
+            }
+        }
+        constexpr int CB = Z < N - 6 ? Z : N - 6;   // constant rows of group B: [12, CB); of group A: [N-6, Z)
+        const int cB = int_rowprod<N, 12, CB>(g, 1);
+        const int cA = int_rowprod<N, N - 6, (Z > N - 6 ? Z : N - 6)>(g, 1);
+        const long long u = mul_wide(int_rowprod<N, 0, 6>(g, 1), int_rowprod<N, 6, 12>(g, 1));
+        const long long w0 = zsplit_w<N, Z>(g, cB, cA);         // term T (sign -)
+        int_flip_rows<N, Z, ((T >> 1) & 1) == 0>(sc, g);         // bit 0 -> term T + 1 (sign +)
+        const long long w1 = zsplit_w<N, Z>(g, cB, cA);
+        const long long F = w1 - w0;
+        const int u0 = (int)((unsigned)u & 0x0FFFFFFFu), u1 = (int)(u >> 28);
+        const int f0 = (int)((unsigned)F & 0x0FFFFFFFu), f1 = (int)(F >> 28);
+        mad_wide(L.s0, u0, f0);
+        mad_wide(L.s1, u0, f1);
+        mad_wide(L.s1, u1, f0);
+        mad_wide(L.s2, u1, f1);
+        if constexpr (T + 2 < (1 << U)) IntInnerZ<N, Z, U, T + 2>::run(sc, g, zmid, L);
+    }
+};
+
+__device__ __forceinline__ void zlimb_fold(ZLimbs& L, u128& acc) {
+    acc += (u128)(__int128)L.s0 + ((u128)(__int128)L.s1 << 28) + ((u128)(__int128)L.s2 << 56);
+    L = ZLimbs{0, 0, 0};
+}
+
+// 29 <= n <= 33 (full-range Ryser of Eq. (3), 0-1 entries: row sums r_i in [0, n], products mod 2^128): the same pair
+// factoring, pair = C (W' - W) mod 2^128 with C = prod_{i<Z} r_i (int32 groups of 6 rows, 33^6 < 2^31; u64 pairs of
+// groups, 33^12 < 2^61; then mod 2^128) once per pair and W = prod_{i>=Z} r_i per term -- an exact u64 when the
+// M = n - Z varying rows number <= 12 (then D = W' - W is an int64), else mod 2^128.
+__device__ __forceinline__ u128 mul_u128_u64(u128 a, unsigned long long y) {
+    const unsigned long long lo = (unsigned long long)a, hi = (unsigned long long)(a >> 64);
+    return ((u128)(hi * y + __umul64hi(lo, y)) << 64) | (u128)(lo * y);
+}
+
+template <int N, int LO, int HI>
+__device__ __forceinline__ unsigned long long rows_u64(const int (&g)[N]) {    // exact: HI - LO <= 12 rows
+    static_assert(HI - LO <= 12 && HI - LO >= 1, "u64 row product: at most 12 rows");
+    constexpr int MID = (HI - LO) > 6 ? LO + 6 : HI;
+    const unsigned a = (unsigned)int_rowprod<N, LO + 1, MID>(g, g[LO]);
+    if constexpr (MID == HI) return (unsigned long long)a;
+    else return (unsigned long long)a * (unsigned)int_rowprod<N, MID + 1, HI>(g, g[MID]);
+}
+
+template <int N, int LO, int HI>
+__device__ __forceinline__ u128 rows_u128(const int (&g)[N]) {                 // mod 2^128
+    if constexpr (HI - LO <= 12) {
+        return (u128)rows_u64<N, LO, HI>(g);
+    } else {
+        constexpr int MID = HI - 12 < LO + 12 ? HI - 12 : LO + 12;
+        const unsigned long long hi12 = rows_u64<N, MID, HI>(g);
+        if constexpr (MID - LO <= 12) {
+            const unsigned long long a = rows_u64<N, LO, MID>(g);
+            return ((u128)__umul64hi(a, hi12) << 64) | (u128)(a * hi12);
+        } else {
+            return mul_u128_u64(rows_u128<N, LO, MID>(g), hi12);
+        }
+    }
+}
+
+template <int N, int Z, int U, int T>
+struct IntInnerZF {
+    static __device__ __forceinline__ void run(uint32_t sc, int (&g)[N], int zmid, u128& acc) {
+        constexpr int NP = I01Cfg<N>::NP;
+        if constexpr (T > 0) {
+            constexpr int J = ctz_c((unsigned)T);
+            if constexpr (J == U - 1) {
+                if constexpr (kZNeg) int_flip_static<N, true>(sc + (zmid < 0 ? kZNegOff<N> : 0u) + 4u * (uint32_t)(J * NP), g);
+                else int_flip<N>(sc + 4u * (uint32_t)(J * NP), zmid, g);
+            } else {
+                constexpr bool PLUS = ((T >> (J + 1)) & 1) == 0;
+                int_flip_static<N, PLUS>(sc + 4u * (uint32_t)(J * NP), g);
+            }
+        }
+        const u128 C = rows_u128<N, 0, Z>(g);
+        if constexpr (N - Z <= 12) {
+            const unsigned long long w0 = rows_u64<N, Z, N>(g);
+            int_flip_rows<N, Z, ((T >> 1) & 1) == 0>(sc, g);
+            const unsigned long long w1 = rows_u64<N, Z, N>(g);
+            const long long D = (long long)(w1 - w0);                 // |D| < 2^61
+            const unsigned long long clo = (unsigned long long)C, chi = (unsigned long long)(C >> 64);
+            const unsigned long long du = (unsigned long long)D;
+            unsigned long long hi = __umul64hi(clo, du) + chi * du;
+            if (D < 0) hi -= clo;                                     // C * (du - 2^64) mod 2^128
+            acc += ((u128)hi << 64) | (u128)(clo * du);
+        } else {
+            const u128 w0 = rows_u128<N, Z, N>(g);
+            int_flip_rows<N, Z, ((T >> 1) & 1) == 0>(sc, g);
+            const u128 w1 = rows_u128<N, Z, N>(g);
+            acc += C * (w1 - w0);
+        }
+        if constexpr (T + 2 < (1 << U)) IntInnerZF<N, Z, U, T + 2>::run(sc, g, zmid, acc);
+    }
+};
+
 template <int N, int U, int T>
 struct IntInner {
     template <class Acc>
@@ -190,7 +393,8 @@ struct IntInner {
             constexpr int J = ctz_c((unsigned)T);
             constexpr int NP = I01Cfg<N>::NP;
             if constexpr (J == U - 1) {
-                int_flip<N>(sc + 4u * (uint32_t)(J * NP), zmid, g);
+                if constexpr (kPNeg >= 1) int_flip_static<N, true>(sc + (zmid < 0 ? kZNegOff<N> : 0u) + 4u * (uint32_t)(J * NP), g);
+                else int_flip<N>(sc + 4u * (uint32_t)(J * NP), zmid, g);
             } else {
                 constexpr bool PLUS = ((T >> (J + 1)) & 1) == 0;
                 int_flip_static<N, PLUS>(sc + 4u * (uint32_t)(J * NP), g);
@@ -231,7 +435,8 @@ __device__ __forceinline__ void int_chunk(uint32_t sc, uint32_t sbase, uint64_t 
             if (q > 0) {
                 const int j = U + __ffsll((long long)q) - 1;
                 const uint64_t nb = (j + 1 < e) ? ((q >> (j + 1 - U)) & 1ull) : cpar;
-                int_flip<N>(sc + 4u * (uint32_t)(j * I01Cfg<N>::NP), nb ? -1 : 1, g);
+                if constexpr (kPNeg >= 2) int_flip_static<N, true>(sc + (nb ? kZNegOff<N> : 0u) + 4u * (uint32_t)(j * I01Cfg<N>::NP), g);
+                else int_flip<N>(sc + 4u * (uint32_t)(j * I01Cfg<N>::NP), nb ? -1 : 1, g);
             }
             const uint64_t nbm = (U < e) ? (q & 1ull) : cpar;
             if constexpr (kLimb<N>) {
@@ -245,27 +450,73 @@ __device__ __forceinline__ void int_chunk(uint32_t sc, uint32_t sbase, uint64_t 
     }
 }
 
+template <int N, int Z>
+__device__ __forceinline__ void int_chunk_z(uint32_t sc, uint32_t sbase, uint64_t c, int e, u128& acc) {
+    constexpr int U = kZU;
+    constexpr uint64_t kFoldBlocks = (uint64_t)kZFoldPairs >> (U - 1);
+    static_assert(U >= 2 && kFoldBlocks >= 1, "pair-factored walk: U >= 2");
+    int g[N];
+    const uint64_t x = ((c ^ (c >> 1)) << e) | ((c & 1ull) << (e - 1));
+    int_seed<N>(sc, sbase, x, e - 1, g);
+    const uint64_t nblk = 1ull << (e - U);
+    const uint64_t cpar = c & 1ull;
+    [[maybe_unused]] ZLimbs L{0, 0, 0};
+    for (uint64_t q = 0; q < nblk; q++) {
+        if (q > 0) {
+            const int j = U + __ffsll((long long)q) - 1;
+            const uint64_t nb = (j + 1 < e) ? ((q >> (j + 1 - U)) & 1ull) : cpar;
+            if constexpr (kZNeg) int_flip_static<N, true>(sc + (nb ? kZNegOff<N> : 0u) + 4u * (uint32_t)(j * I01Cfg<N>::NP), g);
+            else int_flip<N>(sc + 4u * (uint32_t)(j * I01Cfg<N>::NP), nb ? -1 : 1, g);
+        }
+        const uint64_t nbm = (U < e) ? (q & 1ull) : cpar;
+        if constexpr (I01Cfg<N>::FULL) {
+            IntInnerZF<N, Z, U, 0>::run(sc, g, nbm ? -1 : 1, acc);
+        } else {
+            IntInnerZ<N, Z, U, 0>::run(sc, g, nbm ? -1 : 1, L);
+            if ((q & (kFoldBlocks - 1)) == kFoldBlocks - 1 || q + 1 == nblk) zlimb_fold(L, acc);
+        }
+    }
+}
+
+// the chunks [c0, c0 + chunks) of this thread's stride, plain walk (Z = 0) or pair-factored (Z >= 12)
+template <int N, int Z>
+__device__ __forceinline__ void int_walk(uint32_t sc, uint32_t sbase, int e, uint64_t chunks, uint64_t c0, u128& acc) {
+    const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; c < chunks; c += T) {
+        if constexpr (Z > 0) {
+            if (e >= kZU) { int_chunk_z<N, Z>(sc, sbase, c0 + c, e, acc); continue; }
+        }
+        int_chunk<N>(sc, sbase, c0 + c, e, acc);       // chunk c0 + c: ranks [(c0+c) 2^e, (c0+c+1) 2^e)
+    }
+}
+
 // ws layout: [int flag][pad to 16][u128 partials[B][nblk]]
 // PM1 = false: entries are bytes 0/1 (perm_int01); PM1 = true: signed bytes in {-1, 0, 1} (perm_pm1, the
 // Bernoulli +-1 ensemble of Sec. V).  Either way |g_i| <= n, so the product and exactness bounds hold.
 template <int N, bool PM1>
-__global__ void __launch_bounds__(I01Cfg<N>::NT) int01_kernel(const uint8_t* __restrict__ A, int e,
+__global__ void __launch_bounds__(I01Cfg<N>::NT, kInt01MinBlocks) int01_kernel(const uint8_t* __restrict__ A, int e,
                                                               uint64_t chunks, u128* __restrict__ partials,
-                                                              int* __restrict__ flag, uint64_t c0, int accum) {
+                                                              int* __restrict__ flag, uint64_t c0, int accum,
+                                                              int zsplit) {
     constexpr int NP = I01Cfg<N>::NP;
     constexpr bool FULL = I01Cfg<N>::FULL;
     constexpr int CM = FULL ? 1 : 2;               // column increment: 2 a_ij (Glynn) or a_ij (Ryser)
-    __shared__ __align__(16) int s_col[N * NP];   // s_col[j*NP + i] = CM a_ij (rows N..NP-1 zero)
-    __shared__ int s_base[N];                     // Glynn: a_{i,n} - sum_{j<n} a_ij; Ryser: 0
+    constexpr bool ZS = (kZSplit<N> && !FULL) || (kZSplitFull<N> && !PM1);
+    // s_col[j*NP + i] = CM a_ij (rows N..NP-1 zero), then its negation (flips whose sign is known only at run time
+    // read -CM a by address); the pair-factored walk's permuted copy and its negation follow
+    __shared__ __align__(16) int s_col[(ZS ? 4 : 2) * N * NP];
+    __shared__ int s_base[(ZS ? 2 : 1) * N];      // Glynn: a_{i,n} - sum_{j<n} a_ij; Ryser: 0
     const int64_t m = blockIdx.y;
     const uint8_t* a = A + m * (N * N);
-    for (int k = threadIdx.x; k < N * NP; k += blockDim.x) s_col[k] = 0;
+    for (int k = threadIdx.x; k < 2 * N * NP; k += blockDim.x) s_col[k] = 0;
     __syncthreads();
     for (int k = threadIdx.x; k < N * N; k += blockDim.x) {
         const int v = PM1 ? (int)(int8_t)a[k] : (int)a[k];
         if (PM1 ? (v < -1 || v > 1) : (v > 1)) atomicOr(flag, 1);
         const int i = k / N, j = k - i * N;
-        s_col[j * NP + i] = PM1 ? CM * (v < -1 ? -1 : (v > 1 ? 1 : v)) : CM * (v & 1);
+        const int cv = PM1 ? CM * (v < -1 ? -1 : (v > 1 ? 1 : v)) : CM * (v & 1);
+        s_col[j * NP + i] = cv;
+        s_col[N * NP + j * NP + i] = -cv;
     }
     __syncthreads();
     for (int i = threadIdx.x; i < N; i += blockDim.x) {
@@ -274,12 +525,68 @@ __global__ void __launch_bounds__(I01Cfg<N>::NT) int01_kernel(const uint8_t* __r
         s_base[i] = FULL ? 0 : s_col[(N - 1) * NP + i] / 2 - s / 2;
     }
     __syncthreads();
-    const uint32_t sc = (uint32_t)__cvta_generic_to_shared(s_col);
-    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(s_base);
+    uint32_t sc = (uint32_t)__cvta_generic_to_shared(s_col);
+    uint32_t sbase = (uint32_t)__cvta_generic_to_shared(s_base);
     u128 acc = 0;
-    const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; c < chunks; c += T)
-        int_chunk<N>(sc, sbase, c0 + c, e, acc);       // chunk c0 + c: ranks [(c0+c) 2^e, (c0+c+1) 2^e)
+    int zsel = 0;
+    if constexpr (ZS) {
+        // plan of the pair-factored walk (block-uniform): the Gray column js with the most zero entries (lowest index
+        // on ties) goes to position 0, its zero rows first (stable order)
+        __shared__ int s_plan[2 + N];                 // [zsel, js, row order]
+        if (zsplit && threadIdx.x < 32) {
+            const int lane = threadIdx.x;
+            int cnt = -1;
+            if (lane < N - 1) {
+                cnt = 0;
+                for (int i = 0; i < N; i++) cnt += s_col[lane * NP + i] == 0;
+            }
+            int best = cnt, bj = lane;
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                const int ob = __shfl_xor_sync(0xffffffffu, best, off), oj = __shfl_xor_sync(0xffffffffu, bj, off);
+                if (ob > best || (ob == best && oj < bj)) { best = ob; bj = oj; }
+            }
+            if (lane == 0) {
+                s_plan[0] = FULL ? zsplit_menu_full(best, N) : zsplit_menu(best, N);
+                s_plan[1] = bj;
+                int r = 0;
+                for (int i = 0; i < N; i++) if (s_col[bj * NP + i] == 0) s_plan[2 + r++] = i;
+                for (int i = 0; i < N; i++) if (s_col[bj * NP + i] != 0) s_plan[2 + r++] = i;
+            }
+        }
+        __syncthreads();
+        zsel = zsplit ? s_plan[0] : 0;
+        if (zsel) {
+            const int js = s_plan[1];
+            for (int k = threadIdx.x; k < N * NP; k += blockDim.x) {
+                const int jj = k / NP, r = k - jj * NP;
+                const int src = jj == 0 ? js : (jj == js ? 0 : jj);
+                const int v = r < N ? s_col[src * NP + s_plan[2 + r]] : 0;
+                s_col[2 * N * NP + k] = v;
+                s_col[3 * N * NP + k] = -v;
+            }
+            for (int r = threadIdx.x; r < N; r += blockDim.x) s_base[N + r] = s_base[s_plan[2 + r]];
+            __syncthreads();
+            sc += 8u * (uint32_t)(N * NP);
+            sbase += 4u * (uint32_t)N;
+        }
+    }
+    if constexpr (ZS && FULL) {
+        if (zsel == N - 12)      int_walk<N, N - 12>(sc, sbase, e, chunks, c0, acc);
+        else if (zsel == N - 15) int_walk<N, N - 15>(sc, sbase, e, chunks, c0, acc);
+        else if (zsel == N - 18) int_walk<N, N - 18>(sc, sbase, e, chunks, c0, acc);
+        else                     int_walk<N, 0>(sc, sbase, e, chunks, c0, acc);
+    } else if constexpr (ZS) {
+        switch (zsel) {
+            case 18: int_walk<N, 18>(sc, sbase, e, chunks, c0, acc); break;
+            case 16: int_walk<N, 16>(sc, sbase, e, chunks, c0, acc); break;
+            case 14: int_walk<N, 14>(sc, sbase, e, chunks, c0, acc); break;
+            case 12: int_walk<N, 12>(sc, sbase, e, chunks, c0, acc); break;
+            default: int_walk<N, 0>(sc, sbase, e, chunks, c0, acc); break;
+        }
+    } else {
+        int_walk<N, 0>(sc, sbase, e, chunks, c0, acc);
+    }
     // block reduction (exact; order irrelevant)
     unsigned long long lo = (unsigned long long)acc, hi = (unsigned long long)(acc >> 64);
 #pragma unroll
@@ -320,6 +627,12 @@ __global__ void int01_final_kernel(const u128* __restrict__ partials, int nblk, 
     out[2 * m] = (unsigned long long)v;
     out[2 * m + 1] = (unsigned long long)((u128)v >> 64);
 }
+
+// PERM_INT01_ZSPLIT=0 (environment, read once) turns the pair-factored walk off (development comparisons)
+static const int kInt01ZSplit = [] {
+    const char* v = getenv("PERM_INT01_ZSPLIT");
+    return (v && v[0] == '0') ? 0 : 1;
+}();
 
 struct I01Plan {
     int e;
@@ -393,8 +706,8 @@ template <int N>
 cudaError_t int01_launch_t(const uint8_t* A, int64_t B, const I01Plan& p, u128* partials, int* flag, bool pm1,
                            cudaStream_t s) {
     dim3 grid((unsigned)p.nblk, (unsigned)B);
-    if (pm1) int01_kernel<N, true><<<grid, I01Cfg<N>::NT, 0, s>>>(A, p.e, p.chunks, partials, flag, 0, 0);
-    else     int01_kernel<N, false><<<grid, I01Cfg<N>::NT, 0, s>>>(A, p.e, p.chunks, partials, flag, 0, 0);
+    if (pm1) int01_kernel<N, true><<<grid, I01Cfg<N>::NT, 0, s>>>(A, p.e, p.chunks, partials, flag, 0, 0, kInt01ZSplit);
+    else     int01_kernel<N, false><<<grid, I01Cfg<N>::NT, 0, s>>>(A, p.e, p.chunks, partials, flag, 0, 0, kInt01ZSplit);
     return cudaGetLastError();
 }
 
@@ -448,7 +761,7 @@ __global__ void int01_range_final_kernel(const u128* __restrict__ partials, int 
 template <int N>
 cudaError_t int01_range_seg(const uint8_t* A, int e, uint64_t c0, uint64_t count, int nblk, u128* partials, int* flag,
                             int accum, cudaStream_t s) {
-    int01_kernel<N, false><<<dim3((unsigned)nblk, 1), I01Cfg<N>::NT, 0, s>>>(A, e, count, partials, flag, c0, accum);
+    int01_kernel<N, false><<<dim3((unsigned)nblk, 1), I01Cfg<N>::NT, 0, s>>>(A, e, count, partials, flag, c0, accum, kInt01ZSplit);
     return cudaGetLastError();
 }
 

@@ -63,6 +63,25 @@ def bernoulli01(shape, seed: int) -> np.ndarray:
     return np.ascontiguousarray(rng.integers(0, 2, size=shape, dtype=np.uint8))
 
 
+def zero_column01(n: int, z: int, seed: int, p_one: float = 0.7, col: int | None = None) -> np.ndarray:
+    """An n x n 0-1 matrix (Bernoulli(p_one) entries) whose column `col` (default: a seeded choice among the
+    first n-1) holds exactly z zeros and every other column fewer than z -- test inputs that fix the largest
+    zero count of a column (the int01 pair-factored walk's plan)."""
+    rng = np.random.default_rng(seed)
+    A = (rng.random((n, n)) < p_one).astype(np.uint8)
+    if col is None:
+        col = int(rng.integers(0, max(1, n - 1)))
+    A[:, col] = 1
+    A[rng.choice(n, z, replace=False), col] = 0
+    for j in range(n):
+        if j == col:
+            continue
+        zr = np.flatnonzero(A[:, j] == 0)
+        if len(zr) >= z:
+            A[rng.choice(zr, len(zr) - z + 1, replace=False), j] = 1
+    return np.ascontiguousarray(A)
+
+
 # ---------------------------------------------------------------- the 5 configs
 
 def cfg1() -> np.ndarray:

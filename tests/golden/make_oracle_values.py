@@ -4,7 +4,7 @@ the seeded input generators).  Usage:
 
     python tests/golden/make_oracle_values.py [section ...]
 
-Sections: cfg1 cfg3 blockdiag44 ranges44 ranges32 chunks44 chunks32 cfg2 cfg4 (cfg4 takes ~1 h on 8 cores).
+Sections: int01_full cfg1 cfg3 blockdiag44 ranges44 ranges32 chunks44 chunks32 cfg2 cfg4 (cfg4 takes ~1 h on 8 cores).
 Each section is merged into the JSON file as it finishes, with the oracle
 function used and its wall time.
 """
@@ -159,7 +159,22 @@ def sec_cfg4():
             "seconds": time.time() - t, "threads": oracle.num_threads()}
 
 
-SECTIONS = {"cfg1": sec_cfg1, "cfg3": sec_cfg3, "blockdiag44": sec_blockdiag44, "ranges44": sec_ranges44,
+# 0-1 matrices of the full-range int01 orders with a fixed largest column zero count z (inputs.zero_column01):
+# (n, z, seed) -- z picks the pair-factored walk's menu entry (n - 12 / n - 15 / n - 18 varying rows)
+INT01_FULL = [(29, 15, 2915), (29, 12, 2912), (31, 19, 3119)]
+
+
+def sec_int01_full():
+    out = []
+    for n, z, seed in INT01_FULL:
+        A = inputs.zero_column01(n, z, seed)
+        t = time.time()
+        v = oracle.ryser_i01_batch(A[None])[0]
+        out.append({"n": n, "z": z, "seed": seed, "sha256": sha(A), "value": str(v), "seconds": time.time() - t})
+    return {"fn": "oracle.ryser_i01_batch (Eq. 3, int128)", "cases": out}
+
+
+SECTIONS = {"int01_full": sec_int01_full, "cfg1": sec_cfg1, "cfg3": sec_cfg3, "blockdiag44": sec_blockdiag44, "ranges44": sec_ranges44,
             "ranges32": sec_ranges32, "chunks44": sec_chunks44, "chunks32": sec_chunks32, "cfg2": sec_cfg2,
             "cfg4": sec_cfg4}
 

@@ -1,6 +1,7 @@
 """GPU parity of perm_int01 (BASELINE config 3): bit-exact against the CPU oracle."""
 from __future__ import annotations
 
+import hashlib
 import json
 import math
 import os
@@ -112,3 +113,43 @@ def test_int01_range_closed_forms_and_errors(torch):
     with pytest.raises(pb.PermError) as e:
         pb.perm_int01_range(J, 0, N + 1)
     assert e.value.name == "PERM_E_ORDER"
+
+
+# ---- the pair-factored walk: matrices whose largest column zero count z selects each menu entry
+# (Glynn orders 20..24: Z = 18/16/14/12, below 12 the plain walk; full-range orders: n - 12 / n - 15 / n - 18)
+
+@pytest.mark.parametrize("n,z", [(20, 18), (20, 19), (21, 16), (22, 14), (22, 15), (23, 12), (24, 13), (24, 11),
+                                 (24, 17), (20, 20), (24, 24)])
+def test_pair_factored_menu_vs_oracle(torch, n, z):
+    A = np.stack([inputs.zero_column01(n, z, 5000 + 37 * n + z + k, col=k * (n - 2) // 2) for k in range(3)])
+    assert _run(torch, A) == oracle.ryser_i01_batch(A)
+
+
+@pytest.mark.parametrize("n", [20, 24])
+def test_pair_factored_pm1_with_zeros(torch, n):
+    # signed entries {-1, 0, 1}: the same plan (zero counts) on perm_pm1
+    rng = np.random.default_rng(77 + n)
+    P = rng.integers(-1, 2, size=(2, n, n)).astype(np.int8)
+    P[0, rng.choice(n, 15, replace=False), 3] = 0
+    got = pb.perm_pm1(torch.from_numpy(P).cuda())
+    assert got == [oracle.ryser_i8(P[b]) for b in range(2)]
+
+
+def test_pair_factored_full_range_goldens(torch, golden_dir):
+    # 29 <= n <= 33 pair-factored walk at each menu entry, against oracle values written by make_oracle_values.py
+    g = json.load(open(os.path.join(golden_dir, "oracle_values.json")))["int01_full"]
+    for c in g["cases"]:
+        A = inputs.zero_column01(c["n"], c["z"], c["seed"])
+        assert hashlib.sha256(A.tobytes()).hexdigest() == c["sha256"], "generator changed: regenerate the golden"
+        assert _run(torch, A[None]) == [int(c["value"])], c
+
+
+def test_pair_factored_range_partition(torch):
+    # perm_int01_range walks the same planned matrix: disjoint spans still finalize to per(A)
+    from paper_1904_06229_b200 import shard
+    A = inputs.zero_column01(22, 16, 2216)
+    ref = oracle.ryser_i01_batch(A[None])[0]
+    Ad = torch.from_numpy(A).cuda()
+    N = shard.int01_rank_space(22)
+    cuts = [0, 5, 1 << 10, (N // 3) | 1, N - 17, N]
+    assert pb.perm_int01_finalize([pb.perm_int01_range(Ad, cuts[i], cuts[i + 1]) for i in range(5)], 22) == ref
