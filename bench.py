@@ -92,7 +92,7 @@ class ClockSampler:
     REASON_BITS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20,
                    "hw_thermal_slowdown": 0x40}
 
-    def __init__(self, gpu_index: int, period_s: float = 0.002):
+    def __init__(self, gpu_index: int, period_s: float = float(os.environ.get("PERM_BENCH_CLOCK_MS", "2")) * 1e-3):
         self.gpu = gpu_index
         self.period = period_s
         self.proc = None
@@ -963,15 +963,19 @@ def run_ours(args):
             n3 = 33 if cfg == "cfg3s" else 24
             ops = (units_per_step / world * 2 * n3 if cfg == "cfg3s"
                    else units_per_step / world * (1 << (n3 - 1)) * 2 * n3)
-            kname = {"cfgpm": "int01_kernel<24, pm1> (INT fma + alu pipes)",
-                     "cfg3s": "int01_kernel<33> (Eq. (3) branch, INT fma + alu pipes)"}.get(cfg, "int01_kernel<24> (INT fma + alu pipes)")
+            kname = {"cfgpm": "int01_kernel<24, pm1> (plain walk: no zero entries; INT fma + alu pipes)",
+                     "cfg3s": "int01_kernel<33> (Eq. (3) branch, pair-factored walk; INT fma + alu pipes)"}.get(
+                         cfg, "int01_kernel<24> (pair-factored walk; INT fma + alu pipes)")
             achieved = ops / (dev_ms / K * 1e-3) / 1e12
             ipeak = int_nominal_tops()
             out["roofline"] = {"bound": "alu", "achieved": achieved, "peak": ipeak, "unit": "Tops/s",
                                "frac": achieved / ipeak, "traffic": ncu_traffic(cfg),
                                "kernel": kname,
                                "algorithmic": ("2n integer ops per Gray term x 2^n terms / ranks" if cfg == "cfg3s" else
-                                               "2n integer ops per Gray term x 2^(n-1) terms x matrices"),
+                                               "2n integer ops per Gray term x 2^(n-1) terms x matrices") +
+                                              ("" if cfg == "cfgpm" else
+                                               " (the plain walk's count: the pair-factored walk needs fewer "
+                                               "operations per term, so frac is an effective rate; DESIGN.md 5.3)"),
                                "peak_note": "derived: 148 SMs x 128 int lanes/clk (issue-bound) x 1965 MHz"}
     out["e2e"] = {"value": e2e_val, "unit": unit, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
     if cfg == "cfg3s":
