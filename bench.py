@@ -815,10 +815,12 @@ def run_ours(args):
         h2d, d2h = hostC.numel() * 16 + hostM.numel() * 4, abs2_h.numel() * 8
         terms_w = float(np.sum(np.prod(M_np[b0:b1].astype(np.float64) + 1.0, axis=1)))
         walk_launches_per_step = 1
+        nlaunch = [2]
 
         def step():
             e0.record(stream)
             pb.perm_c128_weighted_batched(devC, devM, per=per_d, abs2=abs2_d, stream=stream)
+            nlaunch[0] = pb.last_launches()                    # order kernel + weighted kernel
             e1.record(stream)
             torch.cuda.synchronize()
             es = torch.cuda.Event(enable_timing=True)
@@ -980,6 +982,8 @@ def run_ours(args):
     out["e2e"] = {"value": e2e_val, "unit": unit, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
     if cfg == "cfg3s":
         gpu_launches_per_step = nlaunch[0]             # range pieces + the summing kernel (library count)
+    if cfg == "cfgw":
+        gpu_launches_per_step = 2 * nlaunch[0]         # device-timed + e2e calls, library count each
     if cfg in ("cfg5", "cfg4", "cfg1"):
         gpu_launches_per_step = launch_count[0] / K
     out["gpu_launches"] = int(round(gpu_launches_per_step * K))

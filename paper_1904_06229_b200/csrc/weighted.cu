@@ -27,6 +27,12 @@
 
 namespace perm {
 
+// largest-first work order (wgt_order_kernel); 0: input order
+#ifndef PERM_WGT_ORDERED
+#define PERM_WGT_ORDERED 1
+#endif
+constexpr bool kWgtOrdered = PERM_WGT_ORDERED != 0;
+
 // unroll factor of the sweep loop (1: rolled)
 #ifndef PERM_WGT_UNROLL
 #define PERM_WGT_UNROLL 1
@@ -100,10 +106,44 @@ __device__ __forceinline__ void wgt_sweep(int ms, double sc2, const double* tsw,
     }
 }
 
+// Work order of the persistent queue: problems largest first (longest-processing-time rule), so that the big
+// patterns start early instead of running alone at the end (problem sizes prod_k (m_k + 1) vary ~10x; ncu of the
+// input-order queue: SMs active 82% of the launch).  One block counting-sorts the problems by floor(log2 |Omega|)
+// into `order` (descending bucket; the order inside a bucket is whatever the atomics give -- scheduling only: every
+// problem's result is computed by one warp from its own data, so the outputs do not depend on it).
+constexpr int kWgtBuckets = 64;
+__global__ void __launch_bounds__(1024) wgt_order_kernel(const int32_t* __restrict__ mult, int R, int64_t B,
+                                                         int64_t* __restrict__ order) {
+    __shared__ unsigned long long cnt[kWgtBuckets];
+    __shared__ unsigned long long pos[kWgtBuckets];
+    if (threadIdx.x < kWgtBuckets) cnt[threadIdx.x] = 0;
+    __syncthreads();
+    auto bucket = [&](int64_t b) {
+        double sz = 1.0;
+        for (int k = 0; k < R; k++) {
+            const int m = mult[b * R + k];
+            sz *= (double)((m > 0 ? m : 0) + 1);
+        }
+        int e = 0;
+        frexp(sz, &e);                                    // sz in [2^{e-1}, 2^e)
+        e = e < 0 ? 0 : (e >= kWgtBuckets ? kWgtBuckets - 1 : e);
+        return kWgtBuckets - 1 - e;                       // largest first
+    };
+    for (int64_t b = threadIdx.x; b < B; b += blockDim.x) atomicAdd(&cnt[bucket(b)], 1ull);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long run = 0;
+        for (int k = 0; k < kWgtBuckets; k++) { pos[k] = run; run += cnt[k]; }
+    }
+    __syncthreads();
+    for (int64_t b = threadIdx.x; b < B; b += blockDim.x) order[atomicAdd(&pos[bucket(b)], 1ull)] = b;
+}
+
 template <int N>
 __global__ void __launch_bounds__(WgtCfg<N>::NT, WgtCfg<N>::MINB)
     weighted_kernel(const double2* __restrict__ C, const int32_t* __restrict__ mult, int R, int64_t B,
-                    double2* __restrict__ per, double* __restrict__ abs2, unsigned long long* __restrict__ next) {
+                    double2* __restrict__ per, double* __restrict__ abs2, unsigned long long* __restrict__ next,
+                    const int64_t* __restrict__ qorder) {
     extern __shared__ __align__(16) unsigned char wsm[];
     const int lane = threadIdx.x & 31;
     double2* col = (double2*)wsm;                                         // col[k*N + i] = cbar_i(k)
@@ -125,8 +165,9 @@ __global__ void __launch_bounds__(WgtCfg<N>::NT, WgtCfg<N>::MINB)
         __syncwarp();
         unsigned long long bq = 0;
         if (lane == 0) bq = atomicAdd(next, 1ull);
-        const int64_t b = (int64_t)__shfl_sync(0xffffffffu, bq, 0);
-        if (b >= B) break;
+        const int64_t qpos = (int64_t)__shfl_sync(0xffffffffu, bq, 0);
+        if (qpos >= B) break;
+        const int64_t b = qorder ? qorder[qpos] : qpos;
         const int32_t* mb = mult + b * (int64_t)R;
         int msum = 0, mbad = 0, s = 0, ms = -1;
         for (int k = 0; k < R; k++) {                                     // warp-uniform scan
@@ -275,7 +316,7 @@ __global__ void __launch_bounds__(WgtCfg<N>::NT, WgtCfg<N>::MINB)
 
 template <int N>
 cudaError_t weighted_launch_t(const double2* C, const int32_t* mult, int R, int64_t B, double2* per, double* abs2,
-                              cudaStream_t st) {
+                              cudaStream_t st, int* launches) {
     const size_t smem = wgt_slot_bytes(N, R);
     cudaError_t err = cudaFuncSetAttribute(weighted_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (err != cudaSuccess) return err;
@@ -287,14 +328,22 @@ cudaError_t weighted_launch_t(const double2* C, const int32_t* mult, int R, int6
     if (bps < 1) return cudaErrorInvalidConfiguration;       // R too large for shared memory
     const int64_t cap = (int64_t)sms * bps;
     const int64_t grid = B < cap ? B : cap;
-    unsigned long long* next = nullptr;                     // the work-queue counter, stream-ordered
-    err = malloc_async((void**)&next, sizeof(unsigned long long), st);
+    // the work-queue counter and (more than one resident wave of problems) the largest-first order, stream-ordered
+    const bool ordered = kWgtOrdered && B > grid;
+    unsigned long long* next = nullptr;
+    err = malloc_async((void**)&next, 16 + (ordered ? (size_t)B * sizeof(int64_t) : 0), st);
     if (err != cudaSuccess) return err;
+    int64_t* order = ordered ? (int64_t*)((char*)next + 16) : nullptr;
     err = cudaMemsetAsync(next, 0, sizeof(unsigned long long), st);
-    if (err == cudaSuccess) {
-        weighted_kernel<N><<<(unsigned)grid, WgtCfg<N>::NT, smem, st>>>(C, mult, R, B, per, abs2, next);
+    if (err == cudaSuccess && ordered) {
+        wgt_order_kernel<<<1, 1024, 0, st>>>(mult, R, B, order);
         err = cudaGetLastError();
     }
+    if (err == cudaSuccess) {
+        weighted_kernel<N><<<(unsigned)grid, WgtCfg<N>::NT, smem, st>>>(C, mult, R, B, per, abs2, next, order);
+        err = cudaGetLastError();
+    }
+    *launches = ordered ? 2 : 1;
     const cudaError_t e2 = cudaFreeAsync(next, st);
     return err != cudaSuccess ? err : e2;
 }
@@ -305,8 +354,7 @@ cudaError_t weighted_launch(const double2* C, const int32_t* mult, int n, int R,
                             double* abs2, cudaStream_t s, int* launches) {
     *launches = 0;
     if (B == 0) return cudaSuccess;
-    *launches = 1;
-#define PERM_CASE(N) case N: return weighted_launch_t<N>(C, mult, R, B, per, abs2, s);
+#define PERM_CASE(N) case N: return weighted_launch_t<N>(C, mult, R, B, per, abs2, s, launches);
     switch (n) { PERM_R8(PERM_CASE, 0) PERM_R8(PERM_CASE, 8) PERM_R8(PERM_CASE, 16) PERM_R8(PERM_CASE, 24)
                  default: return cudaErrorInvalidValue; }
 #undef PERM_CASE
