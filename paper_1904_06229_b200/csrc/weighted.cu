@@ -51,7 +51,7 @@ struct WgtCfg {
 #ifndef PERM_WGT_REG_EXTRA
     // working-set registers beyond the 4n row sums (0 spill bytes at every order, tools/spills.py, with the
     // unrolled sweeps of m_s <= kWgtSpecMax)
-    static constexpr int EXTRA = (N == 23 || N == 24) ? 160 : 128;
+    static constexpr int EXTRA = (N == 18 || N == 23 || N == 24) ? 160 : 128;
 #else
     static constexpr int EXTRA = PERM_WGT_REG_EXTRA;
 #endif
@@ -108,42 +108,57 @@ __device__ __forceinline__ void wgt_sweep(int ms, double sc2, const double* tsw,
 
 // Work order of the persistent queue: problems largest first (longest-processing-time rule), so that the big
 // patterns start early instead of running alone at the end (problem sizes prod_k (m_k + 1) vary ~10x; ncu of the
-// input-order queue: SMs active 82% of the launch).  One block counting-sorts the problems by floor(log2 |Omega|)
-// into `order` (descending bucket; the order inside a bucket is whatever the atomics give -- scheduling only: every
-// problem's result is computed by one warp from its own data, so the outputs do not depend on it).
-constexpr int kWgtBuckets = 64;
+// input-order queue: SMs active 82% of the launch).  One block counting-sorts the problems by floor(8 log2 |Omega|)
+// (eighth-octave classes) into `order` (descending class, index order inside a class) -- scheduling only: every
+// problem's result is computed by one warp from its own data, so the outputs do not depend on it.
+constexpr int kWgtBuckets = 256;                  // eighth-octave size classes, 2^0 .. 2^32
 __global__ void __launch_bounds__(1024) wgt_order_kernel(const int32_t* __restrict__ mult, int R, int64_t B,
                                                          int64_t* __restrict__ order) {
     __shared__ unsigned long long cnt[kWgtBuckets];
-    __shared__ unsigned long long pos[kWgtBuckets];
-    if (threadIdx.x < kWgtBuckets) cnt[threadIdx.x] = 0;
-    __syncthreads();
     auto bucket = [&](int64_t b) {
         double sz = 1.0;
         for (int k = 0; k < R; k++) {
             const int m = mult[b * R + k];
             sz *= (double)((m > 0 ? m : 0) + 1);
         }
-        int e = 0;
-        frexp(sz, &e);                                    // sz in [2^{e-1}, 2^e)
+        int e = (int)(8.0 * log2(sz));                   // floor(8 log2 |Omega|)
         e = e < 0 ? 0 : (e >= kWgtBuckets ? kWgtBuckets - 1 : e);
         return kWgtBuckets - 1 - e;                       // largest first
     };
+    for (int k = threadIdx.x; k < kWgtBuckets; k += blockDim.x) cnt[k] = 0;
+    __syncthreads();
     for (int64_t b = threadIdx.x; b < B; b += blockDim.x) atomicAdd(&cnt[bucket(b)], 1ull);
     __syncthreads();
     if (threadIdx.x == 0) {
         unsigned long long run = 0;
-        for (int k = 0; k < kWgtBuckets; k++) { pos[k] = run; run += cnt[k]; }
+        for (int k = 0; k < kWgtBuckets; k++) { const unsigned long long c = cnt[k]; cnt[k] = run; run += c; }
     }
     __syncthreads();
-    for (int64_t b = threadIdx.x; b < B; b += blockDim.x) order[atomicAdd(&pos[bucket(b)], 1ull)] = b;
+    // stable placement (index order inside a class, so the schedule is the same on every run): warp 0 walks the
+    // problems 32 at a time; lanes of one class take consecutive slots in lane order
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        for (int64_t b0 = 0; b0 < B; b0 += 32) {
+            const int64_t b = b0 + lane;
+            const int key = b < B ? bucket(b) : -1 - lane;
+            const unsigned peers = __match_any_sync(0xffffffffu, key);
+            const int before = __popc(peers & ((1u << lane) - 1u));
+            const int leader = __ffs(peers) - 1;
+            unsigned long long base = 0;
+            if (b < B && lane == leader) base = cnt[key];
+            base = __shfl_sync(0xffffffffu, base, leader);
+            if (b < B) order[base + before] = b;
+            __syncwarp();
+            if (b < B && lane == leader) cnt[key] = base + __popc(peers);
+            __syncwarp();
+        }
+    }
 }
 
 template <int N>
 __global__ void __launch_bounds__(WgtCfg<N>::NT, WgtCfg<N>::MINB)
     weighted_kernel(const double2* __restrict__ C, const int32_t* __restrict__ mult, int R, int64_t B,
-                    double2* __restrict__ per, double* __restrict__ abs2, unsigned long long* __restrict__ next,
-                    const int64_t* __restrict__ qorder) {
+                    double2* __restrict__ per, double* __restrict__ abs2, unsigned long long* __restrict__ next) {
     extern __shared__ __align__(16) unsigned char wsm[];
     const int lane = threadIdx.x & 31;
     double2* col = (double2*)wsm;                                         // col[k*N + i] = cbar_i(k)
@@ -164,10 +179,13 @@ __global__ void __launch_bounds__(WgtCfg<N>::NT, WgtCfg<N>::MINB)
     for (;;) {                                                            // persistent: a shared work queue
         __syncwarp();
         unsigned long long bq = 0;
-        if (lane == 0) bq = atomicAdd(next, 1ull);
-        const int64_t qpos = (int64_t)__shfl_sync(0xffffffffu, bq, 0);
-        if (qpos >= B) break;
-        const int64_t b = qorder ? qorder[qpos] : qpos;
+        if (lane == 0) {
+            bq = atomicAdd(next, 1ull);
+            // the queue position's problem: the largest-first order follows the counter (wgt_order_kernel)
+            if (kWgtOrdered && bq < (unsigned long long)B) bq = (unsigned long long)((const int64_t*)(next + 2))[bq];
+        }
+        const int64_t b = (int64_t)__shfl_sync(0xffffffffu, bq, 0);
+        if (b >= B) break;
         const int32_t* mb = mult + b * (int64_t)R;
         int msum = 0, mbad = 0, s = 0, ms = -1;
         for (int k = 0; k < R; k++) {                                     // warp-uniform scan
@@ -329,18 +347,18 @@ cudaError_t weighted_launch_t(const double2* C, const int32_t* mult, int R, int6
     const int64_t cap = (int64_t)sms * bps;
     const int64_t grid = B < cap ? B : cap;
     // the work-queue counter and (more than one resident wave of problems) the largest-first order, stream-ordered
-    const bool ordered = kWgtOrdered && B > grid;
+    const bool ordered = kWgtOrdered;
     unsigned long long* next = nullptr;
     err = malloc_async((void**)&next, 16 + (ordered ? (size_t)B * sizeof(int64_t) : 0), st);
     if (err != cudaSuccess) return err;
-    int64_t* order = ordered ? (int64_t*)((char*)next + 16) : nullptr;
+    int64_t* order = (int64_t*)((char*)next + 16);
     err = cudaMemsetAsync(next, 0, sizeof(unsigned long long), st);
     if (err == cudaSuccess && ordered) {
         wgt_order_kernel<<<1, 1024, 0, st>>>(mult, R, B, order);
         err = cudaGetLastError();
     }
     if (err == cudaSuccess) {
-        weighted_kernel<N><<<(unsigned)grid, WgtCfg<N>::NT, smem, st>>>(C, mult, R, B, per, abs2, next, order);
+        weighted_kernel<N><<<(unsigned)grid, WgtCfg<N>::NT, smem, st>>>(C, mult, R, B, per, abs2, next);
         err = cudaGetLastError();
     }
     *launches = ordered ? 2 : 1;
