@@ -450,6 +450,91 @@ __device__ __forceinline__ void int_chunk(uint32_t sc, uint32_t sbase, uint64_t 
     }
 }
 
+// ---- quad-factored walk (perm_pm1, 20 <= n <= 24, columns without zero entries) ------------------------------
+// The four ranks of an aligned quad 4t .. 4t+3 run through the four sign pairs (delta_0, delta_1) of Gray bits 0 and
+// 1 at fixed higher bits (App. A).  With the rows negated so that the bit-0 column is all +1 (per changes by the
+// product of the row signs) and the bit-1 column negated if that balances the classes below, every row reads
+// g_i = h_i + delta_0 + delta_1 a_i1 with h_i the part of the other columns: the rows with a_i1 = +1 (class P,
+// rows [0, Z)) take the values h + {2, 0, -2} as delta_0 + delta_1 = 2, 0, -2, the rows with a_i1 = -1 (class M)
+// as delta_0 - delta_1 does.  The term signs (-1)^{r+1} equal d delta_0 delta_1 over the quad with d = +1 iff
+// bit 2 of r is set, so the quad sums to
+//     d [ M(0) (P(2) + P(-2)) - P(0) (M(2) + M(-2)) ],   X(s) = prod_{i in X} (h_i + s),
+// six products over about n/2 rows instead of four over n, and two row adds instead of four flips per row.  The
+// walk carries h (Gray bits >= 2 only); |h_i + s| <= n, a class of <= 13 rows multiplies exactly in int64
+// (24^13 < 2^60), the two class products exactly in int128.
+template <int N, bool PM1>
+constexpr bool kQuad = PM1 && N >= 20 && N <= 24;
+constexpr int kQuadCode = 1000;                    // plan code kQuadCode + Z selects the quad walk with |P| = Z
+
+template <int N, int LO, int HI, int OFF>
+__device__ __forceinline__ long long quad_prod(const int (&h)[N]) {
+    static_assert(HI - LO >= 1 && HI - LO <= 13, "quad class: 1..13 rows");
+    constexpr int M1 = (HI - LO) > 6 ? LO + 6 : HI;
+    int p0 = h[LO] + OFF;
+#pragma unroll
+    for (int i = LO + 1; i < M1; i++) p0 *= h[i] + OFF;
+    if constexpr (M1 == HI) {
+        return (long long)p0;
+    } else {
+        constexpr int M2 = (HI - M1) > 6 ? M1 + 6 : HI;
+        int p1 = h[M1] + OFF;
+#pragma unroll
+        for (int i = M1 + 1; i < M2; i++) p1 *= h[i] + OFF;
+        const long long q = mul_wide(p0, p1);
+        if constexpr (M2 == HI) return q;
+        else return q * (long long)(h[M2] + OFF);          // the 13th row
+    }
+}
+
+template <int N, int Z, int U, int T>
+struct IntInnerQ {
+    static __device__ __forceinline__ void run(uint32_t sc, int (&h)[N], int zmid, u128& acc) {
+        constexpr int NP = I01Cfg<N>::NP;
+        static_assert(T % 4 == 0 && U >= 3, "quads of an aligned block of >= 8 ranks");
+        if constexpr (T > 0) {                       // flip of Gray bit J >= 2 (bits 0 and 1 live in the quad formula)
+            constexpr int J = ctz_c((unsigned)T);
+            if constexpr (J == U - 1) {
+                int_flip_static<N, true>(sc + (zmid < 0 ? kZNegOff<N> : 0u) + 4u * (uint32_t)(J * NP), h);
+            } else {
+                constexpr bool PLUS = ((T >> (J + 1)) & 1) == 0;
+                int_flip_static<N, PLUS>(sc + 4u * (uint32_t)(J * NP), h);
+            }
+        }
+        const long long P2 = quad_prod<N, 0, Z, 2>(h), P0 = quad_prod<N, 0, Z, 0>(h), Pm = quad_prod<N, 0, Z, -2>(h);
+        const long long M2 = quad_prod<N, Z, N, 2>(h), M0 = quad_prod<N, Z, N, 0>(h), Mm = quad_prod<N, Z, N, -2>(h);
+        const __int128 v = (__int128)M0 * (P2 + Pm) - (__int128)P0 * (M2 + Mm);
+        if constexpr (((T >> 2) & 1) != 0) acc += (u128)v; else acc -= (u128)v;
+        if constexpr (T + 4 < (1 << U)) IntInnerQ<N, Z, U, T + 4>::run(sc, h, zmid, acc);
+    }
+};
+
+// one aligned chunk of 2^e ranks (e >= kZU) on the quad walk; hbase = the rows' base without columns 0 and 1
+template <int N, int Z>
+__device__ __forceinline__ void int_chunk_q(uint32_t sc, uint32_t hbase, uint64_t c, int e, u128& acc) {
+    constexpr int U = kZU;
+    int h[N];
+    const uint64_t x = ((c ^ (c >> 1)) << e) | ((c & 1ull) << (e - 1));
+    int_seed<N>(sc, hbase, x, e - 1, h);              // e - 1 >= 2: columns 0 and 1 are not seeded
+    const uint64_t nblk = 1ull << (e - U);
+    const uint64_t cpar = c & 1ull;
+    for (uint64_t q = 0; q < nblk; q++) {
+        if (q > 0) {
+            const int j = U + __ffsll((long long)q) - 1;
+            const uint64_t nb = (j + 1 < e) ? ((q >> (j + 1 - U)) & 1ull) : cpar;
+            int_flip_static<N, true>(sc + (nb ? kZNegOff<N> : 0u) + 4u * (uint32_t)(j * I01Cfg<N>::NP), h);
+        }
+        const uint64_t nbm = (U < e) ? (q & 1ull) : cpar;
+        IntInnerQ<N, Z, U, 0>::run(sc, h, nbm ? -1 : 1, acc);
+    }
+}
+
+template <int N, int Z>
+__device__ __forceinline__ void int_walk_q(uint32_t sc, uint32_t hbase, int e, uint64_t chunks, uint64_t c0, u128& acc) {
+    const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; c < chunks; c += T)
+        int_chunk_q<N, Z>(sc, hbase, c0 + c, e, acc);    // the plan selects the quad walk only when e >= kZU
+}
+
 template <int N, int Z>
 __device__ __forceinline__ void int_chunk_z(uint32_t sc, uint32_t sbase, uint64_t c, int e, u128& acc) {
     constexpr int U = kZU;
@@ -529,10 +614,11 @@ __global__ void __launch_bounds__(I01Cfg<N>::NT, kInt01MinBlocks) int01_kernel(c
     uint32_t sbase = (uint32_t)__cvta_generic_to_shared(s_base);
     u128 acc = 0;
     int zsel = 0;
+    [[maybe_unused]] int qsign = 1;
     if constexpr (ZS) {
         // plan of the pair-factored walk (block-uniform): the Gray column js with the most zero entries (lowest index
         // on ties) goes to position 0, its zero rows first (stable order)
-        __shared__ int s_plan[2 + N];                 // [zsel, js, row order]
+        __shared__ int s_plan[5 + N];                 // [zsel, js, quad: c1, tau, sign, row order]
         if (zsplit && threadIdx.x < 32) {
             const int lane = threadIdx.x;
             int cnt = -1;
@@ -550,22 +636,105 @@ __global__ void __launch_bounds__(I01Cfg<N>::NT, kInt01MinBlocks) int01_kernel(c
                 s_plan[0] = FULL ? zsplit_menu_full(best, N) : zsplit_menu(best, N);
                 s_plan[1] = bj;
                 int r = 0;
-                for (int i = 0; i < N; i++) if (s_col[bj * NP + i] == 0) s_plan[2 + r++] = i;
-                for (int i = 0; i < N; i++) if (s_col[bj * NP + i] != 0) s_plan[2 + r++] = i;
+                for (int i = 0; i < N; i++) if (s_col[bj * NP + i] == 0) s_plan[5 + r++] = i;
+                for (int i = 0; i < N; i++) if (s_col[bj * NP + i] != 0) s_plan[5 + r++] = i;
+                if constexpr (kQuad<N, PM1>) {
+                    // no useful zeros: the quad plan -- bit-0 column c0 and bit-1 column c1 without zero entries,
+                    // class P (rows whose a_{i,c1} matches the sign of a_{i,c0}, times tau) of size N/2 - 1 or N/2
+                    if (s_plan[0] == 0 && e >= kZU) {
+                        int q0 = -1, q1 = -1, tau = 1, zq = 0;
+                        for (int j = 0; j < N - 1 && q0 < 0; j++) {
+                            bool nz = true;
+                            for (int i = 0; i < N; i++) nz = nz && s_col[j * NP + i] != 0;
+                            if (nz) q0 = j;
+                        }
+                        for (int j = 0; j < N - 1 && q0 >= 0 && q1 < 0; j++) {
+                            if (j == q0) continue;
+                            int z = 0;
+                            bool nz = true;
+                            for (int i = 0; i < N; i++) {
+                                const int v = s_col[j * NP + i];
+                                nz = nz && v != 0;
+                                z += (v > 0) == (s_col[q0 * NP + i] > 0);
+                            }
+                            if (!nz) continue;
+                            const int zz = z < N - z ? z : N - z;
+                            if (zz == N / 2 || zz == N / 2 - 1) { q1 = j; tau = (z == zz) ? 1 : -1; zq = zz; }
+                        }
+                        if (q1 >= 0) {
+                            int sgn = tau, r2 = 0;
+                            for (int i = 0; i < N; i++) {
+                                const int si = s_col[q0 * NP + i] > 0 ? 1 : -1;
+                                sgn *= si;
+                                if ((s_col[q1 * NP + i] > 0 ? 1 : -1) * si * tau > 0) s_plan[5 + r2++] = i;
+                            }
+                            for (int i = 0; i < N; i++) {
+                                const int si = s_col[q0 * NP + i] > 0 ? 1 : -1;
+                                if ((s_col[q1 * NP + i] > 0 ? 1 : -1) * si * tau < 0) s_plan[5 + r2++] = i;
+                            }
+                            s_plan[0] = kQuadCode + zq;
+                            s_plan[1] = q0;
+                            s_plan[2] = q1;
+                            s_plan[3] = tau;
+                            s_plan[4] = sgn;
+                        }
+                    }
+                }
             }
         }
         __syncthreads();
         zsel = zsplit ? s_plan[0] : 0;
-        if (zsel) {
+        if constexpr (kQuad<N, PM1>) {
+            if (zsel >= kQuadCode) {
+                qsign = s_plan[4];
+                // the quad plan's matrix A' = D_sigma A Q: columns c0, c1 first (c1 times tau), rows negated to
+                // make column c0 all +1, class P first; per(A) = sign * per(A')
+                const int q0 = s_plan[1], q1 = s_plan[2], tau = s_plan[3];
+                for (int k = threadIdx.x; k < N * NP; k += blockDim.x) {
+                    const int jj = k / NP, r = k - jj * NP;
+                    int src = jj;
+                    if (jj == 0) src = q0;
+                    else if (jj == 1) src = q1;
+                    else {                                    // the other columns in order, skipping q0 and q1
+                        int t = jj - 2;
+                        for (src = 0;; src++) {
+                            if (src == q0 || src == q1) continue;
+                            if (t-- == 0) break;
+                        }
+                    }
+                    int v = 0;
+                    if (r < N) {
+                        const int row = s_plan[5 + r];
+                        const int si = s_col[q0 * NP + row] > 0 ? 1 : -1;
+                        v = si * (jj == 1 ? tau : 1) * s_col[src * NP + row];
+                    }
+                    s_col[2 * N * NP + k] = v;
+                    s_col[3 * N * NP + k] = -v;
+                }
+                __syncthreads();
+                // h base of A' (Gray bits >= 2 only): g = base + sum_{x_j = 1} 2 a'_j minus delta_0 a'_0 + delta_1 a'_1,
+                // i.e. base' + a'_0 + a'_1 with a'_0 = +1 and a'_1 = +1 (class P) or -1 (class M)
+                for (int r = threadIdx.x; r < N; r += blockDim.x) {
+                    int t = 0;
+                    for (int j = 0; j < N - 1; j++) t += s_col[2 * N * NP + j * NP + r];
+                    s_base[N + r] = s_col[2 * N * NP + (N - 1) * NP + r] / 2 - t / 2 + 1 +
+                                    (s_col[2 * N * NP + NP + r] > 0 ? 1 : -1);
+                }
+                __syncthreads();
+                sc += 8u * (uint32_t)(N * NP);
+                sbase += 4u * (uint32_t)N;
+            }
+        }
+        if (zsel && zsel < kQuadCode) {
             const int js = s_plan[1];
             for (int k = threadIdx.x; k < N * NP; k += blockDim.x) {
                 const int jj = k / NP, r = k - jj * NP;
                 const int src = jj == 0 ? js : (jj == js ? 0 : jj);
-                const int v = r < N ? s_col[src * NP + s_plan[2 + r]] : 0;
+                const int v = r < N ? s_col[src * NP + s_plan[5 + r]] : 0;
                 s_col[2 * N * NP + k] = v;
                 s_col[3 * N * NP + k] = -v;
             }
-            for (int r = threadIdx.x; r < N; r += blockDim.x) s_base[N + r] = s_base[s_plan[2 + r]];
+            for (int r = threadIdx.x; r < N; r += blockDim.x) s_base[N + r] = s_base[s_plan[5 + r]];
             __syncthreads();
             sc += 8u * (uint32_t)(N * NP);
             sbase += 4u * (uint32_t)N;
@@ -577,7 +746,12 @@ __global__ void __launch_bounds__(I01Cfg<N>::NT, kInt01MinBlocks) int01_kernel(c
         else if (zsel == N - 18) int_walk<N, N - 18>(sc, sbase, e, chunks, c0, acc);
         else                     int_walk<N, 0>(sc, sbase, e, chunks, c0, acc);
     } else if constexpr (ZS) {
+        if constexpr (kQuad<N, PM1>) {
+            if (zsel == kQuadCode + N / 2)          { int_walk_q<N, N / 2>(sc, sbase, e, chunks, c0, acc); zsel = -1; }
+            else if (zsel == kQuadCode + N / 2 - 1) { int_walk_q<N, N / 2 - 1>(sc, sbase, e, chunks, c0, acc); zsel = -1; }
+        }
         switch (zsel) {
+            case -1: break;
             case 18: int_walk<N, 18>(sc, sbase, e, chunks, c0, acc); break;
             case 16: int_walk<N, 16>(sc, sbase, e, chunks, c0, acc); break;
             case 14: int_walk<N, 14>(sc, sbase, e, chunks, c0, acc); break;
@@ -603,6 +777,9 @@ __global__ void __launch_bounds__(I01Cfg<N>::NT, kInt01MinBlocks) int01_kernel(c
     if (threadIdx.x == 0) {
         u128 t = 0;
         for (int w = 0; w < I01Cfg<N>::NT / 32; w++) t += s_w[w];
+        if constexpr (ZS && kQuad<N, PM1>) {
+            if (qsign < 0) t = (u128)0 - t;             // per(A) = sign * per(A') (quad plan)
+        }
         u128* slot = partials + m * gridDim.x + blockIdx.x;
         *slot = accum ? *slot + t : t;                  // accum: later segments of a range add in (exact)
     }

@@ -68,3 +68,40 @@ def test_haar_minors_a3_expectation(torch):
     assert abs(abs2.mean() - expect) < 5 * se
     ref = oracle.ryser_batch(A[:64])
     assert np.allclose(abs2[:64], np.abs(ref) ** 2, rtol=1e-9, atol=0)
+
+
+# ---- the quad-factored walk: +-1 columns, rows sign-normalised on the bit-0 column, classes by the
+# bit-1 column; each order 20..24, both class sizes of the menu and the column-negation case, plus the fall-backs
+
+@pytest.mark.parametrize("n", [20, 21, 22, 23, 24])
+def test_pm1_quad_vs_oracle(torch, n):
+    A = inputs.bernoulli_pm1((6, n, n), 2000 + n)
+    assert pb.perm_pm1(torch.from_numpy(A).cuda()) == [oracle.ryser_i8(A[b]) for b in range(A.shape[0])]
+
+
+def test_pm1_quad_class_sizes_and_negation(torch):
+    # column 1's agreement with column 0 forced to z rows, z = 11, 12, 13 (13: the plan negates the column)
+    n = 24
+    rng = np.random.default_rng(2411)
+    mats = []
+    for z in (11, 12, 13, 7):
+        A = inputs.bernoulli_pm1((n, n), 5000 + z)
+        agree = np.zeros(n, bool)
+        agree[rng.choice(n, z, replace=False)] = True
+        A[:, 1] = np.where(agree, A[:, 0], -A[:, 0])
+        mats.append(A)
+    A = np.stack(mats)
+    assert pb.perm_pm1(torch.from_numpy(A).cuda()) == [oracle.ryser_i8(A[b]) for b in range(A.shape[0])]
+
+
+def test_pm1_quad_fallbacks(torch):
+    # zeros in every column (plain walk), zeros in a few columns only (quad plan on the others), and many zeros in
+    # one column (the zero-row plan)
+    n = 22
+    rng = np.random.default_rng(2212)
+    A = inputs.bernoulli_pm1((3, n, n), 2213)
+    A[0, rng.integers(0, n, n), np.arange(n)] = 0
+    A[1, 3, 0] = 0
+    A[1, 5, 1] = 0
+    A[2, rng.choice(n, 16, replace=False), 4] = 0
+    assert pb.perm_pm1(torch.from_numpy(A).cuda()) == [oracle.ryser_i8(A[b]) for b in range(A.shape[0])]
