@@ -965,7 +965,7 @@ def run_ours(args):
             n3 = 33 if cfg == "cfg3s" else 24
             ops = (units_per_step / world * 2 * n3 if cfg == "cfg3s"
                    else units_per_step / world * (1 << (n3 - 1)) * 2 * n3)
-            kname = {"cfgpm": "int01_kernel<24, pm1> (plain walk: no zero entries; INT fma + alu pipes)",
+            kname = {"cfgpm": "int01_kernel<24, pm1> (quad-factored walk; INT fma + alu pipes)",
                      "cfg3s": "int01_kernel<33> (Eq. (3) branch, pair-factored walk; INT fma + alu pipes)"}.get(
                          cfg, "int01_kernel<24> (pair-factored walk; INT fma + alu pipes)")
             achieved = ops / (dev_ms / K * 1e-3) / 1e12
@@ -975,9 +975,8 @@ def run_ours(args):
                                "kernel": kname,
                                "algorithmic": ("2n integer ops per Gray term x 2^n terms / ranks" if cfg == "cfg3s" else
                                                "2n integer ops per Gray term x 2^(n-1) terms x matrices") +
-                                              ("" if cfg == "cfgpm" else
-                                               " (the plain walk's count: the pair-factored walk needs fewer "
-                                               "operations per term, so frac is an effective rate; DESIGN.md 5.3)"),
+                                              " (the plain walk's count: the pair/quad-factored walks need fewer "
+                                              "operations per term, so frac is an effective rate; DESIGN.md 5.3)",
                                "peak_note": "derived: 148 SMs x 128 int lanes/clk (issue-bound) x 1965 MHz"}
     out["e2e"] = {"value": e2e_val, "unit": unit, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
     if cfg == "cfg3s":
