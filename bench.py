@@ -909,10 +909,13 @@ def run_ours(args):
         out["roofline"] = {"bound": "alu", "achieved": achieved, "peak": nominal, "unit": "TFLOP/s",
                            "frac": achieved / nominal, "traffic": ncu_traffic(cfg),
                            "kernel": ((f"walk_small_kernel<{n}> (one cluster launch: walk + tree)" if n <= 16
-                                       else f"walk_kernel_c<{n}>" if n == 32
-                                       else f"walk_kernel_cm<{n}>" if 33 <= n <= 48 else f"walk_kernel<{n}>")
+                                       else f"walk_kernel_c<{n}, unit column>" if n == 32
+                                       else f"walk_kernel_cm<{n}, unit column>" if 33 <= n <= 48 else f"walk_kernel<{n}>")
                                       + " (FP64 vector pipe)"),
-                           "algorithmic": "8n flops per Gray term x terms per launch (rank 0)",
+                           "algorithmic": ("8n flops per Gray term x terms per launch (rank 0)" +
+                                           (" (the unit-column walk executes 5n - 2 FP64 instructions per term "
+                                            "instead of 6n - 4: ceiling 0.81 instead of 0.68 of peak at n = 44; "
+                                            "DESIGN.md 5.1)" if 32 <= n <= 48 else "")),
                            "peak_note": "derived: 148 SMs x 64 FP64 FMA/clk x 2 x 1965 MHz",
                            "peak_measured_probe": peak_meas, "frac_of_measured": achieved / peak_meas,
                            "walk_ms_per_launch": walk_ms}

@@ -268,6 +268,43 @@ perm_status_t nonfinite_status(const perm_c128_t* A, int n, cudaStream_t s) {
     return host_matrix(A, n, is_device_ptr(A), true, s, host, &h);
 }
 
+// Unit-column normalisation (internal.h walk_unit0): A'_ij = a_ij / a_i0 with column 0 set to exactly
+// 1, and scale = prod_i a_i0 in double-double (per(A) = scale * per(A') term by term).  false (walk A as is) when the
+// order does not use it or a row's column-0 entry is zero or so far from the row's other entries that A' could
+// overflow.
+bool unit0_normalize(const perm_c128_t* h, int n, std::vector<perm_c128_t>& out, perm::ddc& scale) {
+    if (n < 2 || !perm::walk_unit0(n)) return false;
+    static const bool enabled = !(getenv("PERM_UNIT0") && atoi(getenv("PERM_UNIT0")) == 0);   // (development)
+    if (!enabled) return false;
+    out.resize((size_t)n * n);
+    scale.re = perm::dd{1.0, 0.0};
+    scale.im = perm::dd{0.0, 0.0};
+    for (int i = 0; i < n; i++) {
+        const double ar = h[(size_t)i * n].re, ai = h[(size_t)i * n].im;
+        const double m = std::fabs(ar) > std::fabs(ai) ? std::fabs(ar) : std::fabs(ai);
+        if (!(m > 0.0)) return false;
+        double rmax = 0.0;
+        for (int j = 1; j < n; j++) {
+            const double v = std::fabs(h[(size_t)i * n + j].re) + std::fabs(h[(size_t)i * n + j].im);
+            rmax = v > rmax ? v : rmax;
+        }
+        if (rmax / m > 1e100) return false;               // keep |a'_ij| far from overflow
+        // 1 / a_i0 = conj(a_i0) / |a_i0|^2, scaled by m to avoid underflow of |a_i0|^2
+        const double sr = ar / m, si = ai / m, d = sr * sr + si * si;
+        const double ir = sr / (d * m), ii = -si / (d * m);
+        out[(size_t)i * n] = perm_c128_t{1.0, 0.0};
+        for (int j = 1; j < n; j++) {
+            const perm_c128_t a = h[(size_t)i * n + j];
+            out[(size_t)i * n + j] = perm_c128_t{a.re * ir - a.im * ii, a.re * ii + a.im * ir};
+        }
+        perm::ddc f;
+        f.re = perm::dd{ar, 0.0};
+        f.im = perm::dd{ai, 0.0};
+        scale = perm::ddc_mul(scale, f);
+    }
+    return std::isfinite(scale.re.hi) && std::isfinite(scale.im.hi);
+}
+
 // The walk of plan p over A into items (device, p.items entries).  ws_a: device scratch for A if A is host.
 perm_status_t launch_walk(const perm_c128_t* A, int n, const WalkPlan& p, ddc* items, char* ws_a, cudaStream_t s,
                           perm_stats_t* stats, uint32_t* launches) {
@@ -277,7 +314,16 @@ perm_status_t launch_walk(const perm_c128_t* A, int n, const WalkPlan& p, ddc* i
     perm_status_t st = host_matrix(A, n, a_dev, p.use_const != 0, s, host, &h);
     if (st != PERM_OK) return st;
     const double2* A_dev = (const double2*)A;
-    if (!a_dev) {
+    // unit-column walk (internal.h walk_unit0): A' = D^{-1} A with column 0 all ones, scale = prod_i a_i0
+    std::vector<perm_c128_t> unit;
+    perm::ddc scale{};
+    const bool use_unit = p.use_const && h != nullptr && unit0_normalize(h, n, unit, scale);
+    if (use_unit) {
+        PERM_CUDA(cudaMemcpyAsync(ws_a, unit.data(), (size_t)n * n * sizeof(double2), cudaMemcpyHostToDevice, s),
+                  "cudaMemcpyAsync(A' H2D)");
+        A_dev = (const double2*)ws_a;
+        h = unit.data();
+    } else if (!a_dev) {
         PERM_CUDA(cudaMemcpyAsync(ws_a, A, (size_t)n * n * sizeof(double2), cudaMemcpyHostToDevice, s),
                   "cudaMemcpyAsync(A H2D)");
         A_dev = (const double2*)ws_a;
@@ -285,6 +331,9 @@ perm_status_t launch_walk(const perm_c128_t* A, int n, const WalkPlan& p, ddc* i
     perm::WalkLaunch WL;
     WL.A_dev = A_dev;
     WL.A_host = (const double2*)h;
+    WL.unit0 = use_unit ? 1 : 0;
+    WL.scaled = use_unit ? 1 : 0;
+    WL.scale = scale;
     WL.n = n;
     WL.nseg = p.nseg;
     for (int i = 0; i < p.nseg; i++) WL.seg[i] = p.seg[i];

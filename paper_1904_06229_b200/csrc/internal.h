@@ -63,7 +63,10 @@ __host__ __device__ constexpr int walk_block_threads(int n) {
 constexpr int kWalkFoldBits = PERM_WALK_FOLD;
 // The n = 44 constant-bank walk folds every 2^7 terms: +0.3% (profiles/round1_walk_chains.txt); the plain
 // partial over 128 terms of |prod w| ~ 1e23 carries ~1e9 absolute rounding, 1e-20 of the error floor.
-__host__ __device__ constexpr int walk_fold_bits_const(int n) { return n == 44 ? 7 : kWalkFoldBits; }
+#ifndef PERM_FOLD44
+#define PERM_FOLD44 7
+#endif
+__host__ __device__ constexpr int walk_fold_bits_const(int n) { return n == 44 ? PERM_FOLD44 : kWalkFoldBits; }
 
 // A run of `count` aligned chunks of 2^e ranks: chunk k covers ranks [(c0+k) 2^e, (c0+k+1) 2^e).
 // e == 0 chunks are single terms (seeded from scratch).
@@ -92,6 +95,19 @@ __host__ __device__ constexpr bool walk_const_path(int n) {
 #else
     return n == PERM_CONST_ORDERS || (n >= PERM_CONST_MIN && n <= kConstMaxN);
 #endif
+}
+
+// Unit-column walk: for these constant-bank orders the library walks A' = D^{-1} A, each row
+// divided by its entry in column 0 (the Gray bit-0 column), so that column is all ones; per(A) = prod_i a_i0 *
+// per(A') term by term, and every item partial is multiplied by that product (in double-double) before it is
+// written, so partials, tree nodes and results stay in the units of A.  With a unit bit-0 column the two terms of
+// ranks 2q, 2q+1 are prod v and prod (v + 1) for one row-sum vector v: the bit-0 flips disappear and the "+1" fuses
+// into the product's FMAs.  PERM_UNIT0_ORDERS=0: off; =1: every constant-bank order; else that order only.
+#ifndef PERM_UNIT0_ORDERS
+#define PERM_UNIT0_ORDERS 1
+#endif
+__host__ __device__ constexpr bool walk_unit0(int n) {
+    return PERM_UNIT0_ORDERS == 1 ? walk_const_path(n) : (PERM_UNIT0_ORDERS != 0 && n == PERM_UNIT0_ORDERS);
 }
 
 // chunk walkers per block of the kernel that walks the aligned body (walk_kernel_c)
@@ -125,6 +141,9 @@ struct WalkLaunch {
     int use_const;          // run segment `body` in walk_kernel_c
     int body;               // index of the body segment (use_const)
     int grid_edge;          // blocks of the edge launch (use_const and nseg > 1), else 0
+    int unit0;              // A_dev / A_host hold A' (column 0 all ones, walk_unit0): the body runs the unit-column walk
+    int scaled;             // multiply every item partial by `scale` (= prod_i a_i0 when unit0)
+    ddc scale;
     cudaStream_t stream;
 };
 

@@ -80,6 +80,8 @@ struct WalkParams {
     uint64_t seg_pre[kMaxSegments + 1];    // prefix item counts
     int32_t seg_e[kMaxSegments];
     int32_t nseg;
+    int32_t scaled;                        // unit-column walk: multiply every item partial by `scale`
+    ddc scale;
 };
 
 // Load of one complex entry from shared memory (volatile: never hoisted or merged).
@@ -222,6 +224,54 @@ __device__ __forceinline__ void term_acc(const double (&wr)[R], const double (&w
         two_factors<R, K>(wr, wi, xr, xi, yr, yi);
         fused_acc<SIGN>(xr, xi, yr, yi, ar, ai);
     }
+}
+
+// Unit-column walk (internal.h walk_unit0): x *= (y + 1) as 4 DFMA -- the "+1" of the unit bit-0 column rides in
+// the FMAs' addends: re = xr (yr + 1) - xi yi = fma(-xi, yi, fma(xr, yr, xr)), im = fma(xr, yi, fma(xi, yr, xi)).
+__device__ __forceinline__ void cmul_shift1(double& xr, double& xi, double yr, double yi) {
+    const double t = fma(xr, yr, xr);
+    const double u = fma(xi, yr, xi);
+    const double nr = fma(-xi, yi, t);
+    xi = fma(xr, yi, u);
+    xr = nr;
+}
+
+// prod_i (w_i + 1) split into two factors X * Y (the two_factors chain layouts, K = 2 or 4)
+template <int R, int K>
+__device__ __forceinline__ void two_factors_shift1(const double (&wr)[R], const double (&wi)[R], double& xr, double& xi,
+                                                   double& yr, double& yi) {
+    static_assert(K == 2 || K == 4, "unit-column walk: two or four chains");
+    if constexpr (K == 2) {
+        xr = wr[0] + 1.0;
+        xi = wi[0];
+#pragma unroll
+        for (int i = 1; i < R / 2; i++) cmul_shift1(xr, xi, wr[i], wi[i]);
+        yr = wr[R / 2] + 1.0;
+        yi = wi[R / 2];
+#pragma unroll
+        for (int i = R / 2 + 1; i < R; i++) cmul_shift1(yr, yi, wr[i], wi[i]);
+    } else {
+        double r0 = wr[0] + 1.0, i0 = wi[0], r1 = wr[1] + 1.0, i1 = wi[1];
+        double r2 = wr[2] + 1.0, i2 = wi[2], r3 = wr[3] + 1.0, i3 = wi[3];
+#pragma unroll
+        for (int i = 4; i < R; i++) {
+            if ((i & 3) == 0) cmul_shift1(r0, i0, wr[i], wi[i]);
+            else if ((i & 3) == 1) cmul_shift1(r1, i1, wr[i], wi[i]);
+            else if ((i & 3) == 2) cmul_shift1(r2, i2, wr[i], wi[i]);
+            else cmul_shift1(r3, i3, wr[i], wi[i]);
+        }
+        cmul2(r0, i0, r1, i1);
+        cmul2(r2, i2, r3, i3);
+        xr = r0; xi = i0; yr = r2; yi = i2;
+    }
+}
+
+// acc += SIGN * prod_i (w_i + 1)
+template <int R, int K, int SIGN>
+__device__ __forceinline__ void term_acc_shift1(const double (&wr)[R], const double (&wi)[R], double& ar, double& ai) {
+    double xr, xi, yr, yi;
+    two_factors_shift1<R, K>(wr, wi, xr, xi, yr, yi);
+    fused_acc<SIGN>(xr, xi, yr, yi, ar, ai);
 }
 
 __device__ __forceinline__ double flip_sign_if(double v, uint32_t mask_hi) {
@@ -496,6 +546,7 @@ __global__ void __launch_bounds__(WalkCfg<N>::NT, WalkCfg<N>::MINB) walk_kernel(
                 for (int off = C::S / 2; off > 0; off >>= 1) v = ddc_add(v, shfl_down_ddc(v, off, group_mask<C::S>()));
             }
             PERM_DCHECK(P.seg_item0[s] + i < P.nitems);
+            if (P.scaled) v = ddc_mul(v, P.scale);             // unit-column walk: back to the units of A
             if (h == 0) P.items[P.seg_item0[s] + i] = v;
         }
     }
@@ -523,7 +574,7 @@ template <int N>
 struct WalkParamsC {
     static constexpr int NC = walk_inner_bits(N);   // columns held in the constant bank (the inner flips)
     static constexpr int MN = walk_const_midneg(N);
-    double2 col[NC + MN][N];               // col[j][i] = a_ij, j < U; col[U][i] = -a_{i,U-1} (MN = 1)
+    double2 col[NC + 1][N];                // col[j][i] = a_ij, j < U; col[U][i] = -a_{i,U-1} (used by MN = 1 and unit)
     const double2* A;                      // device, row-major (staged to shared memory)
     ddc* items;                            // item partials; body chunk c0 + g -> items[item0 + g]
     uint64_t item0;
@@ -533,6 +584,8 @@ struct WalkParamsC {
     uint64_t c0;                           // first body chunk
     uint64_t count;                        // body chunks
     int32_t eb;                            // log2 body chunk length (>= U)
+    int32_t scaled;                        // unit-column walk: multiply every item partial by `scale`
+    ddc scale;
 };
 
 template <class C, int T>
@@ -580,7 +633,53 @@ struct InnerStepC {
     }
 };
 
-template <class C>
+// product chains per factor of the unit-column walk (development: PERM_UNIT_K overrides the plain walk's K)
+#ifndef PERM_UNIT_K
+#define PERM_UNIT_K 0
+#endif
+__host__ __device__ constexpr int unit_chains(int n, int k) { return PERM_UNIT_K > 0 ? PERM_UNIT_K : k; }
+
+// Unit-column walk over the pairs (T, T+1), T even, of the inner block: the row sums v hold Gray bit 0 = 0 (column 0
+// is all ones and never added), term T + (bit 0) reads v + 1.  Gray bit 0 of rank T is bit 1 of T, so the pair is
+// s_T (prod (v + 1) - prod v) with s_T = +1 if bit 1 of T is 0, else -1 (signs (-1)^{r+1}, App. A).
+template <class C, int T>
+struct InnerStepCU {
+    static constexpr int N = C::N;
+    static __device__ __forceinline__ void run(const WalkParamsC<N>& P, int z, double (&wr)[N], double (&wi)[N],
+                                               double zmid, double& ar, double& ai) {
+        constexpr int U = C::U;
+        static_assert(T % 2 == 0 && U >= 2, "pairs of an aligned block of >= 4 ranks");
+        if constexpr (T > 0) {
+            constexpr int J = ctz_c((unsigned)T);            // >= 1
+            const int jj = J + z * (T + 1);
+            if constexpr (J == U - 1) {
+                // the mid-block column with its sign by address (+a at col[U-1], -a at col[U]): DADD R, R, UR
+                const int jm = jj + (zmid < 0.0 ? 1 : 0);
+#pragma unroll
+                for (int i = 0; i < N; i++) {
+                    const double2 a = P.col[jm][i];
+                    wr[i] += a.x;
+                    wi[i] += a.y;
+                }
+            } else {
+                constexpr bool PLUS = ((T >> (J + 1)) & 1) == 0;
+#pragma unroll
+                for (int i = 0; i < N; i++) {
+                    const double2 a = P.col[jj][i];
+                    if (PLUS) { wr[i] += a.x; wi[i] += a.y; }
+                    else      { wr[i] -= a.x; wi[i] -= a.y; }
+                }
+            }
+        }
+        constexpr int SP = ((T >> 1) & 1) ? -1 : 1;
+        constexpr int KU = unit_chains(N, C::K);
+        term_acc<N, KU, -SP>(wr, wi, ar, ai);
+        term_acc_shift1<N, KU, SP>(wr, wi, ar, ai);
+        if constexpr (T + 2 < (1 << U)) InnerStepCU<C, T + 2>::run(P, z, wr, wi, zmid, ar, ai);
+    }
+};
+
+template <class C, bool UNIT>
 __device__ __forceinline__ void walk_chunk_const(const WalkParamsC<C::N>& P, uint32_t lc, uint32_t lb, uint64_t c,
                                                  ddc& acc) {
     constexpr int N = C::N, U = C::U;
@@ -608,7 +707,8 @@ __device__ __forceinline__ void walk_chunk_const(const WalkParamsC<C::N>& P, uin
             const uint64_t nb = (j + 1 < e) ? (uint64_t)((q >> (j + 1 - U)) & 1) : cpar;
             flip_add<N>(lc + (uint32_t)(j * N) * 16u + (nb ? C::NEG : 0u), wr, wi);
         }
-        InnerStepC<C, 0>::run(P, z, wr, wi, (q & 1) ? -1.0 : 1.0, ar, ai);   // bit_U(rank) = q & 1 (e > U)
+        if constexpr (UNIT) InnerStepCU<C, 0>::run(P, z, wr, wi, (q & 1) ? -1.0 : 1.0, ar, ai);
+        else                InnerStepC<C, 0>::run(P, z, wr, wi, (q & 1) ? -1.0 : 1.0, ar, ai);   // bit_U(rank) = q & 1 (e > U)
         if (((q + 1) & kFoldMask) == 0 || q + 1 == nblk) {
             acc.re = dd_add_d(acc.re, ar);
             acc.im = dd_add_d(acc.im, ai);
@@ -624,32 +724,35 @@ __device__ __forceinline__ void walk_chunk_const(const WalkParamsC<C::N>& P, uin
 // measured to produce LDCU with 0 spill bytes (rescanned in round 2 for the per-chunk partial stores,
 // profiles/round2_const_ldcu_scan.txt; n = 42 only with its mid-block sign by address), and
 // tests/test_abi_cpu.py checks the built library still does.
+#ifndef PERM_CAP44
+#define PERM_CAP44 244
+#endif
 __host__ __device__ constexpr int walk_const_maxnreg(int n) {
 #ifdef PERM_CONST_MAXNREG_ALL
     return PERM_CONST_MAXNREG_ALL;                  // scans only (tools/const_ldcu_scan.sh)
 #else
     return n == 33 ? (PERM_U2_FROM33 ? 176 : 172) : n == 34 ? 192 : n == 35 ? 196
          : n == 36 ? (PERM_U2_FROM33 ? 196 : 188) : n == 37 ? 204 : n == 38 ? (PERM_U2_FROM33 ? 204 : 200)
-         : n == 39 ? 212 : n == 40 ? 212 : n == 41 ? 212 : n == 42 ? 216 : n == 43 ? 204 : n == 44 ? 244
+         : n == 39 ? 212 : n == 40 ? 212 : n == 41 ? 212 : n == 42 ? 216 : n == 43 ? 204 : n == 44 ? PERM_CAP44
          : n == 45 ? 236 : n == 46 ? 240 : n == 47 ? 240 : n == 48 ? 244 : 0;
 #endif
 }
 
-template <int N>
+template <int N, bool UNIT>
 __device__ __forceinline__ void walk_body_c(const WalkParamsC<N>& P);
 
-template <int N>
+template <int N, bool UNIT>
 __global__ void __launch_bounds__(walk_block_threads(N)) walk_kernel_c(const __grid_constant__ WalkParamsC<N> P) {
-    walk_body_c<N>(P);
+    walk_body_c<N, UNIT>(P);
 }
 
-template <int N>
+template <int N, bool UNIT>
 __global__ void __maxnreg__(walk_const_maxnreg(N) > 0 ? walk_const_maxnreg(N) : 255)
     walk_kernel_cm(const __grid_constant__ WalkParamsC<N> P) {
-    walk_body_c<N>(P);
+    walk_body_c<N, UNIT>(P);
 }
 
-template <int N>
+template <int N, bool UNIT>
 __device__ __forceinline__ void walk_body_c(const WalkParamsC<N>& P) {
     using C = WCfg<N, 1>;
     extern __shared__ double2 smem[];
@@ -683,7 +786,8 @@ __device__ __forceinline__ void walk_body_c(const WalkParamsC<N>& P) {
         const bool valid = g < P.count;
         ddc part;
         part.re.hi = part.re.lo = part.im.hi = part.im.lo = 0.0;
-        walk_chunk_const<C>(P, lc, lb, P.c0 + (valid ? g : 0), part);
+        walk_chunk_const<C, UNIT>(P, lc, lb, P.c0 + (valid ? g : 0), part);
+        if (P.scaled) part = ddc_mul(part, P.scale);          // unit-column walk: back to the units of A
 #ifdef PERM_DEBUG_CHECKS
         PERM_DCHECK(!valid || P.item0 + g < P.nitems);
 #endif
@@ -898,9 +1002,27 @@ cudaError_t walk_launch_smem(const WalkLaunch& L, const Segment* seg, const uint
     }
     P.seg_pre[kMaxSegments] = pre;
     P.nseg = nseg;
+    P.scaled = L.scaled;
+    P.scale = L.scale;
     // the dynamic shared-memory attribute was set by walk_occupancy<N> (abi.cu geometry cache)
     walk_kernel<N><<<grid, C::NT, C::smem_bytes, L.stream>>>(P);
     return cudaGetLastError();
+}
+
+// Dynamic shared memory attribute of a unit-column walk kernel (set once per kernel and device; the non-unit kernel's
+// is set by walk_occupancy_c).
+template <class K>
+cudaError_t unit0_attr(K* kern, size_t smem) {
+    static std::once_flag once[64];
+    static cudaError_t err[64];
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+    std::call_once(once[dev], [&] {
+        err[dev] = cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    });
+    return err[dev];
 }
 
 // Launches the walk over L.seg; item k of the plan (segments in order, chunks in rank order) writes its dd
@@ -920,11 +1042,10 @@ cudaError_t walk_launch(const WalkLaunch& L) {
             WalkParamsC<N> P;
             for (int j = 0; j < WalkParamsC<N>::NC; j++)
                 for (int i = 0; i < N; i++) P.col[j][i] = L.A_host[(size_t)i * N + j];
-            if constexpr (WalkParamsC<N>::MN == 1)
-                for (int i = 0; i < N; i++) {
-                    const double2 a = L.A_host[(size_t)i * N + WalkParamsC<N>::NC - 1];
-                    P.col[WalkParamsC<N>::NC][i] = make_double2(-a.x, -a.y);
-                }
+            for (int i = 0; i < N; i++) {
+                const double2 a = L.A_host[(size_t)i * N + WalkParamsC<N>::NC - 1];
+                P.col[WalkParamsC<N>::NC][i] = make_double2(-a.x, -a.y);
+            }
             P.A = L.A_dev;
             P.items = L.items;
             P.item0 = item0[L.body];
@@ -934,10 +1055,29 @@ cudaError_t walk_launch(const WalkLaunch& L) {
             P.c0 = b.c0;
             P.count = b.count;
             P.eb = b.e;
-            if constexpr (walk_const_maxnreg(N) > 0)
-                walk_kernel_cm<N><<<L.grid, walk_block_threads(N), WCfg<N, 1>::smem_bytes, L.stream>>>(P);
-            else
-                walk_kernel_c<N><<<L.grid, walk_block_threads(N), WCfg<N, 1>::smem_bytes, L.stream>>>(P);
+            P.scaled = L.scaled;
+            P.scale = L.scale;
+            const bool unit = walk_unit0(N) && L.unit0;
+            if constexpr (walk_unit0(N)) {
+                if (unit) {
+                    cudaError_t ea = cudaSuccess;
+                    if constexpr (walk_const_maxnreg(N) > 0)
+                        ea = unit0_attr(walk_kernel_cm<N, true>, WCfg<N, 1>::smem_bytes);
+                    else
+                        ea = unit0_attr(walk_kernel_c<N, true>, WCfg<N, 1>::smem_bytes);
+                    if (ea != cudaSuccess) return ea;
+                    if constexpr (walk_const_maxnreg(N) > 0)
+                        walk_kernel_cm<N, true><<<L.grid, walk_block_threads(N), WCfg<N, 1>::smem_bytes, L.stream>>>(P);
+                    else
+                        walk_kernel_c<N, true><<<L.grid, walk_block_threads(N), WCfg<N, 1>::smem_bytes, L.stream>>>(P);
+                }
+            }
+            if (!unit) {
+                if constexpr (walk_const_maxnreg(N) > 0)
+                    walk_kernel_cm<N, false><<<L.grid, walk_block_threads(N), WCfg<N, 1>::smem_bytes, L.stream>>>(P);
+                else
+                    walk_kernel_c<N, false><<<L.grid, walk_block_threads(N), WCfg<N, 1>::smem_bytes, L.stream>>>(P);
+            }
             cudaError_t err = cudaGetLastError();
             if (err != cudaSuccess || L.grid_edge == 0) return err;
             Segment rest[kMaxSegments];
@@ -960,8 +1100,8 @@ cudaError_t walk_occupancy_c(int* blocks_per_sm) {
     *blocks_per_sm = 0;
     if constexpr (walk_const_path(N) && walk_inner_bits(N) >= 1) {
         const void* k;
-        if constexpr (walk_const_maxnreg(N) > 0) k = (const void*)walk_kernel_cm<N>;
-        else                                     k = (const void*)walk_kernel_c<N>;
+        if constexpr (walk_const_maxnreg(N) > 0) k = (const void*)walk_kernel_cm<N, false>;
+        else                                     k = (const void*)walk_kernel_c<N, false>;
         cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                (int)WCfg<N, 1>::smem_bytes);
         if (err != cudaSuccess) return err;

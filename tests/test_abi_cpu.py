@@ -136,16 +136,23 @@ def test_const_walk_keeps_uniform_column_operands():
     if not os.path.exists(cuobjdump):
         pytest.skip("cuobjdump not available")
     lib = pb._LIB_PATH
-    fns = ["_ZN4perm13walk_kernel_cILi32EEEvNS_11WalkParamsCIXT_EEE"]
-    fns += [f"_ZN4perm14walk_kernel_cmILi{n}EEEvNS_11WalkParamsCIXT_EEE" for n in (34, 35, 37, 39, 43, 44, 45)]
+    def walk_fn(n, unit):
+        k = "13walk_kernel_c" if n == 32 else "14walk_kernel_cm"
+        return f"_ZN4perm{k}ILi{n}ELb{int(unit)}EEEvNS_11WalkParamsCIXT_EEE"
+
+    # plain constant-bank walks: every inner column flip from uniform registers (> 100 LDCU.64 per kernel)
+    fns = [(walk_fn(n, False), 100) for n in (32, 34, 35, 37, 39, 43, 44, 45)]
+    # unit-column walks (column 0 all ones, internal.h walk_unit0): the one inner column flip per pair of terms,
+    # n complex entries = 2n LDCU.64 per block at least
+    fns += [(walk_fn(n, True), 2 * n - 1) for n in range(32, 49) if n != 42]
     # the sparse kernel's constant-bank variant (sparse.cuh, sparse_const_path)
-    fns += [f"_ZN4perm15sparse_kernel_cILi{n}EEEvNS_13SparseParamsCIXT_EEE"
+    fns += [(f"_ZN4perm15sparse_kernel_cILi{n}EEEvNS_13SparseParamsCIXT_EEE", 100)
             for n in list(range(17, 24)) + list(range(25, 34)) + [47, 48]]
-    for fn in fns:
+    for fn, least in fns:
         sass = subprocess.run([cuobjdump, "-sass", "-fun", fn, lib], capture_output=True, text=True).stdout
         uniform = sum(1 for l in sass.splitlines() if "LDCU.64" in l and "c[0x0][UR" in l)
         lane = sum(1 for l in sass.splitlines() if " LDC.64 R" in l and "c[0x0][R" in l)
-        assert uniform > 100 and lane == 0, (fn, uniform, lane)
+        assert uniform > least and lane == 0, (fn, uniform, lane)
 
 
 def test_no_register_spills_in_library_kernels():
