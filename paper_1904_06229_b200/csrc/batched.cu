@@ -14,6 +14,12 @@
 
 namespace perm {
 
+// unit-column walk in the batched kernel (development: PERM_BATCHED_UNIT=0 walks every matrix as given)
+#ifndef PERM_BATCHED_UNIT
+#define PERM_BATCHED_UNIT 1
+#endif
+constexpr bool kBatchedUnit = PERM_BATCHED_UNIT != 0;
+
 template <int N>
 struct BatCfg {
     static constexpr int LOG_L = (N - 1 - 5) < 0 ? 0 : ((N - 1 - 5) > 5 ? 5 : (N - 1 - 5));
@@ -50,6 +56,49 @@ __global__ void __launch_bounds__(BatCfg<N>::NT) batched_kernel(const double2* _
         wbase[g * C::SLOT + N * N + j * N + i] = make_double2(-a.x, -a.y);
     }
     __syncwarp();
+    // unit-column walk (walk.cuh InnerStepU) when a warp walks one matrix (n >= 11): rows divided by their column-0
+    // entry, scale = prod_i a_i0 in double-double (a fixed shuffle tree over the rows' lanes); a matrix with a zero (or
+    // relatively tiny) column-0 entry is walked as given
+    constexpr bool UNIT = kBatchedUnit && C::G == 1 && C::E >= WCfg<N, 1>::U && WCfg<N, 1>::K >= 2;
+    [[maybe_unused]] bool unit = false;
+    [[maybe_unused]] ddc scale;
+    if constexpr (UNIT) {
+        ddc f;
+        f.re = dd{1.0, 0.0};
+        f.im = dd{0.0, 0.0};
+        bool okl = true;
+        if (lane < N) {
+            const double2 a = wbase[lane];                        // column 0, row `lane`
+            const double m = fmax(fabs(a.x), fabs(a.y));
+            double rmax = 0.0;
+            for (int j = 1; j < N; j++) rmax = fmax(rmax, fabs(wbase[j * N + lane].x) + fabs(wbase[j * N + lane].y));
+            okl = m > 0.0 && rmax / m <= 1e100;
+            f.re = dd{a.x, 0.0};
+            f.im = dd{a.y, 0.0};
+        }
+        unit = __all_sync(0xffffffffu, okl);
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) f = ddc_mul(f, shfl_down_ddc(f, off));   // lane 0: the product
+        scale = f;
+        if (unit) {
+            // a'_ij = a_ij / a_i0 (= a_ij conj(a_i0) / |a_i0|^2, scaled by max(|re|, |im|) against underflow)
+            for (int r = lane; r < N * N; r += 32) {
+                const int jc = r / N, i = r - jc * N;             // column-major: r = j N + i
+                const double2 a0 = wbase[i];
+                const double m = fmax(fabs(a0.x), fabs(a0.y));
+                const double sr = a0.x / m, si = a0.y / m, d = sr * sr + si * si;
+                const double ir = sr / (d * m), ii = -si / (d * m);
+                const double2 a = wbase[r];
+                const double2 v = jc == 0 ? make_double2(1.0, 0.0)
+                                          : make_double2(a.x * ir - a.y * ii, a.x * ii + a.y * ir);
+                wbase[N * N + r] = make_double2(-v.x, -v.y);
+                if (jc != 0) wbase[r] = v;
+            }
+            __syncwarp();
+            if (lane < N) wbase[lane] = make_double2(1.0, 0.0);  // column 0 last (the others read it)
+            __syncwarp();
+        }
+    }
     for (int k = lane; k < gcount * N; k += 32) {
         const int g = k / N, i = k - g * N;
         const double2* sc = wbase + g * C::SLOT;
@@ -72,6 +121,9 @@ __global__ void __launch_bounds__(BatCfg<N>::NT) batched_kernel(const double2* _
         const uint32_t sbase = sc + (uint32_t)(2 * N * N) * 16u;
         if constexpr (C::E == 0) {
             single_term<WC>(sc, sbase, 0u, (uint64_t)l, acc);
+        } else if constexpr (UNIT) {
+            if (unit) walk_chunk_unit<WC>(sc, sbase, (uint64_t)l, C::E, acc);
+            else      walk_chunk<WC>(sc, sbase, 0u, (uint64_t)l, C::E, acc);
         } else {
             walk_chunk<WC>(sc, sbase, 0u, (uint64_t)l, C::E, acc);
         }
@@ -80,6 +132,9 @@ __global__ void __launch_bounds__(BatCfg<N>::NT) batched_kernel(const double2* _
 #pragma unroll
     for (int off = C::L / 2; off > 0; off >>= 1) acc = ddc_add(acc, shfl_down_ddc(acc, off));
     if (l == 0 && g < gcount) {
+        if constexpr (UNIT) {
+            if (unit) acc = ddc_mul(acc, scale);                 // back to the units of A (lane 0 holds the scale)
+        }
         const double f = (N & 1) ? -2.0 : 2.0;
         const double re = (acc.re.hi + acc.re.lo) * f;
         const double im = (acc.im.hi + acc.im.lo) * f;

@@ -266,6 +266,28 @@ __device__ __forceinline__ void two_factors_shift1(const double (&wr)[R], const 
     }
 }
 
+// acc += SP (prod (w_i + 1) - prod w_i) with the two products' chains interleaved row by row (K = 4 each: eight
+// independent chains in flight; development variant PERM_UNIT_INTERLEAVE)
+template <int R, int SP>
+__device__ __forceinline__ void pair_acc_interleaved(const double (&wr)[R], const double (&wi)[R], double& ar, double& ai) {
+    double r0 = wr[0], i0 = wi[0], r1 = wr[1], i1 = wi[1], r2 = wr[2], i2 = wi[2], r3 = wr[3], i3 = wi[3];
+    double s0 = wr[0] + 1.0, j0 = wi[0], s1 = wr[1] + 1.0, j1 = wi[1];
+    double s2 = wr[2] + 1.0, j2 = wi[2], s3 = wr[3] + 1.0, j3 = wi[3];
+#pragma unroll
+    for (int i = 4; i < R; i++) {
+        if ((i & 3) == 0)      { cmul2(r0, i0, wr[i], wi[i]); cmul_shift1(s0, j0, wr[i], wi[i]); }
+        else if ((i & 3) == 1) { cmul2(r1, i1, wr[i], wi[i]); cmul_shift1(s1, j1, wr[i], wi[i]); }
+        else if ((i & 3) == 2) { cmul2(r2, i2, wr[i], wi[i]); cmul_shift1(s2, j2, wr[i], wi[i]); }
+        else                   { cmul2(r3, i3, wr[i], wi[i]); cmul_shift1(s3, j3, wr[i], wi[i]); }
+    }
+    cmul2(r0, i0, r1, i1);
+    cmul2(s0, j0, s1, j1);
+    cmul2(r2, i2, r3, i3);
+    cmul2(s2, j2, s3, j3);
+    fused_acc<-SP>(r0, i0, r2, i2, ar, ai);
+    fused_acc<SP>(s0, j0, s2, j2, ar, ai);
+}
+
 // acc += SIGN * prod_i (w_i + 1)
 template <int R, int K, int SIGN>
 __device__ __forceinline__ void term_acc_shift1(const double (&wr)[R], const double (&wi)[R], double& ar, double& ai) {
@@ -439,6 +461,62 @@ __device__ __forceinline__ void walk_seeded(uint32_t lc, uint32_t h, uint64_t c,
         const uint32_t lmid = lc + (uint32_t)((U - 1) * C::P) * 16u + (nbm ? C::NEG : 0u);
         InnerStep<C, 0>::run(lc, lmid, h, wr, wi, ar, ai, pr, pi);
         // fold the plain block sums into the dd accumulator every 2^kWalkFoldBits terms (and at the end)
+        if (((q + 1) & kFoldMask) == 0 || q + 1 == nblk) {
+            acc.re = dd_add_d(acc.re, ar);
+            acc.im = dd_add_d(acc.im, ai);
+            ar = 0.0;
+            ai = 0.0;
+        }
+    }
+}
+
+// Unit-column walk on shared-memory columns (batched kernel; internal.h walk_unit0): column 0 of the staged matrix
+// is all ones and never added -- the row sums v hold Gray bit 0 = 0 -- and the pair (T, T+1), T even, adds
+// s_T (prod (v + 1) - prod v), s_T = +1 iff bit 1 of T is 0 (see InnerStepCU).  One lane per chunk.
+template <class C, int T>
+struct InnerStepU {
+    static constexpr int R = C::R;
+    static __device__ __forceinline__ void run(uint32_t lc, uint32_t lmid, double (&wr)[R], double (&wi)[R], double& ar,
+                                               double& ai) {
+        constexpr int U = C::U;
+        static_assert(C::S == 1 && T % 2 == 0 && U >= 2, "unit-column walk: one lane per chunk, blocks of >= 4");
+        if constexpr (T > 0) {
+            constexpr int J = ctz_c((unsigned)T);            // >= 1
+            if constexpr (J == U - 1) {
+                flip_add<R>(lmid, wr, wi);
+            } else {
+                constexpr bool PLUS = ((T >> (J + 1)) & 1) == 0;
+                flip_static<R, PLUS>(lc + (uint32_t)(J * C::P) * 16u, wr, wi);
+            }
+        }
+        constexpr int SP = ((T >> 1) & 1) ? -1 : 1;
+        term_acc<R, C::K, -SP>(wr, wi, ar, ai);
+        term_acc_shift1<R, C::K, SP>(wr, wi, ar, ai);
+        if constexpr (T + 2 < (1 << U)) InnerStepU<C, T + 2>::run(lc, lmid, wr, wi, ar, ai);
+    }
+};
+
+// One aligned chunk of 2^e ranks (e >= U >= 2) on the unit-column walk: the seed never includes column 0 (its Gray
+// bit is 0 at an aligned start with e >= 2), and the bit-0 flips are replaced by the pairs of InnerStepU.
+template <class C>
+__device__ __forceinline__ void walk_chunk_unit(uint32_t lc, uint32_t lb, uint64_t c, int e, ddc& acc) {
+    constexpr int U = C::U, R = C::R;
+    double wr[R], wi[R];
+    const uint64_t x = ((c ^ (c >> 1)) << e) | ((c & 1ull) << (e - 1));
+    seed_rows<C>(lc, lb, x, e - 1, wr, wi);
+    const uint32_t nblk = 1u << (e - U);
+    const uint32_t cpar = (uint32_t)(c & 1ull);
+    constexpr uint32_t kFoldMask = (U >= kWalkFoldBits) ? 0u : ((1u << (kWalkFoldBits - U)) - 1u);
+    double ar = 0.0, ai = 0.0;
+    for (uint32_t q = 0; q < nblk; q++) {
+        if (q > 0) {
+            const int j = U + __ffs((int)q) - 1;
+            const uint32_t nb = (j + 1 < e) ? ((q >> (j + 1 - U)) & 1u) : cpar;
+            flip_add<R>(lc + (uint32_t)(j * C::P) * 16u + (nb ? C::NEG : 0u), wr, wi);
+        }
+        const uint32_t nbm = (U < e) ? (q & 1u) : cpar;
+        const uint32_t lmid = lc + (uint32_t)((U - 1) * C::P) * 16u + (nbm ? C::NEG : 0u);
+        InnerStepU<C, 0>::run(lc, lmid, wr, wi, ar, ai);
         if (((q + 1) & kFoldMask) == 0 || q + 1 == nblk) {
             acc.re = dd_add_d(acc.re, ar);
             acc.im = dd_add_d(acc.im, ai);
@@ -637,6 +715,9 @@ struct InnerStepC {
 #ifndef PERM_UNIT_K
 #define PERM_UNIT_K 0
 #endif
+#ifndef PERM_UNIT_INTERLEAVE
+#define PERM_UNIT_INTERLEAVE 0
+#endif
 __host__ __device__ constexpr int unit_chains(int n, int k) { return PERM_UNIT_K > 0 ? PERM_UNIT_K : k; }
 
 // Unit-column walk over the pairs (T, T+1), T even, of the inner block: the row sums v hold Gray bit 0 = 0 (column 0
@@ -673,8 +754,12 @@ struct InnerStepCU {
         }
         constexpr int SP = ((T >> 1) & 1) ? -1 : 1;
         constexpr int KU = unit_chains(N, C::K);
-        term_acc<N, KU, -SP>(wr, wi, ar, ai);
-        term_acc_shift1<N, KU, SP>(wr, wi, ar, ai);
+        if constexpr (PERM_UNIT_INTERLEAVE && KU == 4) {
+            pair_acc_interleaved<N, SP>(wr, wi, ar, ai);
+        } else {
+            term_acc<N, KU, -SP>(wr, wi, ar, ai);
+            term_acc_shift1<N, KU, SP>(wr, wi, ar, ai);
+        }
         if constexpr (T + 2 < (1 << U)) InnerStepCU<C, T + 2>::run(P, z, wr, wi, zmid, ar, ai);
     }
 };
