@@ -317,7 +317,7 @@ perm_status_t launch_walk(const perm_c128_t* A, int n, const WalkPlan& p, ddc* i
     // unit-column walk (internal.h walk_unit0): A' = D^{-1} A with column 0 all ones, scale = prod_i a_i0
     std::vector<perm_c128_t> unit;
     perm::ddc scale{};
-    const bool use_unit = p.use_const && h != nullptr && unit0_normalize(h, n, unit, scale);
+    const bool use_unit = p.use_const && h != nullptr && ws_a != nullptr && unit0_normalize(h, n, unit, scale);
     if (use_unit) {
         PERM_CUDA(cudaMemcpyAsync(ws_a, unit.data(), (size_t)n * n * sizeof(double2), cudaMemcpyHostToDevice, s),
                   "cudaMemcpyAsync(A' H2D)");
@@ -598,13 +598,13 @@ perm_status_t perm_c128_chunks(const perm_c128_t* A, int n, int chunk_log2, uint
     const size_t a_bytes = (size_t)n * n * sizeof(double2);
     char* ws = (char*)workspace;
     bool own = false;
-    if (!a_dev) {
-        if (!ws) {
-            PERM_CUDA(perm::malloc_async((void**)&ws, a_bytes, s), "cudaMallocAsync(A)");
-            own = true;
-        } else if (workspace_bytes < a_bytes) {
-            return PERM_E_WORKSPACE;
-        }
+    if (!ws) {
+        // (a device matrix needs scratch only for the unit-column walk's normalised copy)
+        PERM_CUDA(perm::malloc_async((void**)&ws, a_bytes, s), "cudaMallocAsync(A)");
+        own = true;
+    } else if (workspace_bytes < a_bytes) {
+        if (!a_dev) return PERM_E_WORKSPACE;
+        ws = nullptr;                                       // device A, scratch too small: walk A as given
     }
     uint32_t launches = 0;
     // the chunk walk always checks A on the host (a device matrix is copied back once): it has no

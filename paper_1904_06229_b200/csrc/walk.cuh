@@ -718,6 +718,9 @@ struct InnerStepC {
 #ifndef PERM_UNIT_INTERLEAVE
 #define PERM_UNIT_INTERLEAVE 0
 #endif
+#ifndef PERM_UNIT_KP
+#define PERM_UNIT_KP 0
+#endif
 __host__ __device__ constexpr int unit_chains(int n, int k) { return PERM_UNIT_K > 0 ? PERM_UNIT_K : k; }
 
 // Unit-column walk over the pairs (T, T+1), T even, of the inner block: the row sums v hold Gray bit 0 = 0 (column 0
@@ -754,10 +757,11 @@ struct InnerStepCU {
         }
         constexpr int SP = ((T >> 1) & 1) ? -1 : 1;
         constexpr int KU = unit_chains(N, C::K);
+        constexpr int KP = PERM_UNIT_KP > 0 ? PERM_UNIT_KP : KU;   // development: chains of the plain product
         if constexpr (PERM_UNIT_INTERLEAVE && KU == 4) {
             pair_acc_interleaved<N, SP>(wr, wi, ar, ai);
         } else {
-            term_acc<N, KU, -SP>(wr, wi, ar, ai);
+            term_acc<N, KP, -SP>(wr, wi, ar, ai);
             term_acc_shift1<N, KU, SP>(wr, wi, ar, ai);
         }
         if constexpr (T + 2 < (1 << U)) InnerStepCU<C, T + 2>::run(P, z, wr, wi, zmid, ar, ai);

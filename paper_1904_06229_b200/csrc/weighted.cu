@@ -33,6 +33,12 @@ namespace perm {
 #endif
 constexpr bool kWgtOrdered = PERM_WGT_ORDERED != 0;
 
+// unit sweep column (normalised rows); 0: every problem walked as given
+#ifndef PERM_WGT_UNIT
+#define PERM_WGT_UNIT 1
+#endif
+constexpr bool kWgtUnit = PERM_WGT_UNIT != 0;
+
 // unroll factor of the sweep loop (1: rolled)
 #ifndef PERM_WGT_UNROLL
 #define PERM_WGT_UNROLL 1
@@ -51,7 +57,7 @@ struct WgtCfg {
 #ifndef PERM_WGT_REG_EXTRA
     // working-set registers beyond the 4n row sums (0 spill bytes at every order, tools/spills.py, with the
     // unrolled sweeps of m_s <= kWgtSpecMax)
-    static constexpr int EXTRA = (N == 18 || N == 23 || N == 24) ? 160 : 128;
+    static constexpr int EXTRA = ((N >= 14 && N <= 18) || N == 21 || N == 23 || N == 24) ? 160 : 128;
 #else
     static constexpr int EXTRA = PERM_WGT_REG_EXTRA;
 #endif
@@ -86,7 +92,8 @@ constexpr bool kWgtSpecialise = PERM_WGT_SPECIALISE != 0;
 #define PERM_WGT_SPEC_MAX 2
 #endif
 constexpr int kWgtSpecMax = PERM_WGT_SPEC_MAX;   // largest m_s with an unrolled sweep
-template <int N, int MS>
+// UNIT: the sweep column was normalised to 1 (its flips change the real parts only: n DADD instead of 2n)
+template <int N, int MS, bool UNIT>
 __device__ __forceinline__ void wgt_sweep(int ms, double sc2, const double* tsw, int& f1, int d1, uint32_t step,
                                           double (&wr)[N], double (&wi)[N], double& ar, double& ai) {
     const int m = MS >= 0 ? MS : ms;
@@ -100,7 +107,13 @@ __device__ __forceinline__ void wgt_sweep(int ms, double sc2, const double* tsw,
         xi *= wt;
         fused_acc<+1>(xr, xi, yr, yi, ar, ai);
         if (j < m) {
-            flip_add<N>(step, wr, wi);
+            if constexpr (UNIT) {
+                const double dz = (double)d1;
+#pragma unroll
+                for (int i = 0; i < N; i++) wr[i] += dz;
+            } else {
+                flip_add<N>(step, wr, wi);
+            }
             f1 += d1;
         }
     }
@@ -215,6 +228,50 @@ __global__ void __launch_bounds__(WgtCfg<N>::NT, WgtCfg<N>::MINB)
             }
             continue;
         }
+        // unit sweep column: rows divided by their entry in the sweep column s (per(A) is multilinear in
+        // the rows; scale = prod_i c_is in double-double, a fixed shuffle tree), so the fast flips change real parts
+        // only; a problem with a zero (or relatively tiny) entry in column s is walked as given
+        bool unit = false;
+        __shared__ ddc s_uscale;
+        if constexpr (kWgtUnit) {
+            __syncwarp();
+            ddc f;
+            f.re = dd{1.0, 0.0};
+            f.im = dd{0.0, 0.0};
+            bool okl = true;
+            if (lane < N) {
+                const double2 a = col[s * N + lane];
+                const double m = fmax(fabs(a.x), fabs(a.y));
+                double rmax = 0.0;
+                for (int k = 0; k < R; k++) rmax = fmax(rmax, fabs(col[k * N + lane].x) + fabs(col[k * N + lane].y));
+                okl = m > 0.0 && rmax / m <= 1e100;
+                f.re = dd{a.x, 0.0};
+                f.im = dd{a.y, 0.0};
+            }
+            unit = __all_sync(0xffffffffu, okl);
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) f = ddc_mul(f, shfl_down_ddc(f, off));
+            if (lane == 0) s_uscale = f;
+            if (unit) {
+                for (int k = lane; k < N * R; k += 32) {                  // col[k] = a_{i, j}, k = j N + i
+                    const int j = k / N, i = k - j * N;
+                    if (j == s) continue;
+                    const double2 a0 = col[s * N + i];
+                    const double m = fmax(fabs(a0.x), fabs(a0.y));
+                    const double sr = a0.x / m, si = a0.y / m, d2 = sr * sr + si * si;
+                    const double ir = sr / (d2 * m), ii = -si / (d2 * m);
+                    const double2 a = col[k];
+                    col[k] = make_double2(a.x * ir - a.y * ii, a.x * ii + a.y * ir);
+                }
+                __syncwarp();
+                for (int i = lane; i < N; i += 32) {
+                    col[s * N + i] = make_double2(1.0, 0.0);
+                    negs[i] = make_double2(-1.0, 0.0);
+                    if (s2 >= 0) negs2[i] = make_double2(-col[s2 * N + i].x, -col[s2 * N + i].y);
+                }
+            }
+            __syncwarp();
+        }
         for (int k = lane; k < R * (N + 1); k += 32) {
             const int d = k / (N + 1), f = k - d * (N + 1);
             const int m = mb[d];
@@ -285,12 +342,14 @@ __global__ void __launch_bounds__(WgtCfg<N>::NT, WgtCfg<N>::MINB)
                     const uint32_t step = fwd1 ? cs : nbase;
                     const int d1 = fwd1 ? 1 : -1;
                     // the fast sweep, unrolled for the common small multiplicities (warp-uniform switch)
-                    switch (kWgtSpecialise && N <= 24 && ms <= kWgtSpecMax ? ms : -1) {
-                        case 1: wgt_sweep<N, 1>(ms, sc2, tsw, f1, d1, step, wr, wi, ar, ai); break;
-                        case 2: wgt_sweep<N, 2>(ms, sc2, tsw, f1, d1, step, wr, wi, ar, ai); break;
-                        case 3: wgt_sweep<N, (kWgtSpecMax >= 3 ? 3 : -1)>(ms, sc2, tsw, f1, d1, step, wr, wi, ar, ai); break;
-                        case 4: wgt_sweep<N, (kWgtSpecMax >= 4 ? 4 : -1)>(ms, sc2, tsw, f1, d1, step, wr, wi, ar, ai); break;
-                        default: wgt_sweep<N, -1>(ms, sc2, tsw, f1, d1, step, wr, wi, ar, ai); break;
+                    const int sw = (kWgtSpecialise && N <= 24 && ms <= kWgtSpecMax ? ms : -1) + (unit ? 16 : 0);
+                    switch (sw) {
+                        case 1: wgt_sweep<N, 1, false>(ms, sc2, tsw, f1, d1, step, wr, wi, ar, ai); break;
+                        case 2: wgt_sweep<N, 2, false>(ms, sc2, tsw, f1, d1, step, wr, wi, ar, ai); break;
+                        case 17: wgt_sweep<N, 1, true>(ms, sc2, tsw, f1, d1, step, wr, wi, ar, ai); break;
+                        case 18: wgt_sweep<N, 2, true>(ms, sc2, tsw, f1, d1, step, wr, wi, ar, ai); break;
+                        case 15: wgt_sweep<N, -1, true>(ms, sc2, tsw, f1, d1, step, wr, wi, ar, ai); break;
+                        default: wgt_sweep<N, -1, false>(ms, sc2, tsw, f1, d1, step, wr, wi, ar, ai); break;
                     }
                     fwd1 = !fwd1;
                     if (r < ms2) {
@@ -323,6 +382,7 @@ __global__ void __launch_bounds__(WgtCfg<N>::NT, WgtCfg<N>::MINB)
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) acc = ddc_add(acc, shfl_down_ddc(acc, off));
         if (lane == 0) {
+            if (unit) acc = ddc_mul(acc, s_uscale);                       // back to the units of the problem
             const double f = (N & 1) ? -1.0 : 1.0;
             const double re = (acc.re.hi + acc.re.lo) * f;
             const double im = (acc.im.hi + acc.im.lo) * f;

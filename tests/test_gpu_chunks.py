@@ -247,3 +247,26 @@ def test_cfg5_self_consistency_transpose_and_permutation():
     v_p, _ = _sharded(PAQ, 3, 2)
     for x, y in ((v_a, v_t), (v_a, v_p), (v_t, v_p)):
         assert pins.scaled_error(x, y, A) <= 1e-11, (v_a, v_t, v_p)
+
+
+def test_unit_column_walk_device_and_host_matrix_bit_identical():
+    """The unit-column walk normalises A on the host for every call: a device-resident matrix
+    without a workspace (scratch allocated inside), with one, and the host matrix give the same bits; a matrix
+    with a zero in column 0 takes the plain walk and still matches the oracle's App. A span."""
+    import torch
+    for n in (33, 44):
+        A = inputs.complex_gaussian((n, n), 7700 + n)
+        b = pb.chunk_log2(n)
+        c0, c1 = 5, 5 + 300
+        ref = pb.perm_c128_chunks(A, c0, c1).cpu().numpy()
+        Ad = torch.from_numpy(A).cuda()
+        assert np.array_equal(pb.perm_c128_chunks(Ad, c0, c1).cpu().numpy(), ref)
+        ws = torch.empty(n * n * 16, dtype=torch.uint8, device="cuda")
+        assert np.array_equal(pb.perm_c128_chunks(Ad, c0, c1, workspace=ws).cpu().numpy(), ref)
+    n = 33
+    A = inputs.complex_gaussian((n, n), 7733)
+    A[4, 0] = 0.0
+    raw = _span_raw(A, 0, 4, 10)
+    ref = oracle.subpermanent(A, 0, 4 << 10)
+    scale = max(abs(ref.value), pins.range_scale(A, 4 << 10))
+    assert abs(raw.value - ref.value) <= 1e-12 * scale
