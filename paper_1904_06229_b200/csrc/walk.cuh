@@ -719,7 +719,7 @@ struct InnerStepC {
 #define PERM_UNIT_INTERLEAVE 0
 #endif
 #ifndef PERM_UNIT_KP
-#define PERM_UNIT_KP 0
+#define PERM_UNIT_KP 2
 #endif
 __host__ __device__ constexpr int unit_chains(int n, int k) { return PERM_UNIT_K > 0 ? PERM_UNIT_K : k; }
 

@@ -127,7 +127,11 @@ __device__ __forceinline__ void wgt_sweep(int ms, double sc2, const double* tsw,
 constexpr int kWgtBuckets = 256;                  // eighth-octave size classes, 2^0 .. 2^32
 __global__ void __launch_bounds__(1024) wgt_order_kernel(const int32_t* __restrict__ mult, int R, int64_t B,
                                                          int64_t* __restrict__ order) {
-    __shared__ unsigned long long cnt[kWgtBuckets];
+    // stable counting sort by one block: warp w owns the contiguous problems [w B / 32, (w + 1) B / 32); per-warp
+    // class counts, an exclusive scan over (class, warp), then every warp places its problems in index order
+    __shared__ uint32_t cnt[32][kWgtBuckets];                // per-warp counts, then per-warp cursors
+    __shared__ unsigned long long tot[kWgtBuckets];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     auto bucket = [&](int64_t b) {
         double sz = 1.0;
         for (int k = 0; k < R; k++) {
@@ -138,34 +142,46 @@ __global__ void __launch_bounds__(1024) wgt_order_kernel(const int32_t* __restri
         e = e < 0 ? 0 : (e >= kWgtBuckets ? kWgtBuckets - 1 : e);
         return kWgtBuckets - 1 - e;                       // largest first
     };
-    for (int k = threadIdx.x; k < kWgtBuckets; k += blockDim.x) cnt[k] = 0;
+    for (int k = threadIdx.x; k < 32 * kWgtBuckets; k += blockDim.x) (&cnt[0][0])[k] = 0;
     __syncthreads();
-    for (int64_t b = threadIdx.x; b < B; b += blockDim.x) atomicAdd(&cnt[bucket(b)], 1ull);
+    const int64_t b0 = B * w / 32, b1 = B * (w + 1) / 32;
+    for (int64_t b = b0 + lane; b < b1; b += 32) atomicAdd(&cnt[w][bucket(b)], 1u);
+    __syncthreads();
+    for (int k = threadIdx.x; k < kWgtBuckets; k += blockDim.x) {
+        unsigned long long t = 0;
+        for (int v = 0; v < 32; v++) t += cnt[v][k];
+        tot[k] = t;
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
         unsigned long long run = 0;
-        for (int k = 0; k < kWgtBuckets; k++) { const unsigned long long c = cnt[k]; cnt[k] = run; run += c; }
+        for (int k = 0; k < kWgtBuckets; k++) { const unsigned long long c = tot[k]; tot[k] = run; run += c; }
     }
     __syncthreads();
-    // stable placement (index order inside a class, so the schedule is the same on every run): warp 0 walks the
-    // problems 32 at a time; lanes of one class take consecutive slots in lane order
-    if (threadIdx.x < 32) {
-        const int lane = threadIdx.x;
-        for (int64_t b0 = 0; b0 < B; b0 += 32) {
-            const int64_t b = b0 + lane;
-            const int key = b < B ? bucket(b) : -1 - lane;
-            const unsigned peers = __match_any_sync(0xffffffffu, key);
-            const int before = __popc(peers & ((1u << lane) - 1u));
-            const int leader = __ffs(peers) - 1;
-            unsigned long long base = 0;
-            if (b < B && lane == leader) base = cnt[key];
-            base = __shfl_sync(0xffffffffu, base, leader);
-            if (b < B) order[base + before] = b;
-            __syncwarp();
-            if (b < B && lane == leader) cnt[key] = base + __popc(peers);
-            __syncwarp();
-        }
+    for (int k = threadIdx.x; k < kWgtBuckets; k += blockDim.x) {
+        unsigned long long run = tot[k];
+        for (int v = 0; v < 32; v++) { const uint32_t c = cnt[v][k]; cnt[v][k] = (uint32_t)run; run += c; }
     }
+    __syncthreads();
+    // (32-bit cursors: the launch sorts fewer than 2^31 problems; larger batches keep the input order)
+    for (int64_t c0 = b0; c0 < b1; c0 += 32) {
+        const int64_t b = c0 + lane;
+        const int key = b < b1 ? bucket(b) : -1 - lane;
+        const unsigned peers = __match_any_sync(0xffffffffu, key);
+        const int before = __popc(peers & ((1u << lane) - 1u));
+        const int leader = __ffs(peers) - 1;
+        uint32_t base = 0;
+        if (b < b1 && lane == leader) base = cnt[w][key];
+        base = __shfl_sync(0xffffffffu, base, leader);
+        if (b < b1) order[base + before] = b;
+        __syncwarp();
+        if (b < b1 && lane == leader) cnt[w][key] = base + (uint32_t)__popc(peers);
+        __syncwarp();
+    }
+}
+
+__global__ void wgt_identity_order_kernel(int64_t B, int64_t* __restrict__ order) {
+    for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < B; b += (int64_t)gridDim.x * blockDim.x) order[b] = b;
 }
 
 template <int N>
@@ -414,7 +430,8 @@ cudaError_t weighted_launch_t(const double2* C, const int32_t* mult, int R, int6
     int64_t* order = (int64_t*)((char*)next + 16);
     err = cudaMemsetAsync(next, 0, sizeof(unsigned long long), st);
     if (err == cudaSuccess && ordered) {
-        wgt_order_kernel<<<1, 1024, 0, st>>>(mult, R, B, order);
+        if (B < (1ll << 31)) wgt_order_kernel<<<1, 1024, 0, st>>>(mult, R, B, order);
+        else                 wgt_identity_order_kernel<<<1024, 256, 0, st>>>(B, order);   // (32-bit cursors)
         err = cudaGetLastError();
     }
     if (err == cudaSuccess) {

@@ -16,7 +16,10 @@ per = torch.empty(C.shape[0], dtype=torch.complex128, device="cuda")
 pb.perm_c128_weighted_batched(Cd, Md, per=per, want_abs2=False)
 s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 best = 1e9
+flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda") if os.environ.get("FLUSH") == "1" else None
 for _ in range(5):
+    if flush is not None:
+        flush.fill_(1)                     # evict L2 (as bench.py does between steps)
     s.record()
     pb.perm_c128_weighted_batched(Cd, Md, per=per, want_abs2=False)
     e.record()
