@@ -960,7 +960,7 @@ def run_ours(args):
             achieved = fl / (dev_ms / K * 1e-3) / 1e12
             out["roofline"] = {"bound": "alu", "achieved": achieved, "peak": nominal, "unit": "TFLOP/s",
                                "frac": achieved / nominal, "traffic": ncu_traffic(cfg),
-                               "kernel": "batched_kernel<n> x4 (unit-column walk for n >= 11; FP64 vector pipe)",
+                               "kernel": "batched_kernel<n> x4 (unit-column walk for n >= 14; FP64 vector pipe)",
                                "algorithmic": "8n flops per Gray term x 2^(n-1) terms x 10^5 per n",
                                "peak_measured_probe": peak_meas}
         else:

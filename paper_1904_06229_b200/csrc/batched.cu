@@ -59,7 +59,7 @@ __global__ void __launch_bounds__(BatCfg<N>::NT) batched_kernel(const double2* _
     // unit-column walk (walk.cuh InnerStepU) when a warp walks one matrix (n >= 11): rows divided by their column-0
     // entry, scale = prod_i a_i0 in double-double (a fixed shuffle tree over the rows' lanes); a matrix with a zero (or
     // relatively tiny) column-0 entry is walked as given
-    constexpr bool UNIT = kBatchedUnit && C::G == 1 && C::E >= WCfg<N, 1>::U && WCfg<N, 1>::K >= 2;
+    constexpr bool UNIT = kBatchedUnit && N >= 14 && C::G == 1 && C::E >= WCfg<N, 1>::U && WCfg<N, 1>::K >= 2;
     [[maybe_unused]] bool unit = false;
     [[maybe_unused]] ddc scale;
     if constexpr (UNIT) {
