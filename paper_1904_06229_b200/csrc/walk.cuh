@@ -266,28 +266,6 @@ __device__ __forceinline__ void two_factors_shift1(const double (&wr)[R], const 
     }
 }
 
-// acc += SP (prod (w_i + 1) - prod w_i) with the two products' chains interleaved row by row (K = 4 each: eight
-// independent chains in flight; development variant PERM_UNIT_INTERLEAVE)
-template <int R, int SP>
-__device__ __forceinline__ void pair_acc_interleaved(const double (&wr)[R], const double (&wi)[R], double& ar, double& ai) {
-    double r0 = wr[0], i0 = wi[0], r1 = wr[1], i1 = wi[1], r2 = wr[2], i2 = wi[2], r3 = wr[3], i3 = wi[3];
-    double s0 = wr[0] + 1.0, j0 = wi[0], s1 = wr[1] + 1.0, j1 = wi[1];
-    double s2 = wr[2] + 1.0, j2 = wi[2], s3 = wr[3] + 1.0, j3 = wi[3];
-#pragma unroll
-    for (int i = 4; i < R; i++) {
-        if ((i & 3) == 0)      { cmul2(r0, i0, wr[i], wi[i]); cmul_shift1(s0, j0, wr[i], wi[i]); }
-        else if ((i & 3) == 1) { cmul2(r1, i1, wr[i], wi[i]); cmul_shift1(s1, j1, wr[i], wi[i]); }
-        else if ((i & 3) == 2) { cmul2(r2, i2, wr[i], wi[i]); cmul_shift1(s2, j2, wr[i], wi[i]); }
-        else                   { cmul2(r3, i3, wr[i], wi[i]); cmul_shift1(s3, j3, wr[i], wi[i]); }
-    }
-    cmul2(r0, i0, r1, i1);
-    cmul2(s0, j0, s1, j1);
-    cmul2(r2, i2, r3, i3);
-    cmul2(s2, j2, s3, j3);
-    fused_acc<-SP>(r0, i0, r2, i2, ar, ai);
-    fused_acc<SP>(s0, j0, s2, j2, ar, ai);
-}
-
 // acc += SIGN * prod_i (w_i + 1)
 template <int R, int K, int SIGN>
 __device__ __forceinline__ void term_acc_shift1(const double (&wr)[R], const double (&wi)[R], double& ar, double& ai) {
@@ -711,18 +689,6 @@ struct InnerStepC {
     }
 };
 
-// product chains per factor of the unit-column walk (development: PERM_UNIT_K overrides the plain walk's K)
-#ifndef PERM_UNIT_K
-#define PERM_UNIT_K 0
-#endif
-#ifndef PERM_UNIT_INTERLEAVE
-#define PERM_UNIT_INTERLEAVE 0
-#endif
-#ifndef PERM_UNIT_KP
-#define PERM_UNIT_KP 2
-#endif
-__host__ __device__ constexpr int unit_chains(int n, int k) { return PERM_UNIT_K > 0 ? PERM_UNIT_K : k; }
-
 // Unit-column walk over the pairs (T, T+1), T even, of the inner block: the row sums v hold Gray bit 0 = 0 (column 0
 // is all ones and never added), term T + (bit 0) reads v + 1.  Gray bit 0 of rank T is bit 1 of T, so the pair is
 // s_T (prod (v + 1) - prod v) with s_T = +1 if bit 1 of T is 0, else -1 (signs (-1)^{r+1}, App. A).
@@ -756,14 +722,10 @@ struct InnerStepCU {
             }
         }
         constexpr int SP = ((T >> 1) & 1) ? -1 : 1;
-        constexpr int KU = unit_chains(N, C::K);
-        constexpr int KP = PERM_UNIT_KP > 0 ? PERM_UNIT_KP : KU;   // development: chains of the plain product
-        if constexpr (PERM_UNIT_INTERLEAVE && KU == 4) {
-            pair_acc_interleaved<N, SP>(wr, wi, ar, ai);
-        } else {
-            term_acc<N, KP, -SP>(wr, wi, ar, ai);
-            term_acc_shift1<N, KU, SP>(wr, wi, ar, ai);
-        }
+        // the shifted product keeps the walk's K chains; the plain one two (n = 44: 0.6650 -> 0.6670; interleaving
+        // the two products' chains lost the uniform-register columns, profiles/round2_unit_column_rates.txt)
+        term_acc<N, (C::K < 2 ? C::K : 2), -SP>(wr, wi, ar, ai);
+        term_acc_shift1<N, C::K, SP>(wr, wi, ar, ai);
         if constexpr (T + 2 < (1 << U)) InnerStepCU<C, T + 2>::run(P, z, wr, wi, zmid, ar, ai);
     }
 };
