@@ -6,7 +6,10 @@ of the Glynn sum in exact Python integers on small matrices -- independent of th
 * quad identity (+-1 entries): after negating rows so that the bit-0 column is all +1, the terms of an aligned quad
   of ranks sum to d [M(0) (P(2) + P(-2)) - P(0) (M(2) + M(-2))] over the classes of the bit-1 column, d = +1 iff
   bit 2 of the rank is set; and per(D A Q) = sign * per(A) for the row negations D and the column negation Q
-  (sign = the product of the negations).
+  (sign = the product of the negations);
+* unit-column identities (complex entries, exact Gaussian rationals): per(A) = prod_i a_i0 per(A') for
+  A' = D^{-1} A, and on A' the terms of ranks 2q, 2q+1 sum to s_q (prod (v + 1) - prod v) with v the row sums at
+  Gray bit 0 = 0 -- the algebra of the unit-column walk.
 
 The Glynn sum of App. A / SURVEY S-1: Sum = sum_r (-1)^{r+1} prod_i g_i(gray r), g_i = a_{i,n-1} + sum_{j<n-1}
 delta_j a_ij with delta_j = +1 iff bit j of gray r is set; per = (-1)^n Sum / 2^{n-1}.
@@ -94,3 +97,90 @@ def test_quad_identity_pm1(n, seed):
         assert quad == direct
         total += quad
     assert (-1) ** n * total == per_brute(A) * 2 ** (n - 1)
+
+
+# ---- the unit-column walk, in exact Gaussian rationals
+
+from fractions import Fraction  # noqa: E402
+
+
+class GQ:
+    """Exact complex rational a + bi."""
+    __slots__ = ("a", "b")
+
+    def __init__(self, a, b=0):
+        self.a, self.b = Fraction(a), Fraction(b)
+
+    def __add__(self, o):
+        return GQ(self.a + o.a, self.b + o.b)
+
+    def __sub__(self, o):
+        return GQ(self.a - o.a, self.b - o.b)
+
+    def __mul__(self, o):
+        return GQ(self.a * o.a - self.b * o.b, self.a * o.b + self.b * o.a)
+
+    def __truediv__(self, o):
+        d = o.a * o.a + o.b * o.b
+        return GQ((self.a * o.a + self.b * o.b) / d, (self.b * o.a - self.a * o.b) / d)
+
+    def __eq__(self, o):
+        return self.a == o.a and self.b == o.b
+
+
+def gq_prod(xs):
+    p = GQ(1)
+    for x in xs:
+        p = p * x
+    return p
+
+
+def gq_per(M):
+    n = len(M)
+    tot = GQ(0)
+    for s in itertools.permutations(range(n)):
+        tot = tot + gq_prod(M[i][s[i]] for i in range(n))
+    return tot
+
+
+def gq_w(M, r):
+    """App. A row sums w_i(gray r) = a_{i,n-1} - 1/2 sum_j a_ij + sum_{j<n-1, x_j=1} a_ij."""
+    n = len(M)
+    x = gray(r)
+    out = []
+    for i in range(n):
+        w = M[i][n - 1]
+        for j in range(n):
+            w = w - M[i][j] * GQ(Fraction(1, 2))
+        for j in range(n - 1):
+            if (x >> j) & 1:
+                w = w + M[i][j]
+        out.append(w)
+    return out
+
+
+@pytest.mark.parametrize("n,seed", [(4, 31), (5, 32), (6, 33)])
+def test_unit_column_identities(n, seed):
+    rng = np.random.default_rng(seed)
+    A = [[GQ(int(rng.integers(-3, 4)), int(rng.integers(-3, 4))) for _ in range(n)] for _ in range(n)]
+    for i in range(n):
+        if A[i][0] == GQ(0):
+            A[i][0] = GQ(1, 1)
+    # A' = D^-1 A: column 0 all ones; per(A) = prod_i a_i0 * per(A')
+    Ap = [[A[i][j] / A[i][0] for j in range(n)] for i in range(n)]
+    assert all(Ap[i][0] == GQ(1) for i in range(n))
+    assert gq_per(A) == gq_prod(A[i][0] for i in range(n)) * gq_per(Ap)
+    # the pairs of the walk: ranks 2q, 2q+1 read v (Gray bit 0 = 0) and v + 1, signs (-1)^{r+1}
+    S_terms, S_pairs = GQ(0), GQ(0)
+    for r in range(1 << (n - 1)):
+        t = gq_prod(gq_w(Ap, r))
+        S_terms = S_terms + t if r & 1 else S_terms - t
+    for q in range(1 << (n - 2)):
+        r = 2 * q
+        v = gq_w(Ap, r) if gray(r) & 1 == 0 else [w - GQ(1) for w in gq_w(Ap, r)]
+        sp = 1 if ((r >> 1) & 1) == 0 else -1
+        d = gq_prod(w + GQ(1) for w in v) - gq_prod(v)
+        S_pairs = S_pairs + d if sp > 0 else S_pairs - d
+    assert S_pairs == S_terms
+    # App. A: per = 2 (-1)^n S
+    assert gq_per(Ap) == GQ(2 * (-1) ** n) * S_terms
