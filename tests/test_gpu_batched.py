@@ -138,3 +138,16 @@ def test_cfg2_full_batch_samples(torch, golden_dir, n):
     expect = math.exp(math.lgamma(n + 1) + math.lgamma(m) - math.lgamma(m + n))
     se = np.std(abs2) / np.sqrt(len(abs2))
     assert abs(np.mean(abs2) - expect) < 6 * se, (np.mean(abs2), expect, se)
+
+
+@pytest.mark.parametrize("n", [14, 16, 20])
+def test_unit_column_walk_fallbacks(torch, n):
+    # the unit-column walk normalises each matrix by its column 0; a matrix with a zero there, one
+    # with a column-0 entry 1e-120 times its row's other entries, and one with a scaled row take the plain walk or
+    # the normalised one -- all within the north-star bound of the oracle
+    A = inputs.complex_gaussian((4, n, n), 900 + n)
+    A[0, 3, 0] = 0.0
+    A[1, 5, 0] = 1e-121 * A[1, 5, 0]
+    A[2, 2, :] *= 1e30
+    ref = np.array([oracle.permanent_hr(A[b]).value for b in range(4)])
+    _check_batch(torch, A, ref)

@@ -261,3 +261,23 @@ def test_cfg5_subranges(golden_dir):
         assert abs(got - ref) <= 1e-12 * max(abs(ref), pins.range_scale(A, rr["k1"] - rr["k0"]))
 
 # The n = 44 block-diagonal full walk (P7) runs on the bench's path in tests/test_gpu_chunks.py.
+
+
+@pytest.mark.parametrize("n", [32, 44])
+def test_unit_column_walk_scale_and_fallback(n):
+    # the unit-column walk: rows of very different scale (the normalisation's product of the column-0
+    # entries spans 1e-200 .. 1e200) and a column-0 entry 1e-120 times its row (the plain walk) -- App. A span sums
+    # against the oracle within the range bar
+    A = inputs.complex_gaussian((n, n), 4400 + n)
+    A[1, :] *= 1e-100
+    A[2, :] *= 1e100
+    B = A.copy()
+    B[7, 0] = 1e-121 * B[7, 0]
+    N = 1 << (n - 1)
+    for M in (A, B):
+        for k0 in (0, N // 3):
+            k1 = k0 + (1 << 20)
+            got = pb.perm_c128_range(M, k0, k1).value
+            ref = oracle.subpermanent(M, k0, k1 - k0).value
+            scale = max(abs(ref), pins.range_scale(M, k1 - k0))
+            assert abs(got - ref) <= 1e-12 * scale, (n, k0, got, ref)
