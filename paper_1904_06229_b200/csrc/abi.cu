@@ -853,6 +853,8 @@ perm_status_t perm_c128_sparse(const perm_c128_t* A, int n, perm_c128_t* out_hos
         outer *= (1ull << L.ssz[l]) - 1ull;
     }
     L.outer = outer;
+    for (int i = 0; i < n; i++) L.row[i] = i;
+    L.pair = 0;
     int dev = 0, sms = 0, bps = 0;
     PERM_CUDA(cudaGetDevice(&dev), "cudaGetDevice");
     PERM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "cudaDeviceGetAttribute");
@@ -868,9 +870,49 @@ perm_status_t perm_c128_sparse(const perm_c128_t* A, int n, perm_c128_t* out_hos
         if (e > L.nt) e = L.nt;
         if (e > 30) e = 30;
         if (e < U) e = U;
+        if (const char* f = getenv("PERM_FORCE_CHUNK_LOG2")) {   // test / profiling override, as in choose_b
+            const int fe = atoi(f);
+            if (fe >= U && fe <= L.nt && fe <= 30) e = fe;
+        }
     }
     L.e = e;
     L.chunks = 1ull << (L.nt - e);
+    // shared-rows pair walk (sparse.cuh InnerStepCS): on the constant-bank path (e > U), when some T column has at
+    // most kSparsePairRows nonzero rows: that column becomes T slot 0 (the walk's bit-0 column; any order of the T
+    // columns enumerates the same sets) and the rows are ordered so that its nonzero rows come last (per(PA) =
+    // per(A)).  PERM_SPARSE_PAIR=0 keeps the plain walk.
+    {
+        const char* ev = getenv("PERM_SPARSE_PAIR");
+        const bool allow = !(ev && ev[0] == '0');
+        if (allow && perm::sparse_pair_path(n) && e > U) {
+            int best = -1, bcnt = n + 1;
+            for (int q = 0; q < L.nt; q++) {
+                int cnt = 0;
+                for (int r = 0; r < n; r++) {
+                    const perm_c128_t z = Ah[(size_t)r * n + L.col[q]];
+                    cnt += (z.re != 0.0 || z.im != 0.0);
+                }
+                if (cnt < bcnt) { bcnt = cnt; best = q; }
+            }
+            if (best >= 0 && bcnt <= perm::kSparsePairRows) {
+                std::swap(L.col[0], L.col[best]);
+                const int c0 = L.col[0];
+                int lo = 0, hi = n - perm::kSparsePairRows;
+                std::vector<int> zero_rows, nz_rows;
+                for (int r = 0; r < n; r++) {
+                    const perm_c128_t z = Ah[(size_t)r * n + c0];
+                    ((z.re != 0.0 || z.im != 0.0) ? nz_rows : zero_rows).push_back(r);
+                }
+                // positions n-M .. n-1: the nonzero rows of c0, then zero rows to fill (they give equal factors)
+                for (int r : nz_rows) L.row[hi++] = r;
+                size_t k = 0;
+                for (; lo < n - perm::kSparsePairRows; lo++) L.row[lo] = zero_rows[k++];
+                for (; hi < n; hi++) L.row[hi] = zero_rows[k++];
+                L.pair = 1;
+            }
+        }
+    }
+    I.pair_rows = L.pair ? perm::kSparsePairRows : 0;
     const uint64_t items = L.outer * L.chunks;
     const uint64_t bthreads = (uint64_t)perm::walk_block_threads(n);
     uint64_t grid = (items + bthreads - 1) / bthreads;

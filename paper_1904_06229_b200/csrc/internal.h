@@ -205,6 +205,18 @@ cudaError_t batched_launch(const double2* A, int n, int64_t B, double2* per, dou
 // sparse.cuh / sparse_inst.cu (App. B restricted enumeration), n <= kMaxSparseN
 constexpr int kMaxSparseN = 48;
 constexpr int kSparseMaxD = 64;
+// shared-rows pair walk: the T walk's bit-0 column may have at most this many nonzero rows
+constexpr int kSparsePairRows = 4;
+#ifndef PERM_SPARSE_CONST
+#define PERM_SPARSE_CONST 1
+#endif
+// orders of the constant-bank sparse kernel (sparse.cuh sparse_kernel_c; PERM_SPARSE_CONST=2: every order)
+__host__ __device__ constexpr bool sparse_const_path(int n) {
+    return PERM_SPARSE_CONST == 2 ? true
+         : PERM_SPARSE_CONST == 1 ? ((n >= 17 && n <= 33 && n != 24) || n == 47 || n == 48) : false;
+}
+// ... and of its shared-rows pair walk (InnerStepCS: the product of n - kSparsePairRows >= 4 rows in two chains)
+__host__ __device__ constexpr bool sparse_pair_path(int n) { return sparse_const_path(n) && n >= kSparsePairRows + 8; }
 struct SparseLaunch {
     const double2* A_dev;   // device, row-major n x n
     ddc* partials;          // device, grid entries
@@ -212,6 +224,9 @@ struct SparseLaunch {
     uint64_t chunks;        // T-walk chunks per outer combination
     int e, nt, d, n, grid;
     int col[64];            // permuted column order: T columns, then S_1, S_2, ...
+    int row[64];            // row order (position i holds row row[i] of A; the identity unless pair)
+    int pair;               // shared-rows pair walk (sparse.cuh): T slot 0's nonzero rows are the last
+                            // kSparsePairRows positions
     int soff[kSparseMaxD];  // first slot of S_l
     int ssz[kSparseMaxD];   // |S_l|
     const double2* A_host;  // host, row-major n x n (inner T columns for the constant-bank walk)

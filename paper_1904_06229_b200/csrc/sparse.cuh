@@ -29,6 +29,7 @@ struct SparseParams {   // kernel-parameter copy of SparseLaunch
     int32_t nt;                   // |T|
     int32_t d;                    // number of S sets
     int32_t col[64];              // permuted column order: T columns, then S_1, S_2, ...
+    int32_t row[64];              // row order: position i holds row row[i] of A
     int32_t soff[kSparseMaxD];    // slot of S_l's first column (in the permuted order)
     int32_t ssz[kSparseMaxD];     // |S_l|
 };
@@ -39,13 +40,7 @@ struct SparseParams {   // kernel-parameter copy of SparseLaunch
 // the end walk a valid item and drop it) and e > U; the e <= U case keeps the shared-memory walk.
 // Orders for which ptxas keeps those loads on the uniform datapath (LDCU -> DADD R, R, UR; scanned with
 // PERM_SPARSE_CONST=2, guarded by tests/test_abi_cpu.py); n = 48: 4.96e10 -> 5.55e10 sets/s.
-#ifndef PERM_SPARSE_CONST
-#define PERM_SPARSE_CONST 1
-#endif
-__host__ __device__ constexpr bool sparse_const_path(int n) {
-    return PERM_SPARSE_CONST == 2 ? true
-         : PERM_SPARSE_CONST == 1 ? ((n >= 17 && n <= 33 && n != 24) || n == 47 || n == 48) : false;
-}
+// (sparse_const_path: internal.h)
 
 template <int N>
 struct SparseParamsC {
@@ -53,9 +48,67 @@ struct SparseParamsC {
     SparseParams s;
 };
 
+// Shared-rows pair walk (round 2).  The T walk's Gray bit-0 column c (host-chosen: the T column with the fewest
+// nonzero rows, at most kSparsePairRows = M of them) is never added to the row sums v; the two terms of ranks
+// T, T+1 (T even) are prod v and prod (v + c), and the rows where c is zero give the SAME factor to both.  With
+// the rows ordered so that c's nonzero rows are the last M positions (host row permutation: per(PA) = per(A)),
+//     term(T+1) - term(T) = Z (prod_{i >= N-M} (v_i + c_i) - prod_{i >= N-M} v_i),   Z = prod_{i < N-M} v_i,
+// with the pair's sign s_T = +1 if bit 1 of T is 0, else -1 (Gray bit 0 of an even rank T is bit 1 of T; signs
+// (-1)^{r+1}, App. A).  Per pair: one column flip (2N DADD) + N + M - 2 complex multiplies + 2M + 2 DADD, i.e.
+// 3N + 3M - 3 FP64 instructions per term instead of 6N - 4 -- the same terms, summed as differences of pairs.
+template <class C, int T>
+struct InnerStepCS {
+    static constexpr int N = C::N;
+    static __device__ __forceinline__ void run(const WalkParamsC<N>& P, int z, double (&wr)[N], double (&wi)[N],
+                                               double zmid, double& ar, double& ai) {
+        constexpr int U = C::U, M = kSparsePairRows, Z0 = N - M;
+        static_assert(T % 2 == 0 && U >= 2 && Z0 >= 4, "pairs of an aligned block of >= 4 ranks");
+        if constexpr (T > 0) {
+            constexpr int J = ctz_c((unsigned)T);            // >= 1
+            const int jj = J + z * (T + 1);
+            if constexpr (J == U - 1) {
+                // the mid-block column with its sign by address (+a at col[U-1], -a at col[U]): DADD R, R, UR
+                const int jm = jj + (zmid < 0.0 ? 1 : 0);
+#pragma unroll
+                for (int i = 0; i < N; i++) {
+                    const double2 a = P.col[jm][i];
+                    wr[i] += a.x;
+                    wi[i] += a.y;
+                }
+            } else {
+                constexpr bool PLUS = ((T >> (J + 1)) & 1) == 0;
+#pragma unroll
+                for (int i = 0; i < N; i++) {
+                    const double2 a = P.col[jj][i];
+                    if (PLUS) { wr[i] += a.x; wi[i] += a.y; }
+                    else      { wr[i] -= a.x; wi[i] -= a.y; }
+                }
+            }
+        }
+        constexpr int SP = ((T >> 1) & 1) ? -1 : 1;
+        // Z in two chains; the M rows plain and shifted by c (two more chains)
+        double xr, xi, yr, yi;
+        chain<0, Z0 / 2, N>(wr, wi, xr, xi);
+        chain<Z0 / 2, Z0, N>(wr, wi, yr, yi);
+        const int j0 = z * (T + 2);                          // == 0: column c = T slot 0, per-use load
+        double pr = wr[Z0], pi = wi[Z0];
+        double qr = wr[Z0] + P.col[j0][Z0].x, qi = wi[Z0] + P.col[j0][Z0].y;
+#pragma unroll
+        for (int i = Z0 + 1; i < N; i++) {
+            const double2 c = P.col[j0][i];
+            cmul2(pr, pi, wr[i], wi[i]);
+            cmul2(qr, qi, wr[i] + c.x, wi[i] + c.y);
+        }
+        cmul2(yr, yi, qr - pr, qi - pi);
+        fused_acc<SP>(xr, xi, yr, yi, ar, ai);
+        if constexpr (T + 2 < (1 << U)) InnerStepCS<C, T + 2>::run(P, z, wr, wi, zmid, ar, ai);
+    }
+};
+
 // The walk of one aligned chunk c of the T walk (2^e ranks, e > U) from seeded row sums, inner columns
-// from the constant bank (as walk_chunk_const), block-boundary columns from shared memory.
-template <class C>
+// from the constant bank (as walk_chunk_const), block-boundary columns from shared memory.  PAIR: the
+// shared-rows pair walk (the seed never includes T slot 0: e > U >= 2).
+template <class C, bool PAIR>
 __device__ __forceinline__ void walk_seeded_cbank(const WalkParamsC<C::N>& Pw, uint32_t lc, uint64_t c, int e,
                                                  double (&wr)[C::N], double (&wi)[C::N], ddc& acc) {
     constexpr int N = C::N, U = C::U;
@@ -70,7 +123,8 @@ __device__ __forceinline__ void walk_seeded_cbank(const WalkParamsC<C::N>& Pw, u
             const uint64_t nb = (j + 1 < e) ? (uint64_t)((q >> (j + 1 - U)) & 1) : cpar;
             flip_add<N>(lc + (uint32_t)(j * N) * 16u + (nb ? C::NEG : 0u), wr, wi);
         }
-        InnerStepC<C, 0>::run(Pw, z, wr, wi, (q & 1) ? -1.0 : 1.0, ar, ai);
+        if constexpr (PAIR) InnerStepCS<C, 0>::run(Pw, z, wr, wi, (q & 1) ? -1.0 : 1.0, ar, ai);
+        else                InnerStepC<C, 0>::run(Pw, z, wr, wi, (q & 1) ? -1.0 : 1.0, ar, ai);
         if (((q + 1) & kFoldMask) == 0 || q + 1 == nblk) {
             acc.re = dd_add_d(acc.re, ar);
             acc.im = dd_add_d(acc.im, ai);
@@ -80,14 +134,14 @@ __device__ __forceinline__ void walk_seeded_cbank(const WalkParamsC<C::N>& Pw, u
     }
 }
 
-template <int N>
+template <int N, bool PAIR>
 __global__ void __launch_bounds__(walk_block_threads(N)) sparse_kernel_c(const __grid_constant__ SparseParamsC<N> PC) {
     using C = WCfg<N, 1>;
     const SparseParams& P = PC.s;
     extern __shared__ double2 smem[];
     for (int k = threadIdx.x; k < N * C::P; k += blockDim.x) {
         const int slot = k / C::P, i = k - slot * C::P;
-        const double2 a = (i < N) ? P.A[i * N + P.col[slot]] : make_double2(0.0, 0.0);
+        const double2 a = (i < N) ? P.A[P.row[i] * N + P.col[slot]] : make_double2(0.0, 0.0);
         smem[k] = a;
         smem[N * C::P + k] = make_double2(-a.x, -a.y);
     }
@@ -125,7 +179,7 @@ __global__ void __launch_bounds__(walk_block_threads(N)) sparse_kernel_c(const _
         const uint64_t x = ((c ^ (c >> 1)) << e) | ((c & 1ull) << (e - 1));
         for (int q = e - 1; q < P.nt; q++)
             flip_dyn<N>(lc + (uint32_t)(q * C::P) * 16u, (double)((x >> q) & 1ull), wr, wi);
-        walk_seeded_cbank<C>(PC.w, lc, c, e, wr, wi, part);
+        walk_seeded_cbank<C, PAIR>(PC.w, lc, c, e, wr, wi, part);
         if ((ssum & 1) == 0) {
             part.re.hi = -part.re.hi; part.re.lo = -part.re.lo;
             part.im.hi = -part.im.hi; part.im.lo = -part.im.lo;
@@ -156,7 +210,7 @@ __global__ void __launch_bounds__(WalkCfg<N>::NT, WalkCfg<N>::MINB) sparse_kerne
     // stage the permuted columns (slot k = column P.col[k]) and their negations, walk layout
     for (int k = threadIdx.x; k < N * C::P; k += blockDim.x) {
         const int slot = k / C::P, i = k - slot * C::P;
-        const double2 a = (i < N) ? P.A[i * N + P.col[slot]] : make_double2(0.0, 0.0);
+        const double2 a = (i < N) ? P.A[P.row[i] * N + P.col[slot]] : make_double2(0.0, 0.0);
         smem[k] = a;
         smem[N * C::P + k] = make_double2(-a.x, -a.y);
     }
@@ -264,6 +318,7 @@ cudaError_t sparse_launch_t(const SparseLaunch& L) {
     P.nt = L.nt;
     P.d = L.d;
     for (int k = 0; k < 64; k++) P.col[k] = k < N ? L.col[k] : 0;
+    for (int k = 0; k < 64; k++) P.row[k] = k < N ? L.row[k] : 0;
     for (int l = 0; l < kSparseMaxD; l++) {
         P.soff[l] = l < L.d ? L.soff[l] : 0;
         P.ssz[l] = l < L.d ? L.ssz[l] : 0;
@@ -272,13 +327,19 @@ cudaError_t sparse_launch_t(const SparseLaunch& L) {
         if (L.e > C::U) {
             SparseParamsC<N> PC;
             memset(&PC.w, 0, sizeof(PC.w));
-            for (int j = 0; j < WalkParamsC<N>::NC; j++)
-                for (int i = 0; i < N; i++) PC.w.col[j][i] = L.A_host[(size_t)i * N + L.col[j]];
+            constexpr int NC = WalkParamsC<N>::NC;
+            for (int j = 0; j < NC; j++)
+                for (int i = 0; i < N; i++) PC.w.col[j][i] = L.A_host[(size_t)L.row[i] * N + L.col[j]];
+            for (int i = 0; i < N; i++) {                // -a of the mid-block column (the pair walk's sign by address)
+                const double2 a = L.A_host[(size_t)L.row[i] * N + L.col[NC - 1]];
+                PC.w.col[NC][i] = make_double2(-a.x, -a.y);
+            }
             PC.s = P;
-            cudaError_t err = cudaFuncSetAttribute(sparse_kernel_c<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            auto kern = L.pair ? sparse_kernel_c<N, true> : sparse_kernel_c<N, false>;
+            cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                    (int)C::smem_bytes);
             if (err != cudaSuccess) return err;
-            sparse_kernel_c<N><<<L.grid, walk_block_threads(N), C::smem_bytes, L.stream>>>(PC);
+            kern<<<L.grid, walk_block_threads(N), C::smem_bytes, L.stream>>>(PC);
             return cudaGetLastError();
         }
     }
@@ -294,13 +355,13 @@ cudaError_t sparse_launch_t(const SparseLaunch& L) {
 template <int N>
 cudaError_t sparse_occupancy_t(int* blocks_per_sm) {
     if constexpr (sparse_const_path(N) && WCfg<N, 1>::U >= 1 && WalkParamsC<N>::MN == 0) {
-        cudaError_t err = cudaFuncSetAttribute(sparse_kernel_c<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t err = cudaFuncSetAttribute(sparse_kernel_c<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                (int)WCfg<N, 1>::smem_bytes);
         if (err != cudaSuccess) return err;
         err = cudaFuncSetAttribute(sparse_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)WalkCfg<N>::smem_bytes);
         if (err != cudaSuccess) return err;
-        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, sparse_kernel_c<N>, walk_block_threads(N),
+        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, sparse_kernel_c<N, false>, walk_block_threads(N),
                                                              WCfg<N, 1>::smem_bytes);
     }
     using C = WalkCfg<N>;
