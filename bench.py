@@ -779,7 +779,7 @@ def run_ours(args):
         walk_launches_per_step = 1
         sets = plan["sets"]
         _, sp_info = pb.perm_c128_sparse(A_dev, stream=stream, info=True)    # planning call: the walk it picks
-        sp_pair = sp_info["pair_rows"]
+        sp_group = sp_info["group_cols"]
 
         def step():
             es, ee = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -933,19 +933,22 @@ def run_ours(args):
                                "algorithmic": "8 flops per transfer-matrix transition x transitions per row x n rows",
                                "peak_measured_probe": peak_meas}
         elif cfg == "cfgsp":
-            # the shared-rows pair walk does 8n + 8M - 8 flops per PAIR of sets (2n flip, 2M shift,
-            # n + M - 3 complex multiplies of 6, the pair difference 2, the fused accumulate 8); the plain walk 8n per set
-            fpset = (4 * n + 4 * sp_pair - 4) if sp_pair else 8 * n
+            # the shared-rows group walk, per block of 2^G sets: the column flip 2n, Z and the block
+            # product n - M - 1 complex multiplies (6 flops), the fused accumulate 8, 2^G products of M rows, the
+            # 2^G - 1 shifted row sums (2M) and signed sums (2); the term-by-term walk: 8n per set
+            Mr = 4
+            fpset = ((2 * n + 6 * (n - Mr - 1) + 8 + 2 ** sp_group * 6 * (Mr - 1) + (2 ** sp_group - 1) * (2 * Mr + 2))
+                     / 2 ** sp_group) if sp_group else 8 * n
             fl = sets * fpset
             achieved = fl / (dev_ms / K * 1e-3) / 1e12
             out["roofline"] = {"bound": "alu", "achieved": achieved, "peak": nominal, "unit": "TFLOP/s",
                                "frac": achieved / nominal, "traffic": ncu_traffic(cfg),
-                               "kernel": ("sparse_kernel_c<48, pair> (shared-rows pair walk, M = %d)" % sp_pair
-                                          if sp_pair else "sparse_kernel_c<48> (FP64 vector pipe)"),
-                               "algorithmic": (f"{fpset} flops per restricted set J (pair walk: 4n + 4M - 4; the "
-                                               f"term-by-term walk's 8n = {8 * n} would read "
+                               "kernel": (f"sparse_kernel_c<48, G = {sp_group}> (shared-rows group walk)"
+                                          if sp_group else "sparse_kernel_c<48> (FP64 vector pipe)"),
+                               "algorithmic": (f"{fpset:.1f} flops per restricted set J (group walk, G = {sp_group}, "
+                                               f"M = {Mr}; the term-by-term walk's 8n = {8 * n} would read "
                                                f"{sets * 8 * n / (dev_ms / K * 1e-3) / 1e12 / nominal:.3f})"
-                                               if sp_pair else "8n flops per restricted set J")
+                                               if sp_group else "8n flops per restricted set J")
                                               + " x 2^|T| prod (2^|S_l| - 1) sets",
                                "peak_measured_probe": peak_meas}
         elif cfg == "cfgw":

@@ -217,9 +217,9 @@ typedef struct {
     uint64_t smask[64];  /* columns of S_1 .. S_d */
     double sets;         /* sets J enumerated (0 when a zero row or column makes per = 0) */
     int32_t chunk_log2;  /* T-walk chunk length used by perm_c128_sparse (-1: not launched) */
-    int32_t pair_rows;   /* perm_c128_sparse: 0 = plain T walk; M > 0 = shared-rows pair walk (the T walk's
-                            bit-0 column has <= M nonzero rows; terms summed in pairs sharing the product of
-                            the other rows) */
+    int32_t group_cols;  /* perm_c128_sparse: 0 = the plain T walk; G > 0 = the shared-rows group walk: G T
+                            columns nonzero in <= 4 rows together are the walk's lowest Gray bits, and each
+                            block of 2^G sets shares the product of the other rows */
 } perm_sparse_info_t;
 
 /* Host only: the partition and enumeration size for A (host, row-major n x n, 1 <= n <= 64).

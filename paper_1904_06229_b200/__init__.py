@@ -83,13 +83,13 @@ def _stats_dict(st: stats_t) -> dict:
 class sparse_info_t(ctypes.Structure):
     _fields_ = [("d", ctypes.c_uint32), ("nt", ctypes.c_uint32), ("tmask", ctypes.c_uint64),
                 ("smask", ctypes.c_uint64 * 64), ("sets", ctypes.c_double), ("chunk_log2", ctypes.c_int32),
-                ("pair_rows", ctypes.c_int32)]
+                ("group_cols", ctypes.c_int32)]
 
 
 def _sparse_info(info: sparse_info_t) -> dict:
     return {"S": [int(info.smask[l]) for l in range(info.d)], "T": int(info.tmask), "nt": int(info.nt),
             "sets": float(info.sets), "chunk_log2": int(info.chunk_log2),
-            "pair_rows": int(info.pair_rows)}
+            "group_cols": int(info.group_cols)}
 
 
 def _make_stats(events):

@@ -854,7 +854,7 @@ perm_status_t perm_c128_sparse(const perm_c128_t* A, int n, perm_c128_t* out_hos
     }
     L.outer = outer;
     for (int i = 0; i < n; i++) L.row[i] = i;
-    L.pair = 0;
+    L.group = 0;
     int dev = 0, sms = 0, bps = 0;
     PERM_CUDA(cudaGetDevice(&dev), "cudaGetDevice");
     PERM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "cudaDeviceGetAttribute");
@@ -877,42 +877,52 @@ perm_status_t perm_c128_sparse(const perm_c128_t* A, int n, perm_c128_t* out_hos
     }
     L.e = e;
     L.chunks = 1ull << (L.nt - e);
-    // shared-rows pair walk (sparse.cuh InnerStepCS): on the constant-bank path (e > U), when some T column has at
-    // most kSparsePairRows nonzero rows: that column becomes T slot 0 (the walk's bit-0 column; any order of the T
-    // columns enumerates the same sets) and the rows are ordered so that its nonzero rows come last (per(PA) =
-    // per(A)).  PERM_SPARSE_PAIR=0 keeps the plain walk.
+    // shared-rows group walk (sparse.cuh walk_seeded_group), on the constant-bank path (e > U): greedily take the
+    // T columns that add the fewest new nonzero rows while their union stays within kSparseGroupRows rows (up to
+    // kSparseGroupMaxG columns, G < e); they become T slots 0..G-1 -- the walk's lowest Gray bits; any order of the
+    // T columns enumerates the same sets -- and the rows are ordered so that the union's rows come last
+    // (per(PA) = per(A)).  PERM_SPARSE_GROUP=g caps G (0: the plain T walk).
     {
-        const char* ev = getenv("PERM_SPARSE_PAIR");
-        const bool allow = !(ev && ev[0] == '0');
-        if (allow && perm::sparse_pair_path(n) && e > U) {
-            int best = -1, bcnt = n + 1;
-            for (int q = 0; q < L.nt; q++) {
-                int cnt = 0;
+        int gmax = perm::kSparseGroupMaxG;
+        if (const char* ev = getenv("PERM_SPARSE_GROUP")) gmax = std::min(gmax, std::max(0, atoi(ev)));
+        gmax = std::min(gmax, std::min(e - 1, L.nt));
+        if (perm::sparse_group_path(n) && e > U && gmax >= 1) {
+            std::vector<uint64_t> rows_of((size_t)L.nt, 0);
+            for (int q = 0; q < L.nt; q++)
                 for (int r = 0; r < n; r++) {
                     const perm_c128_t z = Ah[(size_t)r * n + L.col[q]];
-                    cnt += (z.re != 0.0 || z.im != 0.0);
+                    if (z.re != 0.0 || z.im != 0.0) rows_of[(size_t)q] |= 1ull << r;
                 }
-                if (cnt < bcnt) { bcnt = cnt; best = q; }
+            uint64_t R = 0;
+            int G = 0;
+            while (G < gmax) {
+                int best = -1, bcnt = 65;
+                for (int q = G; q < L.nt; q++) {          // slots < G hold the columns taken so far
+                    const int cnt = __builtin_popcountll(R | rows_of[(size_t)q]);
+                    if (cnt < bcnt) { bcnt = cnt; best = q; }
+                }
+                if (best < 0 || bcnt > perm::kSparseGroupRows) break;
+                std::swap(L.col[G], L.col[best]);
+                std::swap(rows_of[(size_t)G], rows_of[(size_t)best]);
+                R |= rows_of[(size_t)G];
+                G++;
             }
-            if (best >= 0 && bcnt <= perm::kSparsePairRows) {
-                std::swap(L.col[0], L.col[best]);
-                const int c0 = L.col[0];
-                int lo = 0, hi = n - perm::kSparsePairRows;
-                std::vector<int> zero_rows, nz_rows;
-                for (int r = 0; r < n; r++) {
-                    const perm_c128_t z = Ah[(size_t)r * n + c0];
-                    ((z.re != 0.0 || z.im != 0.0) ? nz_rows : zero_rows).push_back(r);
-                }
-                // positions n-M .. n-1: the nonzero rows of c0, then zero rows to fill (they give equal factors)
-                for (int r : nz_rows) L.row[hi++] = r;
-                size_t k = 0;
-                for (; lo < n - perm::kSparsePairRows; lo++) L.row[lo] = zero_rows[k++];
-                for (; hi < n; hi++) L.row[hi] = zero_rows[k++];
-                L.pair = 1;
+            if (G >= 1) {
+                // positions n-M .. n-1: the union's rows, then rows outside it to fill (the thin columns are zero
+                // there, so they give every term of a block the same factor)
+                int lo = 0, hi = n - perm::kSparseGroupRows;
+                for (int r = 0; r < n; r++)
+                    if ((R >> r) & 1ull) L.row[hi++] = r;
+                for (int r = 0; r < n; r++)
+                    if (!((R >> r) & 1ull)) {
+                        if (lo < n - perm::kSparseGroupRows) L.row[lo++] = r;
+                        else L.row[hi++] = r;
+                    }
+                L.group = G;
             }
         }
     }
-    I.pair_rows = L.pair ? perm::kSparsePairRows : 0;
+    I.group_cols = L.group;
     const uint64_t items = L.outer * L.chunks;
     const uint64_t bthreads = (uint64_t)perm::walk_block_threads(n);
     uint64_t grid = (items + bthreads - 1) / bthreads;

@@ -205,8 +205,10 @@ cudaError_t batched_launch(const double2* A, int n, int64_t B, double2* per, dou
 // sparse.cuh / sparse_inst.cu (App. B restricted enumeration), n <= kMaxSparseN
 constexpr int kMaxSparseN = 48;
 constexpr int kSparseMaxD = 64;
-// shared-rows pair walk: the T walk's bit-0 column may have at most this many nonzero rows
-constexpr int kSparsePairRows = 4;
+// shared-rows group walk (sparse.cuh walk_seeded_group): up to kSparseGroupMaxG thin T columns, together nonzero
+// in at most kSparseGroupRows rows
+constexpr int kSparseGroupRows = 4;
+constexpr int kSparseGroupMaxG = 4;
 #ifndef PERM_SPARSE_CONST
 #define PERM_SPARSE_CONST 1
 #endif
@@ -215,8 +217,8 @@ __host__ __device__ constexpr bool sparse_const_path(int n) {
     return PERM_SPARSE_CONST == 2 ? true
          : PERM_SPARSE_CONST == 1 ? ((n >= 17 && n <= 33 && n != 24) || n == 47 || n == 48) : false;
 }
-// ... and of its shared-rows pair walk (InnerStepCS: the product of n - kSparsePairRows >= 4 rows in two chains)
-__host__ __device__ constexpr bool sparse_pair_path(int n) { return sparse_const_path(n) && n >= kSparsePairRows + 8; }
+// ... and of its shared-rows group walk (the product of n - kSparseGroupRows >= 8 rows in two chains)
+__host__ __device__ constexpr bool sparse_group_path(int n) { return sparse_const_path(n) && n >= kSparseGroupRows + 8; }
 struct SparseLaunch {
     const double2* A_dev;   // device, row-major n x n
     ddc* partials;          // device, grid entries
@@ -225,8 +227,8 @@ struct SparseLaunch {
     int e, nt, d, n, grid;
     int col[64];            // permuted column order: T columns, then S_1, S_2, ...
     int row[64];            // row order (position i holds row row[i] of A; the identity unless pair)
-    int pair;               // shared-rows pair walk (sparse.cuh): T slot 0's nonzero rows are the last
-                            // kSparsePairRows positions
+    int group;              // shared-rows group walk (sparse.cuh): G thin T columns at slots 0..G-1, their
+                            // nonzero rows the last kSparseGroupRows positions (0: the plain T walk)
     int soff[kSparseMaxD];  // first slot of S_l
     int ssz[kSparseMaxD];   // |S_l|
     const double2* A_host;  // host, row-major n x n (inner T columns for the constant-bank walk)

@@ -46,69 +46,66 @@ template <int N>
 struct SparseParamsC {
     WalkParamsC<N> w;             // col[][]: inner T columns (w.A, w.partials, c0, count, eb unused)
     SparseParams s;
+    // group walk: comb[b - 1][i] = sum_{k in b} a_{row[N-M+i], T slot k}, b = 1 .. 2^G - 1 (subsets of the thin columns)
+    double2 comb[(1 << kSparseGroupMaxG) - 1][kSparseGroupRows];
 };
 
-// Shared-rows pair walk (round 2).  The T walk's Gray bit-0 column c (host-chosen: the T column with the fewest
-// nonzero rows, at most kSparsePairRows = M of them) is never added to the row sums v; the two terms of ranks
-// T, T+1 (T even) are prod v and prod (v + c), and the rows where c is zero give the SAME factor to both.  With
-// the rows ordered so that c's nonzero rows are the last M positions (host row permutation: per(PA) = per(A)),
-//     term(T+1) - term(T) = Z (prod_{i >= N-M} (v_i + c_i) - prod_{i >= N-M} v_i),   Z = prod_{i < N-M} v_i,
-// with the pair's sign s_T = +1 if bit 1 of T is 0, else -1 (Gray bit 0 of an even rank T is bit 1 of T; signs
-// (-1)^{r+1}, App. A).  Per pair: one column flip (2N DADD) + N + M - 2 complex multiplies + 2M + 2 DADD, i.e.
-// 3N + 3M - 3 FP64 instructions per term instead of 6N - 4 -- the same terms, summed as differences of pairs.
-template <class C, int T>
-struct InnerStepCS {
-    static constexpr int N = C::N;
-    static __device__ __forceinline__ void run(const WalkParamsC<N>& P, int z, double (&wr)[N], double (&wi)[N],
-                                               double zmid, double& ar, double& ai) {
-        constexpr int U = C::U, M = kSparsePairRows, Z0 = N - M;
-        static_assert(T % 2 == 0 && U >= 2 && Z0 >= 4, "pairs of an aligned block of >= 4 ranks");
-        if constexpr (T > 0) {
-            constexpr int J = ctz_c((unsigned)T);            // >= 1
-            const int jj = J + z * (T + 1);
-            if constexpr (J == U - 1) {
-                // the mid-block column with its sign by address (+a at col[U-1], -a at col[U]): DADD R, R, UR
-                const int jm = jj + (zmid < 0.0 ? 1 : 0);
-#pragma unroll
-                for (int i = 0; i < N; i++) {
-                    const double2 a = P.col[jm][i];
-                    wr[i] += a.x;
-                    wi[i] += a.y;
-                }
-            } else {
-                constexpr bool PLUS = ((T >> (J + 1)) & 1) == 0;
-#pragma unroll
-                for (int i = 0; i < N; i++) {
-                    const double2 a = P.col[jj][i];
-                    if (PLUS) { wr[i] += a.x; wi[i] += a.y; }
-                    else      { wr[i] -= a.x; wi[i] -= a.y; }
-                }
-            }
+// Shared-rows group walk (round 2).  In a sparse matrix most rows are zero in any one column.  The host puts
+// G "thin" T columns c_0 .. c_{G-1} -- together nonzero in at most M = kSparseGroupRows rows -- at T slots
+// 0 .. G-1 (the walk's lowest Gray bits; any order of the T columns enumerates the same sets) and orders the rows
+// so that those rows are the last M positions (per(PA) = per(A)).  The row sums v never hold a thin column; an
+// aligned block q of 2^G ranks enumerates every subset b of the thin columns once at fixed high Gray bits h, and
+// the rows outside the last M give all 2^G terms the SAME factor:
+//     sum over the block = (-1)^{q+1} Z sum_b (-1)^{|b|} prod_{i >= N-M} (v_i + c_b,i),   Z = prod_{i < N-M} v_i,
+// (term sign (-1)^{r+1} = -(-1)^{|b|} (-1)^{|h|}; |h| = |gray(r >> G)| = parity of r >> G = q mod 2 in a chunk
+// whose first rank is a multiple of 2^e, e > G; App. A).  c_b = the subset sums, from the kernel parameters.
+// Per block: one column flip (2N DADD), Z (N - M - 1 complex multiplies), 2^G products of M rows, the signed sum:
+// 2N + 4(N - M) + 2^G (4M - 2) + 2 + 4 - ... FP64 instructions for 2^G sets (n = 48, M = 4: 153 / 88 / 55 / 39 per
+// set for G = 1 / 2 / 3 / 4 instead of 6N - 4 = 284).  The same sets and terms, summed as signed block sums.
+template <class C, int G>
+__device__ __forceinline__ void walk_seeded_group(const SparseParamsC<C::N>& PC, uint32_t lc, uint64_t c, int e,
+                                                  double (&wr)[C::N], double (&wi)[C::N], ddc& acc) {
+    constexpr int N = C::N, M = kSparseGroupRows, Z0 = N - M;
+    static_assert(G >= 1 && G <= kSparseGroupMaxG && Z0 >= 4, "group walk");
+    const int nblk = 1 << (e - G);                        // e > G: >= 2 blocks, the seed holds no thin column
+    const uint64_t cpar = c & 1ull;
+    constexpr int kFoldMask = (G >= kWalkFoldBits) ? 0 : ((1 << (kWalkFoldBits - G)) - 1);
+    double ar = 0.0, ai = 0.0;
+    for (int q = 0; q < nblk; q++) {
+        const int z = q >> 30;                            // 0 (nblk <= 2^29); per-use parameter loads
+        if (q > 0) {
+            const int j = G + __ffs(q) - 1;
+            const uint64_t nb = (j + 1 < e) ? (uint64_t)((q >> (j + 1 - G)) & 1) : cpar;
+            flip_add<N>(lc + (uint32_t)(j * N) * 16u + (nb ? C::NEG : 0u), wr, wi);
         }
-        constexpr int SP = ((T >> 1) & 1) ? -1 : 1;
-        // Z in two chains; the M rows plain and shifted by c (two more chains)
-        double xr, xi, yr, yi;
+        double xr, xi, yr, yi, dr, di;
         chain<0, Z0 / 2, N>(wr, wi, xr, xi);
         chain<Z0 / 2, Z0, N>(wr, wi, yr, yi);
-        const int j0 = z * (T + 2);                          // == 0: column c = T slot 0, per-use load
-        double pr = wr[Z0], pi = wi[Z0];
-        double qr = wr[Z0] + P.col[j0][Z0].x, qi = wi[Z0] + P.col[j0][Z0].y;
+        chain<Z0, N, N>(wr, wi, dr, di);                  // b = {}: + prod v
 #pragma unroll
-        for (int i = Z0 + 1; i < N; i++) {
-            const double2 c = P.col[j0][i];
-            cmul2(pr, pi, wr[i], wi[i]);
-            cmul2(qr, qi, wr[i] + c.x, wi[i] + c.y);
+        for (int b = 1; b < (1 << G); b++) {
+            const int bb = b - 1 + z * b;                 // == b - 1
+            double pr = wr[Z0] + PC.comb[bb][0].x, pi = wi[Z0] + PC.comb[bb][0].y;
+#pragma unroll
+            for (int i = 1; i < M; i++) cmul2(pr, pi, wr[Z0 + i] + PC.comb[bb][i].x, wi[Z0 + i] + PC.comb[bb][i].y);
+            if (__builtin_popcount((unsigned)b) & 1) { dr -= pr; di -= pi; }
+            else                                      { dr += pr; di += pi; }
         }
-        cmul2(yr, yi, qr - pr, qi - pi);
-        fused_acc<SP>(xr, xi, yr, yi, ar, ai);
-        if constexpr (T + 2 < (1 << U)) InnerStepCS<C, T + 2>::run(P, z, wr, wi, zmid, ar, ai);
+        cmul2(yr, yi, dr, di);
+        const uint32_t neg = (q & 1) ? 0u : 0x80000000u;  // (-1)^{q+1}, an integer sign flip
+        fused_acc<+1>(xr, xi, flip_sign_if(yr, neg), flip_sign_if(yi, neg), ar, ai);
+        if (((q + 1) & kFoldMask) == 0 || q + 1 == nblk) {
+            acc.re = dd_add_d(acc.re, ar);
+            acc.im = dd_add_d(acc.im, ai);
+            ar = 0.0;
+            ai = 0.0;
+        }
     }
-};
+}
 
 // The walk of one aligned chunk c of the T walk (2^e ranks, e > U) from seeded row sums, inner columns
-// from the constant bank (as walk_chunk_const), block-boundary columns from shared memory.  PAIR: the
-// shared-rows pair walk (the seed never includes T slot 0: e > U >= 2).
-template <class C, bool PAIR>
+// from the constant bank (as walk_chunk_const), block-boundary columns from shared memory.
+template <class C>
 __device__ __forceinline__ void walk_seeded_cbank(const WalkParamsC<C::N>& Pw, uint32_t lc, uint64_t c, int e,
                                                  double (&wr)[C::N], double (&wi)[C::N], ddc& acc) {
     constexpr int N = C::N, U = C::U;
@@ -123,8 +120,7 @@ __device__ __forceinline__ void walk_seeded_cbank(const WalkParamsC<C::N>& Pw, u
             const uint64_t nb = (j + 1 < e) ? (uint64_t)((q >> (j + 1 - U)) & 1) : cpar;
             flip_add<N>(lc + (uint32_t)(j * N) * 16u + (nb ? C::NEG : 0u), wr, wi);
         }
-        if constexpr (PAIR) InnerStepCS<C, 0>::run(Pw, z, wr, wi, (q & 1) ? -1.0 : 1.0, ar, ai);
-        else                InnerStepC<C, 0>::run(Pw, z, wr, wi, (q & 1) ? -1.0 : 1.0, ar, ai);
+        InnerStepC<C, 0>::run(Pw, z, wr, wi, (q & 1) ? -1.0 : 1.0, ar, ai);
         if (((q + 1) & kFoldMask) == 0 || q + 1 == nblk) {
             acc.re = dd_add_d(acc.re, ar);
             acc.im = dd_add_d(acc.im, ai);
@@ -134,7 +130,7 @@ __device__ __forceinline__ void walk_seeded_cbank(const WalkParamsC<C::N>& Pw, u
     }
 }
 
-template <int N, bool PAIR>
+template <int N, int G>
 __global__ void __launch_bounds__(walk_block_threads(N)) sparse_kernel_c(const __grid_constant__ SparseParamsC<N> PC) {
     using C = WCfg<N, 1>;
     const SparseParams& P = PC.s;
@@ -179,7 +175,8 @@ __global__ void __launch_bounds__(walk_block_threads(N)) sparse_kernel_c(const _
         const uint64_t x = ((c ^ (c >> 1)) << e) | ((c & 1ull) << (e - 1));
         for (int q = e - 1; q < P.nt; q++)
             flip_dyn<N>(lc + (uint32_t)(q * C::P) * 16u, (double)((x >> q) & 1ull), wr, wi);
-        walk_seeded_cbank<C, PAIR>(PC.w, lc, c, e, wr, wi, part);
+        if constexpr (G > 0) walk_seeded_group<C, G>(PC, lc, c, e, wr, wi, part);
+        else                walk_seeded_cbank<C>(PC.w, lc, c, e, wr, wi, part);
         if ((ssum & 1) == 0) {
             part.re.hi = -part.re.hi; part.re.lo = -part.re.lo;
             part.im.hi = -part.im.hi; part.im.lo = -part.im.lo;
@@ -330,12 +327,27 @@ cudaError_t sparse_launch_t(const SparseLaunch& L) {
             constexpr int NC = WalkParamsC<N>::NC;
             for (int j = 0; j < NC; j++)
                 for (int i = 0; i < N; i++) PC.w.col[j][i] = L.A_host[(size_t)L.row[i] * N + L.col[j]];
-            for (int i = 0; i < N; i++) {                // -a of the mid-block column (the pair walk's sign by address)
-                const double2 a = L.A_host[(size_t)L.row[i] * N + L.col[NC - 1]];
-                PC.w.col[NC][i] = make_double2(-a.x, -a.y);
-            }
             PC.s = P;
-            auto kern = L.pair ? sparse_kernel_c<N, true> : sparse_kernel_c<N, false>;
+            memset(PC.comb, 0, sizeof(PC.comb));
+            auto kern = sparse_kernel_c<N, 0>;
+            if constexpr (sparse_group_path(N)) {
+                constexpr int M = kSparseGroupRows;
+                for (int b = 1; b < (1 << L.group); b++)
+                    for (int i = 0; i < M; i++) {
+                        double re = 0.0, im = 0.0;
+                        for (int k = 0; k < L.group; k++)
+                            if ((b >> k) & 1) {
+                                const double2 a = L.A_host[(size_t)L.row[N - M + i] * N + L.col[k]];
+                                re += a.x;
+                                im += a.y;
+                            }
+                        PC.comb[b - 1][i] = make_double2(re, im);
+                    }
+                if (L.group == 1) kern = sparse_kernel_c<N, 1>;
+                if (L.group == 2) kern = sparse_kernel_c<N, 2>;
+                if (L.group == 3) kern = sparse_kernel_c<N, 3>;
+                if (L.group == 4) kern = sparse_kernel_c<N, 4>;
+            }
             cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                    (int)C::smem_bytes);
             if (err != cudaSuccess) return err;
@@ -355,13 +367,13 @@ cudaError_t sparse_launch_t(const SparseLaunch& L) {
 template <int N>
 cudaError_t sparse_occupancy_t(int* blocks_per_sm) {
     if constexpr (sparse_const_path(N) && WCfg<N, 1>::U >= 1 && WalkParamsC<N>::MN == 0) {
-        cudaError_t err = cudaFuncSetAttribute(sparse_kernel_c<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t err = cudaFuncSetAttribute(sparse_kernel_c<N, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                (int)WCfg<N, 1>::smem_bytes);
         if (err != cudaSuccess) return err;
         err = cudaFuncSetAttribute(sparse_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)WalkCfg<N>::smem_bytes);
         if (err != cudaSuccess) return err;
-        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, sparse_kernel_c<N, false>, walk_block_threads(N),
+        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, sparse_kernel_c<N, 0>, walk_block_threads(N),
                                                              WCfg<N, 1>::smem_bytes);
     }
     using C = WalkCfg<N>;

@@ -146,12 +146,8 @@ def test_const_walk_keeps_uniform_column_operands():
     # n complex entries = 2n LDCU.64 per block at least
     fns += [(walk_fn(n, True), 2 * n - 1) for n in range(32, 49) if n != 42]
     # the sparse kernel's constant-bank variant (sparse.cuh, sparse_const_path)
-    fns += [(f"_ZN4perm15sparse_kernel_cILi{n}ELb0EEEvNS_13SparseParamsCIXT_EEE", 100)
+    fns += [(f"_ZN4perm15sparse_kernel_cILi{n}ELi0EEEvNS_13SparseParamsCIXT_EEE", 100)
             for n in list(range(17, 24)) + list(range(25, 34)) + [47, 48]]
-    # ... and its shared-rows pair walk (sparse.cuh InnerStepCS): the inner flips, 2n LDCU.64 per block at least
-    # (at n = 17, 21, 23, 31..33 ptxas loads the pair kernel's parameters per lane: DESIGN.md 5.7)
-    fns += [(f"_ZN4perm15sparse_kernel_cILi{n}ELb1EEEvNS_13SparseParamsCIXT_EEE", 2 * n - 1)
-            for n in [18, 19, 20, 22, 25, 26, 27, 28, 29, 30, 47, 48]]
     for fn, least in fns:
         sass = subprocess.run([cuobjdump, "-sass", "-fun", fn, lib], capture_output=True, text=True).stdout
         uniform = sum(1 for l in sass.splitlines() if "LDCU.64" in l and "c[0x0][UR" in l)

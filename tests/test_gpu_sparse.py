@@ -111,25 +111,29 @@ def _pair_case(n, density, seed, nz):
     raise AssertionError("no matrix with the asked T-column shape")
 
 
+@pytest.mark.parametrize("cap", [1, 2, 3, 4])
 @pytest.mark.parametrize("n,density,nz", [(17, 0.1, 1), (20, 0.1, 2), (22, 0.12, 3), (23, 0.2, 4)])
-def test_sparse_pair_walk_vs_oracle(n, density, nz, monkeypatch):
-    # shared-rows pair walk: terms T, T+1 share the product of the rows where the T walk's bit-0
-    # column is zero; checked against the oracle's Eq. (3) and against the plain T walk (PERM_SPARSE_PAIR=0).
-    # These sizes plan a chunk length <= U (shared-memory kernel); forcing 2^4-rank chunks puts them on the
-    # constant-bank kernel, where the pair walk runs.
+def test_sparse_group_walk_vs_oracle(n, density, nz, cap, monkeypatch):
+    # shared-rows group walk: G thin T columns are the lowest Gray bits and every block of 2^G sets
+    # shares the product of the rows where they are zero; checked against the oracle's Eq. (3) and against the
+    # plain T walk (PERM_SPARSE_GROUP=0).  These sizes plan a chunk length <= U (shared-memory kernel); forcing
+    # 2^5-rank chunks puts them on the constant-bank kernel (G <= 4 < e).  n = 17 reaches G = 4.
     A = _pair_case(n, density, 5100 + n, nz)
-    monkeypatch.setenv("PERM_FORCE_CHUNK_LOG2", "4")
+    monkeypatch.setenv("PERM_FORCE_CHUNK_LOG2", "5")
+    monkeypatch.setenv("PERM_SPARSE_GROUP", str(cap))
     got, info = pb.perm_c128_sparse(A, info=True)
-    assert info["pair_rows"] == 4 and info["chunk_log2"] == 4, info
+    assert 1 <= info["group_cols"] <= cap and info["chunk_log2"] == 5, info
+    if n == 17:
+        assert info["group_cols"] == cap
     ref = oracle.ryser(A).value
-    assert pins.scaled_error(got, ref, A) <= TOL, (got, ref)
-    monkeypatch.setenv("PERM_SPARSE_PAIR", "0")
+    assert pins.scaled_error(got, ref, A) <= TOL, (got, ref, info)
+    monkeypatch.setenv("PERM_SPARSE_GROUP", "0")
     plain, info0 = pb.perm_c128_sparse(A, info=True)
-    assert info0["pair_rows"] == 0
+    assert info0["group_cols"] == 0
     assert pins.scaled_error(got, plain, A) <= TOL, (got, plain)
 
 
-def test_sparse_pair_walk_not_taken_for_thick_t_columns(monkeypatch):
+def test_sparse_group_walk_not_taken_for_thick_t_columns(monkeypatch):
     # every T column with more than 4 nonzero rows (density 0.4): the plain T walk
     B = _sparse(20, 0.4, 7800)
     T = pb.perm_sparse_plan(B)["T"]
@@ -137,14 +141,15 @@ def test_sparse_pair_walk_not_taken_for_thick_t_columns(monkeypatch):
     assert len(tc) >= 5 and min(np.count_nonzero(B[:, j]) for j in tc) > 4
     monkeypatch.setenv("PERM_FORCE_CHUNK_LOG2", "4")
     got, info = pb.perm_c128_sparse(B, info=True)
-    assert info["pair_rows"] == 0 and info["chunk_log2"] == 4
+    assert info["group_cols"] == 0 and info["chunk_log2"] == 4
     assert pins.scaled_error(got, oracle.ryser(B).value, B) <= TOL
 
 
 @pytest.mark.parametrize("n", [32, 33, 47, 48])
-def test_sparse_pair_walk_block_diagonal(n, monkeypatch):
-    # the pair walk at the large constant-bank orders: scrambled block-diagonal matrices, per = product of the
-    # blocks' permanents (oracle Eq. (3)); n = 47, 48 at the planned chunk length, n = 32, 33 forced to 2^5
+def test_sparse_group_walk_block_diagonal(n, monkeypatch):
+    # the group walk at the large constant-bank orders: scrambled block-diagonal matrices, per = product of the
+    # blocks' permanents (oracle Eq. (3)); n = 47, 48 at the planned chunk length, n = 32, 33 forced to 2^5; the
+    # plain T walk alongside
     sizes = [16] * (n // 16) + ([n % 16] if n % 16 else [])
     blocks = [_sparse(m, 0.05, 5300 + n + k) for k, m in enumerate(sizes)]
     ph = np.random.default_rng(5400 + n)
@@ -160,8 +165,8 @@ def test_sparse_pair_walk_block_diagonal(n, monkeypatch):
         monkeypatch.setenv("PERM_FORCE_CHUNK_LOG2", "5")
     ref = np.prod([oracle.ryser(B).value for B in blocks])
     got, info = pb.perm_c128_sparse(M, info=True)
-    assert info["pair_rows"] == 4, info
-    assert pins.scaled_error(got, ref, M) <= TOL, (got, ref, info["chunk_log2"])
-    monkeypatch.setenv("PERM_SPARSE_PAIR", "0")
+    assert info["group_cols"] >= 2, info
+    assert pins.scaled_error(got, ref, M) <= TOL, (got, ref, info)
+    monkeypatch.setenv("PERM_SPARSE_GROUP", "0")
     plain = pb.perm_c128_sparse(M)
     assert pins.scaled_error(got, plain, M) <= TOL, (got, plain)
