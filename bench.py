@@ -1022,8 +1022,10 @@ def run_reference(args):
         oracle_rate_cfg(cfg, seconds=1.0)
     rates, samples = [], []
     t0 = time.perf_counter()
+    # each step is a bounded sample; its length shrinks with K so that the whole arm ends within a few minutes
+    per_step = min(args.cpu_seconds, max(1.5, 150.0 / max(1, args.steps)))
     for _ in range(args.steps):
-        r = oracle_rate_cfg(cfg, seconds=args.cpu_seconds)
+        r = oracle_rate_cfg(cfg, seconds=per_step)
         rates.append(r["value"])
         samples.append(r)
     wall = time.perf_counter() - t0

@@ -118,6 +118,66 @@ def sharded_permanent_range(A, group=None, *, workspace=None, stream=None, parti
     return combine(gathered.cpu().numpy(), n)
 
 
+def _matrix_digest(A) -> str:
+    import hashlib
+    a = A.detach().cpu().numpy() if hasattr(A, "detach") else np.asarray(A)
+    return hashlib.sha256(np.ascontiguousarray(a, dtype=np.complex128).tobytes()).hexdigest()
+
+
+def checkpointed_permanent(A, path: str, steps: int, *, world: int = 1, rank: int = 0, max_steps: int | None = None,
+                           wave: int | None = None, stream=None, return_dd: bool = False):
+    """per(A) of one long permanent walked as ``steps`` slices of this rank's chunk span, the tree nodes of every
+    finished slice kept in the checkpoint file ``path`` ("per-chunk partials are naturally
+    checkpointable"; P:202-206 stores the partial sums before the final summation).  A later call with the
+    same matrix, steps, world and rank resumes after the last finished slice; a file written for another
+    matrix or slicing is refused.  ``max_steps`` stops after that many slices of this call (returns None):
+    the hook the tests use to interrupt a run; ``wave``: chunks per slicing round (default: the resident chunk
+    walkers of one launch, so every slice is whole rounds; every slice must be non-empty).  With world = 1 the value returned after the last slice has
+    the bits of perm_c128(A) (the chunk tree does not depend on the slicing); with world > 1 it returns this
+    rank's node array (done, 128, 6) for the caller to gather and pass to combine_nodes.  Host logic only."""
+    import os
+    import torch
+
+    n = A.shape[0]
+    b = chunk_log2(n)
+    c0, c1 = chunk_span(n, world, rank, b)
+    if wave is None:
+        from . import chunk_walkers
+        wave = chunk_walkers(n, b)
+    slices = step_slices(c0, c1, steps, wave)
+    if any(s1 <= s0 for s0, s1 in slices):
+        raise ValueError("more steps than rounds of chunks: an empty slice")
+    key = np.array([n, b, c0, c1, steps, world, rank, wave], dtype=np.int64)
+    digest = _matrix_digest(A)
+    done = 0
+    saved = np.zeros((0, TREE_MAX_NODES, 6), dtype=np.int64)
+    if os.path.exists(path):
+        with np.load(path) as f:
+            if str(f["digest"]) != digest or not np.array_equal(f["key"], key):
+                raise ValueError("checkpoint belongs to another matrix or slicing")
+            saved = np.array(f["nodes"], dtype=np.int64).reshape(-1, TREE_MAX_NODES, 6)
+            done = saved.shape[0]
+            if done > steps:
+                raise ValueError("checkpoint holds more slices than the run has")
+    ran = 0
+    for s in range(done, steps):
+        if max_steps is not None and ran >= max_steps:
+            return None
+        s0, s1 = slices[s]
+        parts = perm_c128_chunks(A, s0, s1, stream=stream)
+        nodes = perm_c128_tree(parts, s0, s1, stream=stream)
+        if stream is not None:
+            stream.synchronize()
+        saved = np.concatenate([saved, nodes.cpu().numpy().reshape(1, TREE_MAX_NODES, 6)])
+        tmp = path + ".tmp.npz"
+        np.savez(tmp, digest=np.array(digest), key=key, nodes=saved)
+        os.replace(tmp, path)                       # a slice is either wholly in the file or not at all
+        ran += 1
+    if world > 1:
+        return saved
+    return combine_nodes(saved.reshape(-1, 6), n, return_dd=return_dd)
+
+
 def int01_rank_space(n: int) -> int:
     """Ranks of perm_int01's walk: 2^{n-1} (half-range Glynn, n <= 28) or 2^n (Eq. (3), 29 <= n <= 33)."""
     return 1 << (n if n > 28 else n - 1)
@@ -160,5 +220,5 @@ def sharded_int01(A, group=None, *, stream=None) -> int:
 
 
 __all__ = ["rank_span", "chunk_span", "step_slices", "combine_nodes", "combine", "sharded_permanent",
-           "sharded_permanent_range", "int01_rank_space", "pack_i128", "combine_int01",
+           "sharded_permanent_range", "checkpointed_permanent", "int01_rank_space", "pack_i128", "combine_int01",
            "sharded_int01", "DD"]

@@ -131,3 +131,23 @@ def test_step_slices_whole_rounds(c0, c1, steps, wave):
     rounds = -(-(c1 - c0) // wave)
     per = [-(-(a1 - a0) // wave) for a0, a1 in sl]
     assert sum(per) == rounds and max(per) - min(per) <= 1
+
+
+def test_checkpoint_of_another_matrix_or_slicing_is_refused_before_any_walk(tmp_path):
+    """shard.checkpointed_permanent validates the file (matrix digest, slicing key) on the host before the
+    first library call that needs a device."""
+    rng = np.random.default_rng(5)
+    A = rng.standard_normal((30, 30)) + 1j * rng.standard_normal((30, 30))
+    b = pb.chunk_log2(30)
+    c0, c1 = shard.chunk_span(30, 1, 0, b)
+    key = np.array([30, b, c0, c1, 4, 1, 0, 4096], dtype=np.int64)
+    path = str(tmp_path / "ck.npz")
+    np.savez(path, digest=np.array("0" * 64), key=key, nodes=np.zeros((1, pb.TREE_MAX_NODES, 6), dtype=np.int64))
+    with pytest.raises(ValueError, match="another matrix"):
+        shard.checkpointed_permanent(A, path, 4, wave=4096)
+    np.savez(path, digest=np.array(shard._matrix_digest(A)), key=key,
+             nodes=np.zeros((1, pb.TREE_MAX_NODES, 6), dtype=np.int64))
+    with pytest.raises(ValueError, match="another matrix or slicing"):
+        shard.checkpointed_permanent(A, path, 3, wave=4096)
+    with pytest.raises(ValueError, match="empty slice"):
+        shard.checkpointed_permanent(A, str(tmp_path / "none.npz"), 4, wave=1 << 30)
